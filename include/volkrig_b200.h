@@ -1,0 +1,157 @@
+/*
+ * volkrig-b200 -- C ABI of the B200-native kriging interpolation path.
+ *
+ * Drop-in boundary for the reference's Python entry points (paths relative to
+ * /root/reference/pkg/src/volkrig):
+ *
+ *   fill_missing(grid, model, drift="linear", return_variance=False)
+ *       kriging.py:458-496 (plane-structured branch kriging.py:499-557)
+ *       -> vk_grid_scan + vk_plan_create(fit_variogram = 0)
+ *          + vk_plan_execute(models = the caller's model) + vk_plan_finish
+ *   fit_variogram(samples, kind="exponential", n_bins=15,
+ *                 max_pairs=100_000, seed=0)
+ *       kriging.py:264-328
+ *       -> vk_fit_variogram_samples
+ *   reconstruct_block's kriging half over Z sub-parts (the
+ *   absent block_pipeline): per-part fit_variogram then
+ *   fill_missing, merged by dropping each part's trailing halo plane
+ *       -> vk_plan_create(fit_variogram = 1, n_subparts = S)
+ *          + vk_plan_execute(models = NULL) + vk_plan_finish
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Volumes are float32
+ * [z][y][x] C-order (model.py:5-9); device pointers are CUDA global memory of
+ * the current device; every call that takes a stream is stream-ordered and
+ * asynchronous; errors detected on the device surface at vk_plan_finish.
+ * The library never frees caller memory; a plan owns its own workspace.
+ * Plans are not thread-safe; use one plan per thread/stream.
+ */
+#ifndef VOLKRIG_B200_H
+#define VOLKRIG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VK_ABI_VERSION 1
+
+/* Status codes; the Python layer maps them to the reference's exception
+ * classes (errors.py:54-67). */
+typedef enum {
+  VK_OK = 0,
+  VK_E_INVALID_ARGUMENT = 1,    /* ValueError                        */
+  VK_E_NO_KNOWN_NEIGHBORS = 2,  /* NoKnownNeighbors  kriging.py:477,513 */
+  VK_E_SINGULAR_SYSTEM = 3,     /* SingularSystem    kriging.py:232,236 */
+  VK_E_INSUFFICIENT_SAMPLES = 4,/* InsufficientSamples kriging.py:275   */
+  VK_E_DEGENERATE_LAGS = 5,     /* DegenerateLags    kriging.py:291     */
+  VK_E_UNSUPPORTED = 6,         /* layout outside the device path      */
+  VK_E_CUDA = 7,                /* CUDA runtime failure                */
+  VK_E_INVALID_GRID = 8,        /* validate(): mask/NaN out of sync (model.py:111-117) */
+  VK_E_FIT_FAILED = 9           /* least_squares raised (scipy ValueError) */
+} vk_status;
+
+enum { VK_KIND_EXPONENTIAL = 0, VK_KIND_GAUSSIAN = 1, VK_KIND_SPHERICAL = 2 };
+enum { VK_DRIFT_LINEAR = 0, VK_DRIFT_CONSTANT = 1 };
+enum { VK_ACCUM_FP64 = 0, VK_ACCUM_FP32 = 1 };
+
+typedef struct vk_plan vk_plan;
+
+typedef struct {
+  int32_t height;          /* dy                                          */
+  int32_t width;           /* dx                                          */
+  int32_t depth;           /* dz of the output grid                       */
+  int32_t n_known;         /* K known planes                              */
+  const int32_t* known_z;  /* host [K], strictly increasing, in [0,depth) */
+  int32_t n_subparts;      /* S >= 1 Z sub-parts (1: whole grid)          */
+  int32_t kind;            /* VK_KIND_*                                   */
+  int32_t drift;           /* VK_DRIFT_*                                  */
+  int32_t accum;           /* VK_ACCUM_* prediction accumulation          */
+  int32_t n_bins;          /* 15 (kriging.py:264)                         */
+  int64_t max_pairs;       /* 100000                                      */
+  uint64_t seed;           /* 0                                           */
+  int32_t fit_variogram;   /* 1: per-part device fit; 0: models supplied  */
+  int32_t flags;           /* VK_FLAG_*                                   */
+} vk_plan_desc;
+
+#define VK_FLAG_FORCE_GENERIC 1   /* disable the streaming fast kernel (testing) */
+
+/* Replaces: the window/stencil setup of fill_missing (kriging.py:485-515)
+ * and the partition of SPEC.md:392-400.  Host-side, O(K + H + W). */
+int vk_plan_create(const vk_plan_desc* desc, vk_plan** out);
+
+void vk_plan_destroy(vk_plan* plan);
+
+/* Replaces: fill_missing / the per-part reconstruct_block kriging chain.
+ *   known   device f32 [K][H][W]  (the known planes, in known_z order)
+ *   models  host f64 [S][3] (nugget, sill, range_len) when fit_variogram==0,
+ *           else NULL
+ *   out     device f32 [depth][H][W]  (known planes copied bit-exactly)
+ *   var     device f64 [depth][H][W] kriging variance or NULL
+ *           (return_variance, kriging.py:482, 492-496)
+ *   stream  cudaStream_t (NULL = legacy default stream)                   */
+int vk_plan_execute(vk_plan* plan, const float* known, const double* models,
+                    float* out, double* var, void* stream);
+
+/* Synchronises the stream, maps device-side statuses to a vk_status.
+ * failed_part: first failing sub-part or -1.  models_out: host f64 [S][3]
+ * fitted (or supplied) models, may be NULL.  lohi_out: host f64 [S][2] clamp
+ * range per part, may be NULL. */
+int vk_plan_finish(vk_plan* plan, void* stream, int32_t* failed_part,
+                   double* models_out, double* lohi_out);
+
+/* Introspection for tests / benchmarks. */
+typedef struct {
+  int32_t fast_path;        /* 1 if the streaming kernel handles all gaps  */
+  int32_t gap_planes;       /* G missing planes per gap on the fast path   */
+  int32_t n_patterns;
+  int32_t n_kinds;
+  int32_t n_systems;
+  int32_t n_missing_planes;
+  int32_t n_pair_classes;
+  int32_t kernels_per_execute;
+  int64_t interpolated_voxels;
+} vk_plan_info;
+int vk_plan_get_info(const vk_plan* plan, vk_plan_info* info);
+
+/* Copies solved stencils to host: weights f64 [n_systems][128] padded
+ * ([plane][oy+1][ox+1]), variance f64 [n_systems], and per system (part,
+ * pattern, ky, kx) int32 [n_systems][4].  Call after vk_plan_finish. */
+int vk_plan_get_systems(vk_plan* plan, double* weights, double* variance,
+                        int32_t* ids);
+
+/* Replaces: fit_variogram(samples, ...) (kriging.py:264-328) for explicit
+ * samples.  coords device f64 [m][3] (x,y,z), values device f64 [m].
+ * Synchronous; writes the model (nugget, sill, range_len) to model_out. */
+int vk_fit_variogram_samples(const double* coords, const double* values,
+                             int64_t m, int32_t kind, int32_t n_bins,
+                             int64_t max_pairs, uint64_t seed,
+                             double* model_out, void* stream);
+
+/* The pair draw of kriging.py:278-286 on the device: ii/jj device int32
+ * [max_pairs] (triu order when m(m-1)/2 <= max_pairs).  Returns the number of
+ * pairs written in *n_out (before dropping ii == jj).  Synchronous. */
+int vk_sample_pairs(int64_t m, int64_t max_pairs, uint64_t seed, int32_t* ii,
+                    int32_t* jj, int64_t* n_out, void* stream);
+
+/* Replaces: VolumeGrid.validate + _plane_structured (model.py:111-117,
+ * kriging.py:434-441).  data device f32 [T][P], mask device u8 [T][P];
+ * counts device int32 [T][4] = (#missing, #nan, #nan!=mask, #known
+ * non-finite) per plane. */
+int vk_grid_scan(const float* data, const uint8_t* mask, int64_t planes,
+                 int64_t plane_elems, int32_t* counts, void* stream);
+
+/* Gathers known planes: dst[k] = src[known_z[k]] (device f32, [*][P]),
+ * known_z host int32 [K]. */
+int vk_gather_planes(const float* src, const int32_t* known_z, int32_t K,
+                     int64_t plane_elems, float* dst, void* stream);
+
+const char* vk_status_string(int status);
+/* Message of the last failing call on this thread (for exceptions). */
+const char* vk_last_error(void);
+int vk_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOLKRIG_B200_H */

@@ -1,0 +1,20 @@
+"""volkrig-b200: B200-native kriging interpolation path of arXiv 2303.09523.
+
+Drop-in for the reference's ``volkrig.kriging`` entry points, backed by
+hand-written sm_100a CUDA kernels behind a C ABI (``include/volkrig_b200.h``).
+"""
+
+from .errors import (DegenerateLags, DeviceError, DeviceUnsupported,
+                     InsufficientSamples, NoKnownNeighbors, SingularSystem,
+                     TooFewSlices, VolkrigError)
+from .model import SliceStack, VolumeGrid, missing_planes_per_gap
+from .kriging import (KrigingPlan, VariogramModel, fill_missing, fit_variogram)
+from .block_pipeline import ZPartKriging, reconstruct_zparts, subpart_ranges
+
+__all__ = [
+    "DegenerateLags", "DeviceError", "DeviceUnsupported", "InsufficientSamples",
+    "NoKnownNeighbors", "SingularSystem", "TooFewSlices", "VolkrigError",
+    "SliceStack", "VolumeGrid", "missing_planes_per_gap", "KrigingPlan",
+    "VariogramModel", "fill_missing", "fit_variogram", "ZPartKriging",
+    "reconstruct_zparts", "subpart_ranges",
+]

@@ -1,0 +1,74 @@
+"""Builds the in-tree CUDA library ``_native/libvolkrig_b200.so`` for sm_100a.
+
+The library is a plain C ABI (``include/volkrig_b200.h``); it is compiled
+with nvcc directly (no torch extension), so it carries no torch types and can
+be bound from any FFI.  The variogram and solver translation units are built
+with ``-fmad=false`` so their arithmetic rounds like numpy's (no contraction
+of a*b+c); the prediction kernels keep FMA.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT_DIR = PKG / "_native"
+LIB = OUT_DIR / "libvolkrig_b200.so"
+INCLUDE = PKG.parent / "include"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+UNITS = {
+    "vk_api.cu": [],
+    "vk_variogram.cu": ["-fmad=false"],
+    "vk_solve.cu": ["-fmad=false"],
+    "vk_predict.cu": [],
+    "vk_geometry.cpp": [],
+}
+
+
+def _deps() -> list[Path]:
+    return sorted(CSRC.glob("*.h")) + sorted(INCLUDE.glob("*.h"))
+
+
+def _stale(target: Path, sources: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(s.stat().st_mtime > t for s in sources)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    OUT_DIR.mkdir(exist_ok=True)
+    objs = []
+    deps = _deps()
+    for unit, extra in UNITS.items():
+        src = CSRC / unit
+        obj = OUT_DIR / (unit + ".o")
+        objs.append(obj)
+        if not force and not _stale(obj, [src] + deps + [Path(__file__)]):
+            continue
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+               "-I", str(INCLUDE), "-I", str(CSRC), *extra, "-c", str(src),
+               "-o", str(obj)]
+        if unit.endswith(".cpp"):
+            cmd.insert(1, "-x")
+            cmd.insert(2, "cu")
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    if force or _stale(LIB, objs):
+        tmp = LIB.with_suffix(".so.tmp")
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs),
+               "-cudart", "static"]
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,649 @@
+// C ABI of the volkrig-b200 kriging path (include/volkrig_b200.h): plan
+// creation (host geometry + device tables), stream-ordered execution of
+// stats -> pairs -> bins -> fit -> solve -> predict, and status mapping.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/volkrig_b200.h"
+#include "pcg64.h"
+#include "vk_geometry.h"
+#include "vk_kernels.h"
+
+namespace vk {
+cudaError_t launch_plane_stats_f64(const double* values, int64_t m, ChunkStat* out, int nchunk,
+                                   cudaStream_t st);
+}
+
+using namespace vk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_err(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define VK_CUDA(call)                                                             \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      return set_err(VK_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+cudaError_t upload(T** dst, const std::vector<T>& src) {
+  *dst = nullptr;
+  if (src.empty()) return cudaSuccess;
+  cudaError_t e = cudaMalloc((void**)dst, src.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+int status_from_part(int ps) {
+  switch (ps) {
+    case PS_OK: return VK_OK;
+    case PS_SINGULAR: return VK_E_SINGULAR_SYSTEM;
+    case PS_INSUFFICIENT: return VK_E_INSUFFICIENT_SAMPLES;
+    case PS_DEGENERATE: return VK_E_DEGENERATE_LAGS;
+    case PS_FIT_FAILED: return VK_E_FIT_FAILED;
+    default: return VK_E_CUDA;
+  }
+}
+
+}  // namespace
+
+struct vk_plan {
+  vk_plan_desc desc;
+  Geometry geo;
+  int num_sms = 0;
+  int NP = 0, NK = 0, n_sys = 0, max_n = 0;
+  int nchunk = 0, nblk = 0;
+  std::vector<void*> allocs;
+  // device tables
+  int32_t *d_known_z = nullptr, *d_miss_z = nullptr, *d_miss_part = nullptr, *d_miss_pattern = nullptr,
+          *d_miss_planes = nullptr, *d_sys_part = nullptr, *d_sys_stencil = nullptr, *d_st_off = nullptr,
+          *d_st_n = nullptr, *d_st_drift = nullptr, *d_st_pattern = nullptr, *d_pat_dz = nullptr,
+          *d_gap_part = nullptr, *d_gap_pattern = nullptr, *d_kmap = nullptr, *d_part_b = nullptr,
+          *d_part_e = nullptr, *d_part_class = nullptr, *d_zloc = nullptr;
+  int8_t* d_taps = nullptr;
+  int16_t* d_pad = nullptr;
+  int64_t *d_part_base = nullptr, *d_part_m = nullptr;
+  // workspace
+  ChunkStat* d_stats = nullptr;
+  double *d_partial = nullptr, *d_models = nullptr, *d_lohi = nullptr, *d_weights = nullptr, *d_var = nullptr;
+  int32_t *d_part_status = nullptr, *d_sys_status = nullptr;
+  std::vector<PairTable> tables;
+  PairTable* d_tables = nullptr;
+  bool pairs_ready = false;
+  double* h_models = nullptr;        // pinned staging [S][3]
+  int kernels = 0;
+
+  template <typename T>
+  cudaError_t alloc(T** p, size_t n) {
+    cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) allocs.push_back(*p);
+    return e;
+  }
+  template <typename T>
+  cudaError_t put(T** p, const std::vector<T>& v) {
+    cudaError_t e = upload(p, v);
+    if (e == cudaSuccess && *p) allocs.push_back(*p);
+    return e;
+  }
+  ~vk_plan() {
+    for (void* p : allocs) cudaFree(p);
+    if (h_models) cudaFreeHost(h_models);
+  }
+};
+
+extern "C" {
+
+int vk_abi_version(void) { return VK_ABI_VERSION; }
+
+const char* vk_status_string(int s) {
+  switch (s) {
+    case VK_OK: return "ok";
+    case VK_E_INVALID_ARGUMENT: return "invalid argument";
+    case VK_E_NO_KNOWN_NEIGHBORS: return "no known neighbors";
+    case VK_E_SINGULAR_SYSTEM: return "singular kriging system";
+    case VK_E_INSUFFICIENT_SAMPLES: return "insufficient samples";
+    case VK_E_DEGENERATE_LAGS: return "degenerate lags";
+    case VK_E_UNSUPPORTED: return "unsupported layout";
+    case VK_E_CUDA: return "cuda error";
+    case VK_E_INVALID_GRID: return "invalid grid";
+    case VK_E_FIT_FAILED: return "variogram fit failed";
+    default: return "unknown";
+  }
+}
+
+const char* vk_last_error(void) { return g_last_error.c_str(); }
+
+int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
+  if (!d || !out) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (d->kind < 0 || d->kind > 2) return set_err(VK_E_INVALID_ARGUMENT, "kind");
+  if (d->drift < 0 || d->drift > 1) return set_err(VK_E_INVALID_ARGUMENT, "drift");
+  if (d->n_bins < 1 || d->n_bins > MAX_BINS) return set_err(VK_E_INVALID_ARGUMENT, "n_bins must be in 1..32");
+  if (d->max_pairs < 1 || d->max_pairs > (1ll << 30)) return set_err(VK_E_INVALID_ARGUMENT, "max_pairs");
+  if (!d->known_z && d->n_known > 0) return set_err(VK_E_INVALID_ARGUMENT, "known_z");
+  vk_plan* p = new vk_plan();
+  p->desc = *d;
+  p->desc.known_z = nullptr;
+  std::string err = build_geometry(d->height, d->width, d->depth, d->known_z, d->n_known, d->n_subparts,
+                                   d->drift, &p->geo);
+  if (!err.empty()) {
+    delete p;
+    if (err.rfind("NoKnownNeighbors", 0) == 0) return set_err(VK_E_NO_KNOWN_NEIGHBORS, err);
+    if (err.rfind("Unsupported", 0) == 0) return set_err(VK_E_UNSUPPORTED, err);
+    return set_err(VK_E_INVALID_ARGUMENT, err);
+  }
+  Geometry& g = p->geo;
+  if (d->flags & VK_FLAG_FORCE_GENERIC) g.fast = false;
+  const int64_t P = (int64_t)g.H * g.W;
+  if (d->fit_variogram) {
+    for (const PartInfo& pi : g.parts)
+      if (pi.m > 0xffffffffll)
+        return delete p, set_err(VK_E_UNSUPPORTED, "more than 2^32 samples in one sub-part");
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  p->NP = (int)g.patterns.size();
+  p->NK = g.n_kinds();
+  p->n_sys = (int)g.sys_part.size();
+  p->nchunk = (int)((P + STATS_CHUNK - 1) / STATS_CHUNK);
+  p->nblk = (int)std::max<int64_t>(1, (std::min<int64_t>(d->max_pairs, (int64_t)1 << 30) + 4095) / 4096);
+
+  // ---- host tables
+  std::vector<int32_t> st_off, st_n, st_drift, st_pattern, pat_dz((size_t)std::max(1, p->NP) * NPMAX, 0);
+  std::vector<int8_t> taps;
+  std::vector<int16_t> pad;
+  for (const StencilGeom& sg : g.stencils) {
+    st_off.push_back((int32_t)pad.size());
+    st_n.push_back(sg.n);
+    st_drift.push_back(sg.drift_cols);
+    st_pattern.push_back(sg.pattern);
+    taps.insert(taps.end(), sg.taps.begin(), sg.taps.end());
+    pad.insert(pad.end(), sg.pad.begin(), sg.pad.end());
+    p->max_n = std::max(p->max_n, sg.n);
+  }
+  for (int q = 0; q < p->NP; ++q)
+    for (size_t i = 0; i < g.patterns[q].size(); ++i) pat_dz[(size_t)q * NPMAX + i] = g.patterns[q][i];
+  std::vector<int32_t> kmap(2 * NKIND1, 0);
+  for (int i = 0; i < NKIND1; ++i) {
+    kmap[i] = std::max(0, g.kx_map[i]);
+    kmap[NKIND1 + i] = std::max(0, g.ky_map[i]);
+  }
+  std::vector<int32_t> part_b, part_e, part_class, zloc_all;
+  std::vector<int64_t> part_base, part_m;
+  std::vector<int32_t> class_zoff;
+  for (const PairClass& pc : g.pair_classes) {
+    class_zoff.push_back((int32_t)zloc_all.size());
+    zloc_all.insert(zloc_all.end(), pc.zloc.begin(), pc.zloc.end());
+  }
+  for (const PartInfo& pi : g.parts) {
+    part_b.push_back(pi.b);
+    part_e.push_back(pi.e);
+    part_class.push_back(pi.pair_class);
+    part_base.push_back((int64_t)pi.b * P);
+    part_m.push_back(pi.m);
+  }
+  std::vector<int32_t> known_z(g.known_z.begin(), g.known_z.end());
+  const int S = g.S;
+  cudaError_t e = cudaSuccess;
+#define VK_TRY(x)                                                           \
+  if ((e = (x)) != cudaSuccess) {                                           \
+    delete p;                                                               \
+    return set_err(VK_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e)); \
+  }
+  VK_TRY(p->put(&p->d_known_z, known_z));
+  VK_TRY(p->put(&p->d_miss_z, g.miss_z));
+  VK_TRY(p->put(&p->d_miss_part, g.miss_part));
+  VK_TRY(p->put(&p->d_miss_pattern, g.miss_pattern));
+  VK_TRY(p->put(&p->d_miss_planes, g.miss_planes));
+  VK_TRY(p->put(&p->d_sys_part, g.sys_part));
+  VK_TRY(p->put(&p->d_sys_stencil, g.sys_stencil));
+  VK_TRY(p->put(&p->d_st_off, st_off));
+  VK_TRY(p->put(&p->d_st_n, st_n));
+  VK_TRY(p->put(&p->d_st_drift, st_drift));
+  VK_TRY(p->put(&p->d_st_pattern, st_pattern));
+  VK_TRY(p->put(&p->d_pat_dz, pat_dz));
+  VK_TRY(p->put(&p->d_taps, taps));
+  VK_TRY(p->put(&p->d_pad, pad));
+  VK_TRY(p->put(&p->d_kmap, kmap));
+  VK_TRY(p->put(&p->d_gap_part, g.gap_part));
+  VK_TRY(p->put(&p->d_gap_pattern, g.gap_pattern));
+  VK_TRY(p->put(&p->d_part_b, part_b));
+  VK_TRY(p->put(&p->d_part_e, part_e));
+  VK_TRY(p->put(&p->d_part_class, part_class));
+  VK_TRY(p->put(&p->d_part_base, part_base));
+  VK_TRY(p->put(&p->d_part_m, part_m));
+  VK_TRY(p->put(&p->d_zloc, zloc_all));
+  VK_TRY(p->alloc(&p->d_stats, (size_t)g.K * p->nchunk));
+  VK_TRY(p->alloc(&p->d_models, (size_t)S * 3));
+  VK_TRY(p->alloc(&p->d_lohi, (size_t)S * 2));
+  VK_TRY(p->alloc(&p->d_part_status, (size_t)S));
+  VK_TRY(p->alloc(&p->d_sys_status, (size_t)std::max(1, p->n_sys)));
+  VK_TRY(p->alloc(&p->d_weights, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK) * WPAD));
+  VK_TRY(p->alloc(&p->d_var, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK)));
+  VK_TRY(cudaMallocHost((void**)&p->h_models, (size_t)S * 3 * sizeof(double)));
+  if (d->fit_variogram) {
+    VK_TRY(p->alloc(&p->d_partial, (size_t)S * p->nblk * d->n_bins));
+    for (size_t c = 0; c < g.pair_classes.size(); ++c) {
+      PairTable t;
+      VK_TRY(p->alloc(&t.ii, (size_t)d->max_pairs));
+      VK_TRY(p->alloc(&t.jj, (size_t)d->max_pairs));
+      VK_TRY(p->alloc(&t.bin, (size_t)d->max_pairs));
+      VK_TRY(p->alloc(&t.counts, (size_t)MAX_BINS));
+      VK_TRY(p->alloc(&t.scal, (size_t)4));
+      p->tables.push_back(t);
+    }
+    VK_TRY(p->put(&p->d_tables, p->tables));
+  }
+#undef VK_TRY
+  (void)class_zoff;
+  *out = p;
+  return VK_OK;
+}
+
+void vk_plan_destroy(vk_plan* p) { delete p; }
+
+int vk_plan_get_info(const vk_plan* p, vk_plan_info* info) {
+  if (!p || !info) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  const Geometry& g = p->geo;
+  info->fast_path = g.fast ? 1 : 0;
+  info->gap_planes = g.G;
+  info->n_patterns = p->NP;
+  info->n_kinds = p->NK;
+  info->n_systems = p->n_sys;
+  info->n_missing_planes = (int32_t)g.miss_z.size();
+  info->n_pair_classes = (int32_t)g.pair_classes.size();
+  info->kernels_per_execute = p->kernels;
+  info->interpolated_voxels = g.n_missing_voxels();
+  return VK_OK;
+}
+
+int vk_plan_execute(vk_plan* p, const float* known, const double* models, float* out, double* var,
+                    void* stream) {
+  if (!p || !known || !out) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geometry& g = p->geo;
+  const vk_plan_desc& d = p->desc;
+  const int64_t P = (int64_t)g.H * g.W;
+  const int S = g.S;
+  int kernels = 0;
+  if (!d.fit_variogram) {
+    if (!models) return set_err(VK_E_INVALID_ARGUMENT, "models required when fit_variogram == 0");
+    std::memcpy(p->h_models, models, (size_t)S * 3 * sizeof(double));
+    VK_CUDA(cudaMemcpyAsync(p->d_models, p->h_models, (size_t)S * 3 * sizeof(double),
+                            cudaMemcpyHostToDevice, st));
+  }
+  VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st));
+  ++kernels;
+  if (d.fit_variogram) {
+    if (!p->pairs_ready) {
+      const Pcg64 gen = pcg64_from_seed(d.seed);
+      std::vector<int32_t> zoff;
+      int32_t acc = 0;
+      for (const PairClass& pc : g.pair_classes) { zoff.push_back(acc); acc += (int32_t)pc.zloc.size(); }
+      for (size_t c = 0; c < g.pair_classes.size(); ++c) {
+        SampleGeom sg;
+        sg.coords = nullptr;
+        sg.zloc = p->d_zloc + zoff[c];
+        sg.P = P;
+        sg.W = g.W;
+        VK_CUDA(launch_pair_table((uint64_t)(gen.state >> 64), (uint64_t)gen.state, (uint64_t)(gen.inc >> 64),
+                                  (uint64_t)gen.inc, g.pair_classes[c].m, d.max_pairs, d.n_bins, sg,
+                                  p->tables[c], st));
+        ++kernels;
+      }
+      p->pairs_ready = true;
+    }
+    BinsArgs ba;
+    ba.known = known;
+    ba.values = nullptr;
+    ba.part_base = p->d_part_base;
+    ba.part_class = p->d_part_class;
+    ba.tables = p->d_tables;
+    ba.max_pairs = d.max_pairs;
+    ba.n_bins = d.n_bins;
+    ba.nblk = p->nblk;
+    ba.S = S;
+    ba.partial = p->d_partial;
+    VK_CUDA(launch_bins(ba, st));
+    ++kernels;
+  }
+  FitArgs fa;
+  fa.S = S;
+  fa.n_bins = d.n_bins;
+  fa.nblk = p->nblk;
+  fa.kind = d.kind;
+  fa.fit = d.fit_variogram;
+  fa.nchunk = p->nchunk;
+  fa.stats = p->d_stats;
+  fa.part_b = p->d_part_b;
+  fa.part_e = p->d_part_e;
+  fa.part_class = p->d_part_class;
+  fa.part_m = p->d_part_m;
+  fa.tables = p->d_tables;
+  fa.partial = p->d_partial;
+  fa.models = p->d_models;
+  fa.lohi = p->d_lohi;
+  fa.status = p->d_part_status;
+  VK_CUDA(launch_fit(fa, st));
+  ++kernels;
+  SolveArgs sa;
+  sa.n_sys = p->n_sys;
+  sa.kind = d.kind;
+  sa.drift = d.drift;
+  sa.NP = p->NP;
+  sa.NK = p->NK;
+  sa.sys_part = p->d_sys_part;
+  sa.sys_stencil = p->d_sys_stencil;
+  sa.st_off = p->d_st_off;
+  sa.st_n = p->d_st_n;
+  sa.st_drift = p->d_st_drift;
+  sa.st_pattern = p->d_st_pattern;
+  sa.taps = p->d_taps;
+  sa.pad = p->d_pad;
+  sa.pat_dz = p->d_pat_dz;
+  sa.models = p->d_models;
+  sa.weights = p->d_weights;
+  sa.var = p->d_var;
+  sa.sys_status = p->d_sys_status;
+  sa.max_n = p->max_n;
+  VK_CUDA(launch_solve(sa, st));
+  if (p->n_sys) ++kernels;
+  PredictArgs pa;
+  pa.known = known;
+  pa.out = out;
+  pa.var = var;
+  pa.H = g.H;
+  pa.W = g.W;
+  pa.K = g.K;
+  pa.NP = p->NP;
+  pa.NK = p->NK;
+  pa.accum = d.accum;
+  pa.P = P;
+  pa.known_z = p->d_known_z;
+  pa.weights = p->d_weights;
+  pa.svar = p->d_var;
+  pa.lohi = p->d_lohi;
+  pa.kmap = p->d_kmap;
+  pa.nkx = g.nkx;
+  pa.n_miss = (int)g.miss_z.size();
+  pa.miss_z = p->d_miss_z;
+  pa.miss_part = p->d_miss_part;
+  pa.miss_pattern = p->d_miss_pattern;
+  pa.miss_planes = p->d_miss_planes;
+  pa.G = g.G;
+  pa.gap_part = p->d_gap_part;
+  pa.gap_pattern = p->d_gap_pattern;
+  pa.num_sms = p->num_sms;
+  if (g.fast && predict_fast_supported(g.G, d.accum)) {
+    VK_CUDA(launch_predict_fast(pa, st));
+    ++kernels;
+  } else {
+    VK_CUDA(launch_copy_known(pa, st));
+    VK_CUDA(launch_predict_generic(pa, st));
+    kernels += 1 + (pa.n_miss > 0);
+  }
+  p->kernels = kernels;
+  return VK_OK;
+}
+
+int vk_plan_finish(vk_plan* p, void* stream, int32_t* failed_part, double* models_out, double* lohi_out) {
+  if (!p) return set_err(VK_E_INVALID_ARGUMENT, "null plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  VK_CUDA(cudaStreamSynchronize(st));
+  const int S = p->geo.S;
+  std::vector<int32_t> ps(S), ss(std::max(1, p->n_sys));
+  VK_CUDA(cudaMemcpy(ps.data(), p->d_part_status, S * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (p->n_sys)
+    VK_CUDA(cudaMemcpy(ss.data(), p->d_sys_status, p->n_sys * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (models_out)
+    VK_CUDA(cudaMemcpy(models_out, p->d_models, (size_t)S * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (lohi_out)
+    VK_CUDA(cudaMemcpy(lohi_out, p->d_lohi, (size_t)S * 2 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (failed_part) *failed_part = -1;
+  for (int s = 0; s < S; ++s) {
+    if (ps[s] != PS_OK) {
+      if (failed_part) *failed_part = s;
+      return set_err(status_from_part(ps[s]), "sub-part " + std::to_string(s) + ": status " +
+                                                  std::to_string(ps[s]));
+    }
+  }
+  for (int i = 0; i < p->n_sys; ++i) {
+    if (ss[i] != PS_OK) {
+      if (failed_part) *failed_part = p->geo.sys_part[i];
+      return set_err(VK_E_SINGULAR_SYSTEM, "extended kriging matrix is singular");
+    }
+  }
+  return VK_OK;
+}
+
+int vk_plan_get_systems(vk_plan* p, double* weights, double* variance, int32_t* ids) {
+  if (!p) return set_err(VK_E_INVALID_ARGUMENT, "null plan");
+  const Geometry& g = p->geo;
+  const size_t nslot = (size_t)g.S * std::max(1, p->NP) * std::max(1, p->NK);
+  std::vector<double> w(nslot * WPAD), v(nslot);
+  VK_CUDA(cudaDeviceSynchronize());
+  VK_CUDA(cudaMemcpy(w.data(), p->d_weights, w.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  VK_CUDA(cudaMemcpy(v.data(), p->d_var, v.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < p->n_sys; ++i) {
+    const int s = g.sys_part[i], stc = g.sys_stencil[i];
+    const StencilGeom& sg = g.stencils[stc];
+    const size_t slot = ((size_t)s * p->NP + sg.pattern) * p->NK + (stc % p->NK);
+    if (weights) std::memcpy(weights + (size_t)i * WPAD, &w[slot * WPAD], WPAD * sizeof(double));
+    if (variance) variance[i] = v[slot];
+    if (ids) {
+      ids[4 * i + 0] = s;
+      ids[4 * i + 1] = sg.pattern;
+      ids[4 * i + 2] = sg.ky;
+      ids[4 * i + 3] = sg.kx;
+    }
+  }
+  return VK_OK;
+}
+
+int vk_sample_pairs(int64_t m, int64_t max_pairs, uint64_t seed, int32_t* ii, int32_t* jj, int64_t* n_out,
+                    void* stream) {
+  if (m < 2 || m > 0xffffffffll || max_pairs < 1) return set_err(VK_E_INVALID_ARGUMENT, "m / max_pairs");
+  cudaStream_t st = (cudaStream_t)stream;
+  PairTable t;
+  t.ii = ii;
+  t.jj = jj;
+  VK_CUDA(cudaMalloc((void**)&t.bin, (size_t)max_pairs));
+  VK_CUDA(cudaMalloc((void**)&t.counts, MAX_BINS * sizeof(int64_t)));
+  VK_CUDA(cudaMalloc((void**)&t.scal, 4 * sizeof(double)));
+  int32_t* zl = nullptr;
+  VK_CUDA(cudaMalloc((void**)&zl, sizeof(int32_t)));
+  VK_CUDA(cudaMemsetAsync(zl, 0, sizeof(int32_t), st));
+  const Pcg64 gen = pcg64_from_seed(seed);
+  SampleGeom sg;
+  sg.coords = nullptr;
+  sg.zloc = zl;
+  sg.P = m;            // one "plane" holding every sample: lags unused here
+  sg.W = (int32_t)std::min<int64_t>(m, 1 << 30);
+  cudaError_t e = launch_pair_table((uint64_t)(gen.state >> 64), (uint64_t)gen.state, (uint64_t)(gen.inc >> 64),
+                                    (uint64_t)gen.inc, m, max_pairs, 15, sg, t, st);
+  double scal[4] = {0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(scal, t.scal, sizeof(scal), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(t.bin);
+  cudaFree(t.counts);
+  cudaFree(t.scal);
+  cudaFree(zl);
+  if (e != cudaSuccess) return set_err(VK_E_CUDA, cudaGetErrorString(e));
+  if (n_out) *n_out = (int64_t)scal[2];
+  return scal[3] == 0.0 ? VK_OK : set_err(VK_E_CUDA, "pair draw ran short");
+}
+
+int vk_fit_variogram_samples(const double* coords, const double* values, int64_t m, int32_t kind,
+                             int32_t n_bins, int64_t max_pairs, uint64_t seed, double* model_out,
+                             void* stream) {
+  if (!coords || !values || !model_out) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  if (kind < 0 || kind > 2 || n_bins < 1 || n_bins > MAX_BINS || max_pairs < 1)
+    return set_err(VK_E_INVALID_ARGUMENT, "kind / n_bins / max_pairs");
+  if (m * (m - 1) / 2 < 30)
+    return set_err(VK_E_INSUFFICIENT_SAMPLES, std::to_string(m) + " samples give " +
+                                                  std::to_string(m * (m - 1) / 2) + " pairs; need >= 30");
+  if (m > 0xffffffffll) return set_err(VK_E_UNSUPPORTED, "more than 2^32 samples");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t npmax = std::min<int64_t>(max_pairs, m * (m - 1) / 2);
+  const int nchunk = (int)((m + STATS_CHUNK - 1) / STATS_CHUNK);
+  const int nblk = (int)std::max<int64_t>(1, (npmax + 4095) / 4096);
+  std::vector<void*> mem;
+  auto get = [&](size_t bytes) -> void* {
+    void* q = nullptr;
+    if (cudaMalloc(&q, std::max<size_t>(bytes, 8)) != cudaSuccess) return nullptr;
+    mem.push_back(q);
+    return q;
+  };
+  PairTable t;
+  t.ii = (int32_t*)get(npmax * 4);
+  t.jj = (int32_t*)get(npmax * 4);
+  t.bin = (uint8_t*)get(npmax);
+  t.counts = (int64_t*)get(MAX_BINS * 8);
+  t.scal = (double*)get(4 * 8);
+  PairTable* d_t = (PairTable*)get(sizeof(PairTable));
+  ChunkStat* stats = (ChunkStat*)get((size_t)nchunk * sizeof(ChunkStat));
+  double* partial = (double*)get((size_t)nblk * n_bins * 8);
+  double* models = (double*)get(3 * 8);
+  double* lohi = (double*)get(2 * 8);
+  int32_t* status = (int32_t*)get(4);
+  int32_t* zero32 = (int32_t*)get(8);
+  int64_t* zero64 = (int64_t*)get(8);
+  int64_t* mm = (int64_t*)get(8);
+  auto cleanup = [&]() { for (void* q : mem) cudaFree(q); };
+  for (void* q : mem)
+    if (!q) { cleanup(); return set_err(VK_E_CUDA, "cudaMalloc failed"); }
+  cudaError_t e = cudaMemcpyAsync(d_t, &t, sizeof(PairTable), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(zero32, 0, 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(zero64, 0, 8, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(mm, &m, 8, cudaMemcpyHostToDevice, st);
+  const Pcg64 gen = pcg64_from_seed(seed);
+  SampleGeom sg;
+  sg.coords = coords;
+  sg.zloc = nullptr;
+  sg.P = m;
+  sg.W = 1;
+  if (e == cudaSuccess)
+    e = launch_pair_table((uint64_t)(gen.state >> 64), (uint64_t)gen.state, (uint64_t)(gen.inc >> 64),
+                          (uint64_t)gen.inc, m, max_pairs, n_bins, sg, t, st);
+  if (e == cudaSuccess) e = launch_plane_stats_f64(values, m, stats, nchunk, st);
+  BinsArgs ba;
+  ba.known = nullptr;
+  ba.values = values;
+  ba.part_base = zero64;
+  ba.part_class = zero32;
+  ba.tables = d_t;
+  ba.max_pairs = npmax;
+  ba.n_bins = n_bins;
+  ba.nblk = nblk;
+  ba.S = 1;
+  ba.partial = partial;
+  if (e == cudaSuccess) e = launch_bins(ba, st);
+  FitArgs fa;
+  fa.S = 1;
+  fa.n_bins = n_bins;
+  fa.nblk = nblk;
+  fa.kind = kind;
+  fa.fit = 1;
+  fa.nchunk = nchunk;
+  fa.stats = stats;
+  fa.part_b = zero32;
+  fa.part_e = zero32;
+  fa.part_class = zero32;
+  fa.part_m = mm;
+  fa.tables = d_t;
+  fa.partial = partial;
+  fa.models = models;
+  fa.lohi = lohi;
+  fa.status = status;
+  if (e == cudaSuccess) e = launch_fit(fa, st);
+  double mo[3] = {0, 0, 0};
+  int32_t s = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(mo, models, sizeof(mo), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&s, status, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cleanup();
+  if (e != cudaSuccess) return set_err(VK_E_CUDA, cudaGetErrorString(e));
+  if (s != PS_OK) {
+    if (s == PS_DEGENERATE) return set_err(VK_E_DEGENERATE_LAGS, "all sample pairs are co-located");
+    return set_err(status_from_part(s), "fit failed with status " + std::to_string(s));
+  }
+  std::memcpy(model_out, mo, sizeof(mo));
+  return VK_OK;
+}
+
+// ---- drop-in helpers for fill_missing(grid): validation + plane compaction
+namespace {
+__global__ void grid_scan_kernel(const float* __restrict__ data, const uint8_t* __restrict__ mask,
+                                 int64_t PE, int32_t* counts) {
+  const int64_t z = blockIdx.y;
+  int c_miss = 0, c_nan = 0, c_bad = 0, c_inf = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < PE; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = data[z * PE + i];
+    const bool m = mask[z * PE + i] != 0;
+    const bool isn = v != v;
+    c_miss += m;
+    c_nan += isn;
+    c_bad += (isn != m);
+    c_inf += (!m && !isn && isinf(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c_miss += __shfl_down_sync(0xffffffffu, c_miss, o);
+    c_nan += __shfl_down_sync(0xffffffffu, c_nan, o);
+    c_bad += __shfl_down_sync(0xffffffffu, c_bad, o);
+    c_inf += __shfl_down_sync(0xffffffffu, c_inf, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&counts[z * 4 + 0], c_miss);
+    atomicAdd(&counts[z * 4 + 1], c_nan);
+    atomicAdd(&counts[z * 4 + 2], c_bad);
+    atomicAdd(&counts[z * 4 + 3], c_inf);
+  }
+}
+
+__global__ void gather_planes_kernel(const float* __restrict__ src, const int32_t* __restrict__ kz, int64_t PE,
+                                     float* __restrict__ dst) {
+  const int k = blockIdx.y;
+  const int64_t z = kz[k];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < PE; i += (int64_t)gridDim.x * blockDim.x)
+    dst[(int64_t)k * PE + i] = src[z * PE + i];
+}
+}  // namespace
+
+int vk_grid_scan(const float* data, const uint8_t* mask, int64_t planes, int64_t plane_elems, int32_t* counts,
+                 void* stream) {
+  if (!data || !mask || !counts || planes < 1 || plane_elems < 1) return set_err(VK_E_INVALID_ARGUMENT, "scan args");
+  cudaStream_t st = (cudaStream_t)stream;
+  VK_CUDA(cudaMemsetAsync(counts, 0, (size_t)planes * 4 * sizeof(int32_t), st));
+  dim3 grid((unsigned)std::min<int64_t>(64, (plane_elems + 255) / 256), (unsigned)planes);
+  grid_scan_kernel<<<grid, 256, 0, st>>>(data, mask, plane_elems, counts);
+  VK_CUDA(cudaGetLastError());
+  return VK_OK;
+}
+
+int vk_gather_planes(const float* src, const int32_t* known_z, int32_t K, int64_t plane_elems, float* dst,
+                     void* stream) {
+  if (!src || !known_z || !dst || K < 1) return set_err(VK_E_INVALID_ARGUMENT, "gather args");
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* dkz = nullptr;
+  VK_CUDA(cudaMallocAsync((void**)&dkz, K * sizeof(int32_t), st));
+  VK_CUDA(cudaMemcpyAsync(dkz, known_z, K * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  dim3 grid((unsigned)std::min<int64_t>(256, (plane_elems + 255) / 256), (unsigned)K);
+  gather_planes_kernel<<<grid, 256, 0, st>>>(src, dkz, plane_elems, dst);
+  VK_CUDA(cudaGetLastError());
+  VK_CUDA(cudaFreeAsync(dkz, st));
+  return VK_OK;
+}
+
+}  // extern "C"

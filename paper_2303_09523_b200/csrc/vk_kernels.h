@@ -1,0 +1,109 @@
+// Internal launcher interface between the plan (vk_api.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "vk_common.h"
+
+namespace vk {
+
+// Per-chunk plane statistics (count, mean, M2, min, max, non-finite).
+struct ChunkStat {
+  double n, mean, m2, mn, mx, bad;
+};
+constexpr int STATS_CHUNK = 32768;   // elements per stats block
+
+struct PairTable {                   // one per pair class (device pointers)
+  int32_t* ii;
+  int32_t* jj;
+  uint8_t* bin;                      // 255 = skipped (i == j or lag == 0)
+  int64_t* counts;                   // [n_bins]
+  double* scal;                      // [0] hmax, [1] lag_max, [2] n_drawn, [3] status
+};
+
+// Coordinates of sample i of a structured sub-part: plane i / P at local z
+// zloc[i / P], pixel (i % P) -> (x, y).  Explicit: coords[i*3 + {0,1,2}].
+struct SampleGeom {
+  const double* coords;              // explicit coords or nullptr
+  const int32_t* zloc;               // structured: local z per known plane
+  int64_t P;
+  int32_t W;
+};
+
+cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out,
+                               int nchunk, cudaStream_t st);
+cudaError_t launch_pair_table(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
+                              int64_t m, int64_t max_pairs, int n_bins, SampleGeom geom,
+                              PairTable t, cudaStream_t st);
+struct BinsArgs {
+  const float* known;      // structured: known planes; sample i of part s = known[base_s + i]
+  const double* values;    // explicit samples (fit_variogram API) or nullptr
+  const int64_t* part_base;// [S] element offset of each part's first sample
+  const int32_t* part_class;
+  const PairTable* tables;  // device array [n_classes]
+  int64_t max_pairs;
+  int n_bins, nblk, S;
+  double* partial;          // [S][nblk][n_bins]
+};
+cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st);
+
+struct FitArgs {
+  int S, n_bins, nblk, kind, fit, nchunk;
+  const ChunkStat* stats;   // [K][nchunk] (structured) or [1][nchunk] (explicit)
+  const int32_t* part_b;    // [S]
+  const int32_t* part_e;    // [S]
+  const int32_t* part_class;
+  const int64_t* part_m;    // [S]
+  const PairTable* tables;
+  const double* partial;    // bins partials
+  double* models;           // [S][3] in/out
+  double* lohi;             // [S][2]
+  int32_t* status;          // [S]
+};
+cudaError_t launch_fit(const FitArgs& a, cudaStream_t st);
+
+struct SolveArgs {
+  int n_sys, kind, drift, NP, NK;
+  const int32_t* sys_part;
+  const int32_t* sys_stencil;
+  const int32_t* st_off;     // [n_stencils] offset into taps/pad
+  const int32_t* st_n;       // [n_stencils]
+  const int32_t* st_drift;   // [n_stencils]
+  const int32_t* st_pattern; // [n_stencils]
+  const int8_t* taps;        // [.. * 3] (ox, oy, plane)
+  const int16_t* pad;
+  const int32_t* pat_dz;     // [NP][NPMAX]
+  const double* models;      // [S][3]
+  double* weights;           // [S][NP][NK][WPAD]
+  double* var;               // [S][NP][NK]
+  int32_t* sys_status;       // [n_sys]
+  int max_n;                 // max neighbours over stencils (smem sizing)
+};
+cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);
+
+struct PredictArgs {
+  const float* known;        // [K][H][W]
+  float* out;                // [T][H][W]
+  double* var;               // [T][H][W] or nullptr
+  int H, W, K, NP, NK, accum;
+  int64_t P;
+  const int32_t* known_z;    // [K]
+  const double* weights;     // [S][NP][NK][WPAD]
+  const double* svar;        // [S][NP][NK]
+  const double* lohi;        // [S][2]
+  const int32_t* kmap;       // [2][NKIND1] compact kind maps (x then y)
+  int nkx;
+  // generic path
+  int n_miss;
+  const int32_t* miss_z, *miss_part, *miss_pattern, *miss_planes;
+  // fast path
+  int G;
+  const int32_t* gap_part;     // [K-1]
+  const int32_t* gap_pattern;  // [(K-1) * G]
+  int num_sms;
+};
+cudaError_t launch_copy_known(const PredictArgs& a, cudaStream_t st);
+cudaError_t launch_predict_generic(const PredictArgs& a, cudaStream_t st);
+cudaError_t launch_predict_fast(const PredictArgs& a, cudaStream_t st);
+int predict_fast_supported(int G, int accum);
+
+}  // namespace vk

@@ -1,0 +1,452 @@
+// Prediction kernels of the plane-structured fill (kriging.py:499-557).
+//
+// predict_fast   : the production layout -- every missing plane reads its two
+//                  bracketing known planes (k, k+1).  Persistent CTAs walk
+//                  (in-plane tile, run of gaps) units; known-plane tiles are
+//                  streamed into a 3-deep shared-memory ring by TMA
+//                  (cp.async.bulk.tensor, OOB zero fill supplies the volume
+//                  halo) so each known plane is read from HBM once per run.
+//                  Each thread keeps one 7-wide input row in registers and
+//                  accumulates 4 columns x G missing planes in fp64 (or fp32)
+//                  with the interior stencil, in the reference tap order
+//                  (plane, oy, ox); results are clamped to the part's known
+//                  range and stored as 128-bit streaming stores; the known
+//                  planes are copied through from the same tiles.  Voxels on
+//                  the clamped-window border (x or y in {0, n-2, n-1}) are
+//                  recomputed per voxel with their own stencil kind from the
+//                  same shared-memory tiles.
+// predict_generic: any plane pattern (up to 8 planes, any dims); one thread
+//                  per missing voxel, reading the known planes through L1/L2.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "vk_kernels.h"
+
+namespace vk {
+
+namespace {
+
+__device__ __forceinline__ int compact_kind(const int32_t* kmap, int nkx, int x, int y, int W, int H) {
+  return kmap[NKIND1 + axis_kind(y, H)] * nkx + kmap[axis_kind(x, W)];
+}
+
+template <typename Acc>
+__device__ __forceinline__ Acc tap_fma(double w, float v, Acc acc);
+template <>
+__device__ __forceinline__ double tap_fma<double>(double w, float v, double acc) {
+  return fma(w, (double)v, acc);
+}
+template <>
+__device__ __forceinline__ float tap_fma<float>(double w, float v, float acc) {
+  return fmaf((float)w, v, acc);
+}
+
+// --------------------------------------------------------------------------
+// generic path
+// --------------------------------------------------------------------------
+template <typename Acc>
+__global__ void __launch_bounds__(256) predict_generic_kernel(PredictArgs a) {
+  const int i = blockIdx.y;
+  const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= a.P) return;
+  const int y = (int)(pix / a.W), x = (int)(pix - (int64_t)y * a.W);
+  const int z = a.miss_z[i], s = a.miss_part[i], p = a.miss_pattern[i];
+  const int kind = compact_kind(a.kmap, a.nkx, x, y, a.W, a.H);
+  const int64_t slot = ((int64_t)s * a.NP + p) * a.NK + kind;
+  const double* w = a.weights + slot * WPAD;
+  const int kx = axis_kind(x, a.W), ky = axis_kind(y, a.H);
+  const int x0 = kind_lo(kx), x1 = kind_hi(kx), y0 = kind_lo(ky), y1 = kind_hi(ky);
+  Acc acc = (Acc)0;
+  for (int pl = 0; pl < NPMAX; ++pl) {
+    const int k = a.miss_planes[i * NPMAX + pl];
+    if (k < 0) break;
+    const float* plane = a.known + (int64_t)k * a.P;
+    for (int oy = y0; oy < y1; ++oy)
+      for (int ox = x0; ox < x1; ++ox)
+        acc = tap_fma<Acc>(w[pl * 16 + (oy + 1) * 4 + (ox + 1)],
+                           __ldg(plane + (int64_t)(y + oy) * a.W + (x + ox)), acc);
+  }
+  const Acc lo = (Acc)a.lohi[2 * s], hi = (Acc)a.lohi[2 * s + 1];
+  acc = acc < lo ? lo : acc;
+  acc = acc > hi ? hi : acc;
+  a.out[(int64_t)z * a.P + pix] = (float)acc;
+  if (a.var) a.var[(int64_t)z * a.P + pix] = a.svar[slot];
+}
+
+__global__ void __launch_bounds__(256) copy_known_kernel(PredictArgs a) {
+  const int k = blockIdx.y;
+  const int64_t z = a.known_z[k];
+  const int64_t n4 = a.P / 4;
+  const float4* src = reinterpret_cast<const float4*>(a.known + (int64_t)k * a.P);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.P; i += (int64_t)gridDim.x * blockDim.x) {
+    if ((a.P & 3) == 0) {
+      if (i < n4) {
+        reinterpret_cast<float4*>(a.out + z * a.P)[i] = src[i];
+        if (a.var) {
+          double2 zz = make_double2(0.0, 0.0);
+          reinterpret_cast<double2*>(a.var + z * a.P)[2 * i] = zz;
+          reinterpret_cast<double2*>(a.var + z * a.P)[2 * i + 1] = zz;
+        }
+      }
+    } else {
+      a.out[z * a.P + i] = a.known[(int64_t)k * a.P + i];
+      if (a.var) a.var[z * a.P + i] = 0.0;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// fast streaming path
+// --------------------------------------------------------------------------
+constexpr int FT_WARPS = 8;
+constexpr int FT_THREADS = FT_WARPS * 32;
+constexpr int FT_TX = 128;                 // tile columns (32 lanes x 4)
+constexpr int FT_TY = 32;                  // tile rows (8 warps x 4 row steps)
+constexpr int FT_SX = FT_TX + 8;           // smem row: x0-4 .. x0+131
+constexpr int FT_SY = FT_TY + 3;           // smem rows: y0-1 .. y0+33
+constexpr int FT_BUF_FLOATS = ((FT_SX * FT_SY * 4 + 127) / 128) * 128 / 4;
+constexpr int FT_STAGES = 3;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename Acc>
+struct AccVec;
+template <>
+struct AccVec<double> {
+  static __device__ __forceinline__ double cvt(float v) { return (double)v; }
+};
+template <>
+struct AccVec<float> {
+  static __device__ __forceinline__ float cvt(float v) { return v; }
+};
+
+__device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_cs_d2(double* p, double a, double b) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+template <int G, typename Acc>
+__global__ void __launch_bounds__(FT_THREADS, 2)
+    predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
+                        int n_tiles, int chunk, int n_units) {
+  extern __shared__ __align__(128) float ring[];           // FT_STAGES x FT_BUF_FLOATS
+  __shared__ __align__(8) uint64_t full[FT_STAGES];
+  __shared__ Acc s_w[G * 32];                              // interior weights of this gap
+  __shared__ double s_var[G];
+  __shared__ Acc s_lohi[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int H = a.H, W = a.W;
+  const int64_t P = a.P;
+  const int kint = a.kmap[NKIND1 + AXIS_INTERIOR] * a.nkx + a.kmap[AXIS_INTERIOR];
+  if (tid == 0) {
+    for (int i = 0; i < FT_STAGES; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t tile_bytes = FT_SX * FT_SY * 4;
+  uint32_t load_seq = 0;                                   // loads issued so far
+  const int n_gaps = a.K - 1;
+
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const int chunk_id = u / n_tiles, tile = u - chunk_id * n_tiles;
+    const int tx = tile % n_tiles_x, ty = tile / n_tiles_x;
+    const int x0 = tx * FT_TX, y0 = ty * FT_TY;
+    const int kb = chunk_id * chunk, ke = min(n_gaps, kb + chunk);   // gaps [kb, ke)
+    const uint32_t seq0 = load_seq;
+    __syncthreads();                                       // previous unit done with the ring
+    if (tid == 0) {
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t sq = seq0 + i;
+        float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
+        mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
+        tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i);
+      }
+    }
+    load_seq += 2;
+    for (int k = kb; k < ke; ++k) {
+      const uint32_t sq_a = seq0 + (k - kb), sq_b = sq_a + 1;
+      __syncthreads();                                     // all threads done with gap k-1
+      if (tid == 0 && k + 2 <= ke) {
+        const uint32_t sq = sq_b + 1;
+        float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
+        mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
+        tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, k + 2);
+      }
+      if (k + 2 <= ke) load_seq += 1;
+      // gap constants: interior weights for the G missing planes, var, clamp
+      const int s = a.gap_part[k];
+      for (int i = tid; i < G * 32; i += FT_THREADS) {
+        const int j = i >> 5, t = i & 31;
+        const int p = a.gap_pattern[k * G + j];
+        s_w[i] = (Acc)a.weights[(((int64_t)s * a.NP + p) * a.NK + kint) * WPAD + t];
+      }
+      if (tid < G) {
+        const int p = a.gap_pattern[k * G + tid];
+        s_var[tid] = a.svar[((int64_t)s * a.NP + p) * a.NK + kint];
+      }
+      if (tid == 0) { s_lohi[0] = (Acc)a.lohi[2 * s]; s_lohi[1] = (Acc)a.lohi[2 * s + 1]; }
+      if (k == kb) mbar_wait(&full[sq_a % FT_STAGES], (sq_a / FT_STAGES) & 1);
+      mbar_wait(&full[sq_b % FT_STAGES], (sq_b / FT_STAGES) & 1);
+      __syncthreads();
+      const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
+      const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
+      const Acc lo = s_lohi[0], hi = s_lohi[1];
+      const int64_t zk = a.known_z[k];
+      const bool copy_b = (k == n_gaps - 1);
+      const int gx = x0 + 4 * lane;
+      const bool col_ok = gx < W;
+      // x-border columns inside this thread's group (handled by the fixup)
+      const bool xb0 = (gx == 0), xb1 = (gx + 4 > W - 2);
+#pragma unroll 1
+      for (int rs = 0; rs < FT_TY / FT_WARPS; ++rs) {
+        const int r = warp + rs * FT_WARPS;                // tile row
+        const int gy = y0 + r;
+        if (gy >= H || !col_ok) continue;
+        Acc acc[G][4];
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[j][c] = (Acc)0;
+        float4 selfA = make_float4(0, 0, 0, 0), selfB = selfA;
+#pragma unroll
+        for (int pl = 0; pl < 2; ++pl) {
+          const float* buf = pl ? bufB : bufA;
+#pragma unroll
+          for (int oy = -1; oy <= 2; ++oy) {
+            const float* row = buf + (r + 1 + oy) * FT_SX + 4 * lane;
+            const float4 q0 = *reinterpret_cast<const float4*>(row);
+            const float4 q1 = *reinterpret_cast<const float4*>(row + 4);
+            const float2 q2 = *reinterpret_cast<const float2*>(row + 8);
+            if (oy == 0) { if (pl) selfB = q1; else selfA = q1; }
+            Acc v[7];
+            v[0] = AccVec<Acc>::cvt(q0.w);
+            v[1] = AccVec<Acc>::cvt(q1.x);
+            v[2] = AccVec<Acc>::cvt(q1.y);
+            v[3] = AccVec<Acc>::cvt(q1.z);
+            v[4] = AccVec<Acc>::cvt(q1.w);
+            v[5] = AccVec<Acc>::cvt(q2.x);
+            v[6] = AccVec<Acc>::cvt(q2.y);
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+#pragma unroll
+              for (int ox = -1; ox <= 2; ++ox) {
+                const Acc w = s_w[j * 32 + pl * 16 + (oy + 1) * 4 + (ox + 1)];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[j][c] = fma(w, v[c + ox + 1], acc[j][c]);
+              }
+            }
+          }
+        }
+        const int64_t pix = (int64_t)gy * W + gx;
+        // known planes pass through bit-exactly (kriging.py:481)
+        st_cs_f4(a.out + zk * P + pix, selfA);
+        if (copy_b) st_cs_f4(a.out + (zk + G + 1) * P + pix, selfB);
+        if (a.var) {
+          st_cs_d2(a.var + zk * P + pix, 0.0, 0.0);
+          st_cs_d2(a.var + zk * P + pix + 2, 0.0, 0.0);
+          if (copy_b) {
+            st_cs_d2(a.var + (zk + G + 1) * P + pix, 0.0, 0.0);
+            st_cs_d2(a.var + (zk + G + 1) * P + pix + 2, 0.0, 0.0);
+          }
+        }
+        const bool row_border = (gy == 0) || (gy >= H - 2);
+        if (row_border) continue;                          // fixup writes these rows
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          float o[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            Acc t = acc[j][c];
+            t = t < lo ? lo : t;
+            t = t > hi ? hi : t;
+            o[c] = (float)t;
+          }
+          float* dst = a.out + (zk + 1 + j) * P + pix;
+          double* vdst = a.var ? a.var + (zk + 1 + j) * P + pix : nullptr;
+          if (!xb0 && !xb1) {
+            st_cs_f4(dst, make_float4(o[0], o[1], o[2], o[3]));
+            if (vdst) { st_cs_d2(vdst, s_var[j], s_var[j]); st_cs_d2(vdst + 2, s_var[j], s_var[j]); }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int xx = gx + c;
+              if (xx >= 1 && xx <= W - 3) {
+                dst[c] = o[c];
+                if (vdst) vdst[c] = s_var[j];
+              }
+            }
+          }
+        }
+      }
+      // ---- border fixup: clamped-window kinds, per voxel, from the same tiles
+      const int ty1 = min(H, y0 + FT_TY), tx1 = min(W, x0 + FT_TX);
+      const bool touches = (y0 == 0) || (ty1 >= H - 2) || (x0 == 0) || (tx1 >= W - 2);
+      if (touches) {
+        int brow[3], nbr = 0;
+        const int rc[3] = {0, H - 2, H - 1};
+        for (int q = 0; q < 3; ++q)
+          if (rc[q] >= y0 && rc[q] < ty1 && (q == 0 || rc[q] != rc[q - 1])) brow[nbr++] = rc[q];
+        int bcol[3], nbc = 0;
+        const int cc[3] = {0, W - 2, W - 1};
+        for (int q = 0; q < 3; ++q)
+          if (cc[q] >= x0 && cc[q] < tx1) bcol[nbc++] = cc[q];
+        const int rows_in = ty1 - y0, cols_in = tx1 - x0;
+        const int n_rowvox = nbr * cols_in;
+        const int n_colvox = nbc * (rows_in - nbr);
+        const int nvox = n_rowvox + n_colvox;
+        for (int idx = tid; idx < nvox * G; idx += FT_THREADS) {
+          const int j = idx / nvox, vi = idx - j * nvox;
+          int gy, gx2;
+          if (vi < n_rowvox) {
+            gy = brow[vi / cols_in];
+            gx2 = x0 + vi % cols_in;
+          } else {
+            const int t = vi - n_rowvox;
+            gx2 = bcol[t % nbc];
+            gy = y0 + t / nbc;                             // (t/nbc)-th non-border row
+            for (int q = 0; q < nbr; ++q)                  // brow ascending
+              if (brow[q] <= gy) ++gy;
+          }
+          const int p = a.gap_pattern[k * G + j];
+          const int kx = axis_kind(gx2, W), ky = axis_kind(gy, H);
+          const int kind = a.kmap[NKIND1 + ky] * a.nkx + a.kmap[kx];
+          const int64_t slot = ((int64_t)s * a.NP + p) * a.NK + kind;
+          const double* wv = a.weights + slot * WPAD;
+          Acc acc = (Acc)0;
+          for (int pl = 0; pl < 2; ++pl) {
+            const float* buf = pl ? bufB : bufA;
+            for (int oy = kind_lo(ky); oy < kind_hi(ky); ++oy)
+              for (int ox = kind_lo(kx); ox < kind_hi(kx); ++ox)
+                acc = tap_fma<Acc>(wv[pl * 16 + (oy + 1) * 4 + (ox + 1)],
+                                   buf[(gy - y0 + 1 + oy) * FT_SX + (gx2 - x0 + 4 + ox)], acc);
+          }
+          acc = acc < lo ? lo : acc;
+          acc = acc > hi ? hi : acc;
+          const int64_t o = (zk + 1 + j) * P + (int64_t)gy * W + gx2;
+          a.out[o] = (float)acc;
+          if (a.var) a.var[o] = a.svar[slot];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_copy_known(const PredictArgs& a, cudaStream_t st) {
+  const int64_t per = (a.P & 3) == 0 ? a.P / 4 : a.P;
+  dim3 grid((unsigned)std::min<int64_t>(1024, (per + 255) / 256), a.K);
+  copy_known_kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_predict_generic(const PredictArgs& a, cudaStream_t st) {
+  if (a.n_miss == 0) return cudaSuccess;
+  dim3 grid((unsigned)((a.P + 255) / 256), a.n_miss);
+  if (a.accum == 1) predict_generic_kernel<float><<<grid, 256, 0, st>>>(a);
+  else predict_generic_kernel<double><<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---- TMA descriptor (driver entry point, no -lcuda needed) ----------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+int predict_fast_supported(int G, int accum) {
+  (void)accum;
+  return G >= 1 && G <= 8;
+}
+
+template <int G, typename Acc>
+static cudaError_t launch_fast_t(const CUtensorMap& map, const PredictArgs& a, cudaStream_t st) {
+  auto kern = predict_fast_kernel<G, Acc>;
+  const size_t smem = (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, FT_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  occ = std::max(1, occ);
+  const int ntx = (a.W + FT_TX - 1) / FT_TX, nty = (a.H + FT_TY - 1) / FT_TY;
+  const int n_tiles = ntx * nty, n_gaps = a.K - 1;
+  const int resident = a.num_sms * occ;
+  // gap runs: long enough to amortise the extra plane per run, short enough
+  // that (tiles x runs) covers the resident CTAs several times
+  int chunk = std::max(1, (int)((int64_t)n_tiles * n_gaps / ((int64_t)resident * 6)));
+  chunk = std::min(std::max(chunk, std::min(4, n_gaps)), n_gaps);
+  const int n_chunks = (n_gaps + chunk - 1) / chunk;
+  const int n_units = n_tiles * n_chunks;
+  const int grid = std::min(n_units, resident);
+  kern<<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_predict_fast(const PredictArgs& a, cudaStream_t st) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {(cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)a.K};
+  const cuuint64_t strides[2] = {(cuuint64_t)a.W * 4, (cuuint64_t)a.P * 4};
+  const cuuint32_t box[3] = {FT_SX, FT_SY, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)a.known, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  const bool f32 = a.accum == 1;
+  switch (a.G) {
+#define VK_CASE(g)                                                                      \
+  case g:                                                                               \
+    return f32 ? launch_fast_t<g, float>(map, a, st) : launch_fast_t<g, double>(map, a, st);
+    VK_CASE(1) VK_CASE(2) VK_CASE(3) VK_CASE(4) VK_CASE(5) VK_CASE(6) VK_CASE(7) VK_CASE(8)
+#undef VK_CASE
+    default:
+      return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace vk

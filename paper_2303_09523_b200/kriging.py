@@ -1,0 +1,327 @@
+"""Drop-in kriging entry points backed by the sm_100a kernels.
+
+Mirrors the reference's public API (``volkrig.kriging``):
+
+* ``VariogramModel``                       kriging.py:44-84
+* ``fit_variogram(samples, kind, n_bins, max_pairs, seed)``   kriging.py:264-328
+* ``fill_missing(grid, model, drift, return_variance)``       kriging.py:458-557
+
+with the same argument meaning, return types and exception classes.  The
+numerics run on the GPU through the C ABI in ``include/volkrig_b200.h``; there
+is no CPU fallback -- without a CUDA device or the built library these raise.
+One optional keyword is added: ``accum`` ("fp64" default, as the reference;
+"fp32" accumulates the prediction stencil in fp32, solves stay fp64).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import (DeviceError, DeviceUnsupported, InsufficientSamples,
+                     NoKnownNeighbors, raise_for_status)
+from .model import VolumeGrid
+
+VARIOGRAM_KINDS = ("exponential", "gaussian", "spherical")
+WPAD = 128
+
+
+@dataclass
+class VariogramModel:
+    """Isotropic variogram nugget + (sill - nugget) * shape(h / range_len)."""
+
+    kind: str
+    nugget: float
+    sill: float
+    range_len: float
+
+    def __post_init__(self):
+        if self.kind not in VARIOGRAM_KINDS:
+            raise ValueError(f"kind must be one of {VARIOGRAM_KINDS}")
+        if self.nugget < 0 or self.sill < self.nugget or self.range_len <= 0:
+            raise ValueError("need 0 <= nugget <= sill and range_len > 0")
+
+    def gamma(self, h):
+        h = np.asarray(h, dtype=np.float64)
+        ps, r = self.sill - self.nugget, self.range_len
+        if self.kind == "exponential":
+            shape = 1.0 - np.exp(-3.0 * h / r)
+        elif self.kind == "gaussian":
+            shape = 1.0 - np.exp(-3.0 * (h / r) ** 2)
+        else:
+            t = np.minimum(h / r, 1.0)
+            shape = 1.5 * t - 0.5 * t ** 3
+        return np.where(h == 0.0, 0.0, self.nugget + ps * shape)
+
+    def covariance(self, h):
+        h = np.asarray(h, dtype=np.float64)
+        if self.sill <= 0.0:
+            return np.where(h == 0.0, 1.0, 0.0)
+        return self.sill - self.gamma(h)
+
+    def as_array(self) -> np.ndarray:
+        return np.array([self.nugget, self.sill, self.range_len], dtype=np.float64)
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("a CUDA device is required (no CPU fallback)")
+    return torch
+
+
+def _stream_handle(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class KrigingPlan:
+    """A device plan: geometry tables, stencil systems and workspace for one
+    grid layout (``vk_plan``).  ``execute`` is stream-ordered and async;
+    ``finish`` synchronises and raises the reference's exceptions."""
+
+    def __init__(self, height, width, depth, known_z, n_subparts=1,
+                 kind="exponential", drift="linear", accum="fp64", fit=True,
+                 n_bins=15, max_pairs=100_000, seed=0, force_generic=False,
+                 part_len=0):
+        if callable(drift):
+            raise DeviceUnsupported("a callable drift cannot cross the C ABI; "
+                                    "use 'linear' or 'constant'")
+        if drift not in _lib.DRIFT_IDS:
+            raise ValueError(f"unknown drift {drift!r}")
+        if kind not in _lib.KIND_IDS:
+            raise ValueError(f"kind must be one of {VARIOGRAM_KINDS}")
+        if accum not in _lib.ACCUM_IDS:
+            raise ValueError("accum must be 'fp64' or 'fp32'")
+        _torch()
+        self.lib = _lib.load()
+        kz = np.ascontiguousarray(known_z, dtype=np.int32)
+        self._kz = kz
+        self.height, self.width, self.depth = int(height), int(width), int(depth)
+        self.n_known = len(kz)
+        self.n_subparts = int(n_subparts)
+        self.kind, self.drift, self.accum, self.fit = kind, drift, accum, bool(fit)
+        desc = _lib.PlanDesc(
+            self.height, self.width, self.depth, len(kz),
+            kz.ctypes.data_as(C.POINTER(C.c_int32)), self.n_subparts,
+            _lib.KIND_IDS[kind], _lib.DRIFT_IDS[drift], _lib.ACCUM_IDS[accum],
+            int(n_bins), int(max_pairs), int(seed), int(bool(fit)),
+            _lib.FLAG_FORCE_GENERIC if force_generic else 0)
+        if part_len:
+            raise DeviceUnsupported("explicit part_len is not supported")
+        handle = C.c_void_p()
+        raise_for_status(self.lib.vk_plan_create(C.byref(desc), C.byref(handle)))
+        self._h = handle
+        self._info = None
+
+    # -- introspection ------------------------------------------------------
+    @property
+    def info(self) -> dict:
+        inf = _lib.PlanInfo()
+        raise_for_status(self.lib.vk_plan_get_info(self._h, C.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in _lib.PlanInfo._fields_}
+
+    @property
+    def interpolated_voxels(self) -> int:
+        return int(self.info["interpolated_voxels"])
+
+    # -- execution ------------------------------------------------------------
+    def execute(self, known, out, var=None, models=None, stream=None) -> None:
+        torch = _torch()
+        K, H, W = self.n_known, self.height, self.width
+        if not (known.is_cuda and known.dtype == torch.float32 and known.is_contiguous()
+                and tuple(known.shape) == (K, H, W)):
+            raise ValueError(f"known must be a contiguous CUDA float32 [{K},{H},{W}] tensor")
+        if not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()
+                and tuple(out.shape) == (self.depth, H, W)):
+            raise ValueError("out must be a contiguous CUDA float32 [depth,H,W] tensor")
+        vptr = None
+        if var is not None:
+            if not (var.is_cuda and var.dtype == torch.float64 and var.is_contiguous()
+                    and tuple(var.shape) == (self.depth, H, W)):
+                raise ValueError("var must be a contiguous CUDA float64 [depth,H,W] tensor")
+            vptr = var.data_ptr()
+        mptr = None
+        if not self.fit:
+            if models is None:
+                raise ValueError("models are required for a plan without fitting")
+            self._models_in = np.ascontiguousarray(models, dtype=np.float64).reshape(
+                self.n_subparts, 3)
+            mptr = self._models_in.ctypes.data
+        raise_for_status(self.lib.vk_plan_execute(
+            self._h, known.data_ptr(), mptr, out.data_ptr(), vptr,
+            _stream_handle(stream)))
+
+    def finish(self, stream=None):
+        """Synchronise; return (models [S,3], lohi [S,2]) or raise."""
+        models = np.zeros((self.n_subparts, 3))
+        lohi = np.zeros((self.n_subparts, 2))
+        failed = C.c_int32(-1)
+        code = self.lib.vk_plan_finish(self._h, _stream_handle(stream), C.byref(failed),
+                                       models.ctypes.data, lohi.ctypes.data)
+        ctx = f"sub-part {failed.value}" if failed.value >= 0 and self.n_subparts > 1 else ""
+        raise_for_status(code, ctx)
+        return models, lohi
+
+    def systems(self):
+        """Solved stencils: (weights [n,128], variance [n], ids [n,4])."""
+        n = self.info["n_systems"]
+        w = np.zeros((n, WPAD))
+        v = np.zeros(n)
+        ids = np.zeros((n, 4), np.int32)
+        raise_for_status(self.lib.vk_plan_get_systems(self._h, w.ctypes.data, v.ctypes.data,
+                                                      ids.ctypes.data))
+        return w, v, ids
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.vk_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_PLANS: "OrderedDict[tuple, KrigingPlan]" = OrderedDict()
+
+
+def cached_plan(**kw) -> KrigingPlan:
+    torch = _torch()
+    key = tuple(sorted((k, tuple(v) if isinstance(v, (list, np.ndarray)) else v)
+                       for k, v in kw.items())) + (torch.cuda.current_device(),)
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = KrigingPlan(**kw)
+        _PLANS[key] = plan
+        while len(_PLANS) > 8:
+            _PLANS.popitem(last=False)[1].close()
+    else:
+        _PLANS.move_to_end(key)
+    return plan
+
+
+# --------------------------------------------------------------------------
+# fit_variogram                                          kriging.py:264-328
+# --------------------------------------------------------------------------
+
+def _as_coord_value_arrays(samples):
+    if isinstance(samples, tuple) and len(samples) == 2:
+        coords = np.asarray(samples[0], dtype=np.float64).reshape(-1, 3)
+        values = np.asarray(samples[1], dtype=np.float64).reshape(-1)
+    else:
+        coords = np.asarray([s[0] for s in samples], dtype=np.float64)
+        values = np.asarray([s[1] for s in samples], dtype=np.float64)
+    if len(coords) != len(values):
+        raise ValueError("coords and values must align")
+    return coords, values
+
+
+def fit_variogram(samples, kind: str = "exponential", n_bins: int = 15,
+                  max_pairs: int = 100_000, seed: int = 0) -> VariogramModel:
+    """Empirical semivariogram + bounded TRF fit, on the device."""
+    if kind not in VARIOGRAM_KINDS:
+        raise ValueError(f"kind must be one of {VARIOGRAM_KINDS}")
+    coords, values = _as_coord_value_arrays(samples)
+    m = len(values)
+    if m * (m - 1) // 2 < 30:
+        raise InsufficientSamples(f"{m} samples give {m * (m - 1) // 2} pairs; need >= 30")
+    torch = _torch()
+    lib = _lib.load()
+    c_d = torch.from_numpy(np.ascontiguousarray(coords)).cuda()
+    v_d = torch.from_numpy(np.ascontiguousarray(values)).cuda()
+    out = np.zeros(3)
+    raise_for_status(lib.vk_fit_variogram_samples(
+        c_d.data_ptr(), v_d.data_ptr(), m, _lib.KIND_IDS[kind], int(n_bins),
+        int(max_pairs), int(seed), out.ctypes.data, _stream_handle(None)))
+    return VariogramModel(kind, float(out[0]), float(out[1]), float(out[2]))
+
+
+# --------------------------------------------------------------------------
+# fill_missing                                           kriging.py:458-557
+# --------------------------------------------------------------------------
+
+def _scan_grid(data_d, mask_d):
+    """Device validate() + plane structure: per-plane (#missing, #nan,
+    #nan != mask, #known non-finite)."""
+    torch = _torch()
+    lib = _lib.load()
+    T = data_d.shape[0]
+    P = data_d[0].numel()
+    counts = torch.empty((T, 4), dtype=torch.int32, device=data_d.device)
+    raise_for_status(lib.vk_grid_scan(data_d.data_ptr(), mask_d.data_ptr(), T, P,
+                                      counts.data_ptr(), _stream_handle(None)))
+    return counts.cpu().numpy()
+
+
+def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
+                 return_variance: bool = False, *, accum: str = "fp64"):
+    """Fill every missing voxel by kriging from known voxels only.
+
+    Known voxels pass through bit-exactly; predictions never read other
+    predictions.  Host (numpy) grids come back as numpy, CUDA grids as CUDA
+    tensors.  Only the plane-structured layout (the production case,
+    kriging.py:485-487) runs on the device in this release; other masks raise
+    ``DeviceUnsupported``.
+    """
+    torch = _torch()
+    if callable(drift):
+        raise DeviceUnsupported("a callable drift cannot cross the C ABI")
+    on_dev = grid.on_device
+    data = grid.data
+    if on_dev:
+        data_d, mask_d = data, grid.missing_mask.view(torch.uint8)
+    else:
+        data_d = torch.from_numpy(data).cuda()
+        mask_d = torch.from_numpy(grid.missing_mask.view(np.uint8)).cuda()
+    T, H, W = data_d.shape
+    counts = _scan_grid(data_d, mask_d)
+    if counts[:, 2].any():
+        raise ValueError("missing_mask out of sync with NaN sentinel")
+    if counts[:, 3].any():
+        raise ValueError("known voxels must be finite")
+    n_missing = counts[:, 0].astype(np.int64)
+    if n_missing.sum() == 0:                                 # kriging.py:469-473
+        out = grid.copy()
+        if return_variance:
+            zeros = (torch.zeros(data_d.shape, dtype=torch.float64, device=data_d.device)
+                     if on_dev else np.zeros(data.shape, dtype=np.float64))
+            return out, zeros
+        return out
+    P = H * W
+    known_z = np.nonzero(n_missing == 0)[0].astype(np.int32)
+    if len(known_z) == 0:
+        raise NoKnownNeighbors("grid has no known voxels at all")
+    if not np.all((n_missing == 0) | (n_missing == P)):
+        raise DeviceUnsupported(
+            "only plane-structured masks (whole known / missing planes) run on "
+            "the device; the per-voxel window path is not implemented yet")
+    if drift not in _lib.DRIFT_IDS:
+        raise ValueError(f"unknown drift {drift!r}")
+    plan = cached_plan(height=H, width=W, depth=T, known_z=known_z.tolist(), n_subparts=1,
+                       kind=model.kind, drift=drift, accum=accum, fit=False)
+    lib = _lib.load()
+    known_d = torch.empty((len(known_z), H, W), dtype=torch.float32, device=data_d.device)
+    raise_for_status(lib.vk_gather_planes(data_d.data_ptr(), known_z.ctypes.data,
+                                          len(known_z), P, known_d.data_ptr(),
+                                          _stream_handle(None)))
+    out_d = torch.empty((T, H, W), dtype=torch.float32, device=data_d.device)
+    var_d = (torch.empty((T, H, W), dtype=torch.float64, device=data_d.device)
+             if return_variance else None)
+    plan.execute(known_d, out_d, var_d, models=model.as_array()[None, :])
+    plan.finish()
+    if on_dev:
+        out_grid = VolumeGrid(out_d, torch.zeros_like(grid.missing_mask), grid.origin_offset)
+        return (out_grid, var_d) if return_variance else out_grid
+    out_grid = VolumeGrid(out_d.cpu().numpy(), np.zeros_like(grid.missing_mask),
+                          grid.origin_offset)
+    if return_variance:
+        return out_grid, var_d.cpu().numpy()
+    return out_grid

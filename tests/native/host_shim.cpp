@@ -1,0 +1,52 @@
+// TEST-ONLY host build of the header-only pieces of the device code (PCG64
+// pair sampling, TRF fit) so tests/ can check them against numpy/scipy on a
+// machine without a GPU.  Never linked into the product library.
+#include <cstdint>
+#include <vector>
+#include "pcg64.h"
+#include "trf.h"
+
+using namespace vk;
+
+extern "C" {
+
+void vkh_pcg_state(uint64_t seed, uint64_t* out4) {
+  Pcg64 g = pcg64_from_seed(seed);
+  out4[0] = (uint64_t)(g.state >> 64); out4[1] = (uint64_t)g.state;
+  out4[2] = (uint64_t)(g.inc >> 64);   out4[3] = (uint64_t)g.inc;
+}
+
+uint64_t vkh_raw(uint64_t seed, uint64_t r) { return pcg_raw_at(pcg64_from_seed(seed), r); }
+
+// Draw 2*n Lemire-bounded integers in [0, m) as the compaction of accepted
+// 32-bit halves (what the device kernel computes in parallel).
+int vkh_draws(uint64_t seed, uint32_t m, int64_t n, int64_t* out) {
+  Pcg64 g = pcg64_from_seed(seed);
+  const uint32_t thr = lemire_threshold(m);
+  int64_t k = 0;
+  u128 st = g.state;
+  while (k < 2 * n) {
+    st = st * pcg_mult() + g.inc;
+    const uint64_t raw = pcg_output(st);
+    const uint32_t halves[2] = {(uint32_t)raw, (uint32_t)(raw >> 32)};
+    for (int h = 0; h < 2 && k < 2 * n; ++h) {
+      const uint64_t prod = (uint64_t)halves[h] * m;
+      if ((uint32_t)prod >= thr) out[k++] = (int64_t)(prod >> 32);
+    }
+  }
+  return 0;
+}
+
+int vkh_trf(int kind, int nb, const double* h, const double* gemp, const double* w,
+            const double* x0, const double* lb, const double* ub, double* x_out,
+            int32_t* info) {
+  TrfProblem P;
+  P.kind = kind; P.nb = nb;
+  for (int i = 0; i < nb; ++i) { P.h[i] = h[i]; P.gemp[i] = gemp[i]; P.w[i] = w[i]; }
+  TrfResult r = trf_fit(P, x0, lb, ub);
+  for (int i = 0; i < 3; ++i) x_out[i] = r.x[i];
+  info[0] = r.status; info[1] = r.nfev; info[2] = r.iterations;
+  return r.status;
+}
+
+}

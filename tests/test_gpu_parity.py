@@ -1,0 +1,137 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle on the
+same seeded inputs (tolerances from BASELINE.json: fp64 max-abs <= 1e-6 of
+the known intensity range, fp32 <= 1e-3; known planes bit-exact)."""
+
+import numpy as np
+import pytest
+
+from oracle import kriging_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-6
+TOL32 = 1e-3
+
+
+def _rng(a):
+    return float(np.max(a) - np.min(a))
+
+
+def _smooth_grid(seed, T, H, W, f, quant=True):
+    r = np.random.default_rng(seed)
+    base = r.normal(size=(T, H, W)).cumsum(1).cumsum(2)
+    base = (base - base.min()) / (base.max() - base.min()) * 200 + 20
+    if quant:
+        base = np.rint(base)
+    data = base.astype(np.float32)
+    mask = np.ones(data.shape, bool)
+    mask[::f] = False
+    data[mask] = np.nan
+    return data, mask
+
+
+def test_pairs_bit_exact(cuda):
+    torch = cuda
+    from paper_2303_09523_b200 import _lib
+    lib = _lib.load()
+    import ctypes as C
+    for m in (500, 81_920, 327_680, 2_359_296, 9_437_184):
+        ii = torch.empty(100_000, dtype=torch.int32, device="cuda")
+        jj = torch.empty_like(ii)
+        n = C.c_int64()
+        assert lib.vk_sample_pairs(m, 100_000, 0, ii.data_ptr(), jj.data_ptr(), C.byref(n),
+                                   torch.cuda.current_stream().cuda_stream) == 0
+        g = np.random.default_rng(0)
+        ei = g.integers(0, m, size=100_000)
+        ej = g.integers(0, m, size=100_000)
+        assert n.value == 100_000
+        assert np.array_equal(ii.cpu().numpy(), ei) and np.array_equal(jj.cpu().numpy(), ej)
+
+
+@pytest.mark.parametrize("f", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("drift", ["linear", "constant"])
+def test_fill_missing_parity(cuda, f, drift):
+    from paper_2303_09523_b200 import VariogramModel, VolumeGrid, fill_missing
+    data, mask = _smooth_grid(f, 2 * f + 1 + f, 21, 28, f)
+    m = VariogramModel("exponential", 0.5, 400.0, 15.0)
+    got, gv = fill_missing(VolumeGrid(data, mask), m, drift, return_variance=True)
+    exp, ev = O.fill_missing(data, mask, O.Model("exponential", 0.5, 400.0, 15.0), drift, True)
+    known = ~mask
+    assert np.array_equal(got.data[known], data[known])
+    assert not got.missing_mask.any()
+    err = np.abs(got.data.astype(np.float64) - exp).max() / _rng(data[known])
+    assert err <= TOL64, err
+    assert np.allclose(gv, ev, rtol=1e-7, atol=1e-9 * m.sill)
+
+
+@pytest.mark.parametrize("W", [64, 128, 200])
+def test_fast_matches_generic_and_oracle(cuda, W):
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("head", 40, W, 9, 4, n_subparts=2, seed=7)
+    ks = known_slices(cfg)
+    kd = torch.from_numpy(ks).cuda()
+    a = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts)
+    assert a.plan.info["fast_path"] == 1
+    oa, va = a.run(kd, return_variance=True)
+    ma, _ = a.finish()
+    b = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts,
+                     force_generic=True)
+    ob, vb = b.run(kd, return_variance=True)
+    b.finish()
+    oa, ob = oa.cpu().numpy(), ob.cpu().numpy()
+    assert np.array_equal(oa, ob), np.abs(oa - ob).max()
+    assert torch.equal(va, vb)
+    ref, rvar, rmodels = O.reconstruct_zparts(ks, cfg.factor, cfg.n_subparts,
+                                              return_variance=True)
+    err = np.abs(oa.astype(np.float64) - ref).max() / _rng(ks)
+    assert err <= TOL64, err
+
+
+def test_c1_head_pipeline(cuda):
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.phantoms import CONFIGS, known_slices
+    cfg = CONFIGS["C1"]
+    ks = known_slices(cfg)
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts)
+    out, _ = zk.run(torch.from_numpy(ks).cuda())
+    models, _ = zk.finish()
+    ref, _, rmodels = O.reconstruct_zparts(ks, cfg.factor, cfg.n_subparts)
+    got = out.cpu().numpy()
+    assert np.array_equal(got[::cfg.factor], ks)
+    err = np.abs(got.astype(np.float64) - ref).max() / _rng(ks)
+    assert err <= TOL64, err
+    assert np.abs(np.rint(got) - np.rint(ref)).max() <= 1
+    for m, r in zip(models, rmodels):
+        assert abs(m.nugget - r.nugget) <= 1e-5 * r.sill
+        assert abs(m.sill - r.sill) <= 1e-5 * r.sill
+        assert abs(m.range_len - r.range_len) <= 1e-3 * r.range_len
+
+
+def test_fp32_accumulation(cuda):
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("brain", 64, 96, 9, 4, n_subparts=2, seed=5)
+    ks = known_slices(cfg)
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts,
+                      accum="fp32")
+    out, _ = zk.run(torch.from_numpy(ks).cuda())
+    zk.finish()
+    ref, _, _ = O.reconstruct_zparts(ks, cfg.factor, cfg.n_subparts)
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref).max() / _rng(ks)
+    assert err <= TOL32, err
+
+
+def test_fit_variogram_samples(cuda):
+    from paper_2303_09523_b200 import fit_variogram
+    r = np.random.default_rng(3)
+    for m in (200, 3000):
+        c = r.integers(0, 40, size=(m, 3)).astype(float)
+        v = np.sin(c[:, 0] / 7) * 10 + c[:, 2] + r.normal(size=m)
+        got = fit_variogram((c, v))
+        exp = O.fit_variogram((c, v))
+        assert abs(got.sill - exp.sill) <= 1e-4 * exp.sill, (got, exp)
+        assert abs(got.range_len - exp.range_len) <= 1e-3 * exp.range_len, (got, exp)
