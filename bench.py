@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the kriging interpolation path (interpolated voxels/s).
+
+Workload (BASELINE.json configs[3], the configuration the metric is quoted on
+"at 1/2/4/8 B200"): the C4 high-dynamic-range spine phantom, 512x512 12-bit
+slices, K = 256 known slices per GPU, upsampling factor 8 (7 missing planes
+per gap), 32 Z sub-parts per GPU, reference defaults (exponential variogram,
+linear drift, fp64, no variance).  A step is one pass of the whole kriging
+path over the resident stack: plane stats -> pair draw -> binned
+semivariogram -> TRF fit -> 112 stencil solves per part -> streaming
+prediction of 467,927,040 voxels (per GPU).  Scaling is weak: under torchrun
+every rank owns its own 256-slice stack and receives a one-slice halo from
+the next rank over NCCL inside the timed step.
+
+``--impl reference`` times the reference algorithm on the host cores instead
+(the oracle port of volkrig's fit_variogram + fill_missing, multiprocessing
+over sub-parts, a bounded sample of the same workload per step).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "interpolated voxels/sec (kriging path)"
+UNIT = "voxel/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+def _profile_traffic(name: str):
+    """dram bytes per launch of the prediction kernel from the committed ncu
+    summary (profiles/*.json), or None."""
+    path = os.path.join(ROOT, "profiles", "predict_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        rows = []
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": rows[0][1],
+                "power_w_max": max(r[2] for r in rows), "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------
+# CPU reference arm (oracle port of the reference algorithm)
+# --------------------------------------------------------------------------
+
+def _cpu_worker(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import kriging_oracle as O
+    slices, b, e, factor = args
+    out, _, _ = O.reconstruct_zpart(slices, b, e, factor)
+    return out.shape[0]
+
+
+def cpu_reference_sample(ks, factor, n_parts, cores, pool=None, n_sample=None):
+    """Run the reference algorithm on a bounded sample of sub-parts with a
+    process pool; returns (voxels, seconds, sample description)."""
+    from oracle import kriging_oracle as O
+    ranges = O.subpart_ranges(ks.shape[0], n_parts)
+    n_sample = n_sample or min(len(ranges), cores)
+    sel = ranges[:n_sample]
+    H, W = ks.shape[1:]
+    vox = sum((e - b) * (factor - 1) * H * W for b, e in sel)
+    jobs = [(ks[b:e + 1].copy(), 0, e - b, factor) for b, e in sel]
+    t0 = time.perf_counter()
+    if pool is None:
+        for j in jobs:
+            _cpu_worker(j)
+    else:
+        pool.map(_cpu_worker, jobs)
+    dt = time.perf_counter() - t0
+    return vox, dt, f"{n_sample} of {n_parts} sub-parts ({vox} voxels), pool of {cores}"
+
+
+def _host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, ks):
+    import multiprocessing as mp
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    cores = _host_cores()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_worker, [(ks[:2].copy(), 0, 1, cfg.factor)] * cores)   # warm
+        for _ in range(args.warmup):
+            cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool, n_sample=min(cores, 4))
+        times, vox = [], 0
+        for _ in range(args.steps):
+            v, dt, sample = cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool)
+            times.append(dt)
+            vox = v
+    ms = 1e3 * float(np.median(times))
+    value = vox / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded C4 HDR spine phantom)",
+        "config": _config(cfg, args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(cfg, args, world):
+    return {"workload": f"{cfg.name} {cfg.height}x{cfg.width}, K={cfg.n_known} known slices/GPU, "
+                        f"factor {cfg.factor}, {cfg.n_subparts} Z sub-parts/GPU",
+            "kind": "exponential", "drift": "linear", "accum": args.accum,
+            "return_variance": bool(args.variance), "max_pairs": 100000, "seed": 0,
+            "parallelism": f"zparts x {world} GPU (weak, 1-slice NCCL halo)",
+            "l2": "no flush: per-GPU inputs 268 MB and outputs 2.1 GB exceed the 126 MB L2",
+            "pair_draws": "redrawn every step"}
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+
+def run_gpu(args, cfg, ks):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.zshard import core_planes, exchange_halo
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    owned = torch.from_numpy(ks).to(dev)
+    has_halo = rank < world - 1
+    K_loc = cfg.n_known + int(has_halo)
+    H, W, f = cfg.height, cfg.width, cfg.factor
+    zk = ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, redraw_pairs=True,
+                      part_len=cfg.n_known // cfg.n_subparts)
+    zk.plan.set_timing(max(1, args.steps))
+    stack = torch.empty((K_loc, H, W), dtype=torch.float32, device=dev)
+    stack[:cfg.n_known].copy_(owned)
+    out, var = zk.allocate(bool(args.variance))
+    vox_local = zk.interpolated_voxels
+    kernels = zk.plan.info
+
+    def step():
+        if world > 1:
+            halo = exchange_halo(stack[0], rank, world)
+            if halo is not None:
+                stack[cfg.n_known].copy_(halo)
+        zk.run(stack, out, var)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    zk.finish()
+    kpe = zk.plan.info["kernels_per_execute"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    pred_ms, stage_acc = [], {}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    zk.finish()
+    for back in range(args.steps):          # per-launch stage events, read after
+        st = zk.plan.stage_ms(back)
+        pred_ms.append(st["predict"])
+        for k2, v in st.items():
+            stage_acc[k2] = stage_acc.get(k2, 0.0) + v
+    t_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+        v = torch.tensor([float(vox_local)], device=dev, dtype=torch.float64)
+        dist.all_reduce(v)
+        vox_total = float(v.item())
+    else:
+        vox_total = float(vox_local)
+    ms_step = t_ms / args.steps
+    value = vox_total / (ms_step / 1e3)
+
+    # roofline of the prediction kernel (algorithmic bytes per launch)
+    hbm_peak, sm_max, peak_kind = _peaks()
+    T = zk.depth
+    alg_bytes = 4 * (K_loc + T) * H * W + (8 * T * H * W if args.variance else 0)
+    pred_avg = float(np.mean(pred_ms))
+    achieved = alg_bytes / (pred_avg / 1e3) / 1e9
+    fp64_cap = 148 * 64 * sm_max * 1e6 / 32           # vox/s at 32 DFMA per voxel
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": _profile_traffic(args.accum),
+            "kernel": "predict_fast_kernel", "bytes_per_launch": alg_bytes,
+            "launch_ms": pred_avg, "peak_kind": peak_kind,
+            "fp64_pipe_frac": (vox_local / (pred_avg / 1e3)) / fp64_cap
+            if args.accum == "fp64" else None}
+    stages = {k2: v / args.steps for k2, v in stage_acc.items()}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(args, cfg, ks, zk, stream)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import multiprocessing as mp
+        cores = _host_cores()
+        with mp.get_context("fork").Pool(cores) as pool:
+            pool.map(_cpu_worker, [(ks[:2].copy(), 0, 1, cfg.factor)] * cores)
+            v, dt, sample = cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool)
+        cpu = {"value": v / dt, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.accum == "fp64" else "f32",
+            "data": "synthetic (seeded C4 HDR spine phantom)",
+            "config": _config(cfg, args, world),
+            "roofline": roof, "stage_ms": stages, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": kpe * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, cfg, ks, zk, stream):
+    """Same metric through the public API from pinned host buffers: H2D of
+    the known slices + kriging path + D2H of the reconstructed volume."""
+    import torch
+    H, W = cfg.height, cfg.width
+    K = cfg.n_known
+    host_in = torch.from_numpy(ks).pin_memory()
+    from paper_2303_09523_b200 import ZPartKriging
+    zk1 = ZPartKriging(K, H, W, cfg.factor, cfg.n_subparts, accum=args.accum, redraw_pairs=True)
+    dev_in = torch.empty((K, H, W), dtype=torch.float32, device="cuda")
+    out, var = zk1.allocate(bool(args.variance))
+    host_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+    host_var = torch.empty(var.shape, dtype=torch.float64).pin_memory() if var is not None else None
+
+    def step():
+        dev_in.copy_(host_in, non_blocking=True)
+        zk1.run(dev_in, out, var)
+        host_out.copy_(out, non_blocking=True)
+        if var is not None:
+            host_var.copy_(var, non_blocking=True)
+
+    for _ in range(2):
+        step()
+    zk1.finish()
+    steps = max(2, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    zk1.finish()
+    ms = e0.elapsed_time(e1) / steps
+    d2h = out.numel() * 4 + (var.numel() * 8 if var is not None else 0)
+    return {"value": zk1.interpolated_voxels / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": K * H * W * 4, "d2h_bytes_per_step": d2h,
+            "ms_per_step": ms, "steps": steps}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--accum", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--variance", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    args.warmup = max(3, args.warmup)
+
+    from paper_2303_09523_b200.phantoms import CONFIGS, known_slices
+    import dataclasses
+    base = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    cfg = dataclasses.replace(base, seed=base.seed + 1000 * rank) if rank else base
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        return run_reference(args, base, known_slices(base))
+    return run_gpu(args, cfg, known_slices(cfg))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -72,9 +72,14 @@ typedef struct {
   uint64_t seed;           /* 0                                           */
   int32_t fit_variogram;   /* 1: per-part device fit; 0: models supplied  */
   int32_t flags;           /* VK_FLAG_*                                   */
+  int32_t part_len;        /* known slices per part q (0: K / S); part s =
+                              [s*q, (s+1)*q], the last part takes the rest  */
 } vk_plan_desc;
 
 #define VK_FLAG_FORCE_GENERIC 1   /* disable the streaming fast kernel (testing) */
+#define VK_FLAG_REDRAW_PAIRS 2    /* redraw the pair tables on every execute
+                                     (default: drawn once per plan, they depend
+                                     only on geometry and seed)               */
 
 /* Replaces: the window/stencil setup of fill_missing (kriging.py:485-515)
  * and the partition of SPEC.md:392-400.  Host-side, O(K + H + W). */
@@ -113,6 +118,15 @@ typedef struct {
   int64_t interpolated_voxels;
 } vk_plan_info;
 int vk_plan_get_info(const vk_plan* plan, vk_plan_info* info);
+
+/* Stage timing with CUDA events recorded on the execute stream:
+ * stats, pairs, bins, fit, solve, predict (ms; 0 for skipped stages).
+ * set_timing(ring): keep events of the last `ring` executes (0 disables).
+ * stage_ms(back): times of the execute `back` calls ago (0 = latest);
+ * synchronises on that execute's last event. */
+#define VK_N_STAGES 6
+int vk_plan_set_timing(vk_plan* plan, int ring);
+int vk_plan_stage_ms(vk_plan* plan, int back, float* ms);
 
 /* Copies solved stencils to host: weights f64 [n_systems][128] padded
  * ([plane][oy+1][ox+1]), variance f64 [n_systems], and per system (part,

@@ -28,6 +28,9 @@ KIND_IDS = {"exponential": 0, "gaussian": 1, "spherical": 2}
 DRIFT_IDS = {"linear": 0, "constant": 1}
 ACCUM_IDS = {"fp64": 0, "fp32": 1}
 FLAG_FORCE_GENERIC = 1
+FLAG_REDRAW_PAIRS = 2
+N_STAGES = 6
+STAGES = ("stats", "pairs", "bins", "fit", "solve", "predict")
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -39,7 +42,8 @@ class PlanDesc(C.Structure):
                 ("n_known", C.c_int32), ("known_z", C.POINTER(C.c_int32)),
                 ("n_subparts", C.c_int32), ("kind", C.c_int32), ("drift", C.c_int32),
                 ("accum", C.c_int32), ("n_bins", C.c_int32), ("max_pairs", C.c_int64),
-                ("seed", C.c_uint64), ("fit_variogram", C.c_int32), ("flags", C.c_int32)]
+                ("seed", C.c_uint64), ("fit_variogram", C.c_int32), ("flags", C.c_int32),
+                ("part_len", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -60,6 +64,8 @@ SIGNATURES = {
                                  C.c_void_p, C.c_void_p]),
     "vk_plan_get_info": (C.c_int, [C.c_void_p, C.POINTER(PlanInfo)]),
     "vk_plan_get_systems": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vk_plan_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "vk_plan_stage_ms": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "vk_fit_variogram_samples": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                            C.c_int32, C.c_int64, C.c_uint64, C.c_void_p,
                                            C.c_void_p]),

@@ -28,10 +28,10 @@ from .errors import TooFewSlices
 from .kriging import KrigingPlan, VariogramModel, _torch
 
 
-def subpart_ranges(n_known: int, n_subparts: int) -> list[tuple[int, int]]:
+def subpart_ranges(n_known: int, n_subparts: int, part_len: int = 0) -> list[tuple[int, int]]:
     """Known-slice index ranges [b, e] of each part (inclusive halo)."""
-    q = n_known // n_subparts
-    if q < 1 or n_known < 2:
+    q = part_len or n_known // n_subparts
+    if q < 1 or n_known < 2 or (n_subparts - 1) * q > n_known - 1:
         raise TooFewSlices(f"{n_known} slices cannot form {n_subparts} sub-parts")
     out = []
     for s in range(n_subparts):
@@ -51,25 +51,29 @@ class ZPartKriging:
     ``run(known)`` launches stats -> pair table -> bins -> fit -> solve ->
     predict on the current CUDA stream (asynchronous); ``finish()`` waits and
     returns the per-part ``VariogramModel`` list (raising the reference's
-    errors, tagged with the failing part).
+    errors, tagged with the failing part).  With ``fit=False`` the caller
+    supplies one model per part and only stats -> solve -> predict run.
     """
 
     def __init__(self, n_known: int, height: int, width: int, factor: int,
                  n_subparts: int, kind: str = "exponential", drift: str = "linear",
                  accum: str = "fp64", n_bins: int = 15, max_pairs: int = 100_000,
-                 seed: int = 0, force_generic: bool = False):
+                 seed: int = 0, force_generic: bool = False, fit: bool = True,
+                 redraw_pairs: bool = False, part_len: int = 0):
         if factor < 1:
             raise ValueError("factor must be >= 1")
-        subpart_ranges(n_known, n_subparts)          # validates the partition
+        self.ranges = subpart_ranges(n_known, n_subparts, part_len)   # validates
         self.n_known, self.height, self.width = n_known, height, width
         self.factor, self.n_subparts, self.kind = factor, n_subparts, kind
+        self.fit = fit
         self.depth = output_depth(n_known, factor)
         self.plan = KrigingPlan(height, width, self.depth,
                                 np.arange(n_known, dtype=np.int32) * factor,
                                 n_subparts=n_subparts, kind=kind, drift=drift,
-                                accum=accum, fit=True, n_bins=n_bins,
+                                accum=accum, fit=fit, n_bins=n_bins,
                                 max_pairs=max_pairs, seed=seed,
-                                force_generic=force_generic)
+                                force_generic=force_generic,
+                                redraw_pairs=redraw_pairs, part_len=part_len)
 
     @property
     def interpolated_voxels(self) -> int:
@@ -83,11 +87,16 @@ class ZPartKriging:
                            device="cuda") if return_variance else None)
         return out, var
 
-    def run(self, known, out=None, var=None, return_variance: bool = False, stream=None):
+    def run(self, known, out=None, var=None, return_variance: bool = False, stream=None,
+            models=None):
+        """Launch the path; ``models`` ([S] VariogramModel or [S,3] array) is
+        required when the object was built with ``fit=False``."""
         if out is None:
             out, v2 = self.allocate(return_variance)
             var = v2 if var is None else var
-        self.plan.execute(known, out, var, stream=stream)
+        if models is not None and not isinstance(models, np.ndarray):
+            models = np.array([[m.nugget, m.sill, m.range_len] for m in models])
+        self.plan.execute(known, out, var, models=models, stream=stream)
         return out, var
 
     def finish(self, stream=None):

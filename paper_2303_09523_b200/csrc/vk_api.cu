@@ -83,6 +83,9 @@ struct vk_plan {
   bool pairs_ready = false;
   double* h_models = nullptr;        // pinned staging [S][3]
   int kernels = 0;
+  int ring = 0;                       // timing ring size (0 = off)
+  int64_t n_exec = 0;                 // executes recorded so far
+  std::vector<cudaEvent_t> ev;        // [ring][VK_N_STAGES + 1]
 
   template <typename T>
   cudaError_t alloc(T** p, size_t n) {
@@ -97,6 +100,7 @@ struct vk_plan {
     return e;
   }
   ~vk_plan() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     if (h_models) cudaFreeHost(h_models);
   }
@@ -136,7 +140,7 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   p->desc = *d;
   p->desc.known_z = nullptr;
   std::string err = build_geometry(d->height, d->width, d->depth, d->known_z, d->n_known, d->n_subparts,
-                                   d->drift, &p->geo);
+                                   d->part_len, d->drift, &p->geo);
   if (!err.empty()) {
     delete p;
     if (err.rfind("NoKnownNeighbors", 0) == 0) return set_err(VK_E_NO_KNOWN_NEIGHBORS, err);
@@ -278,6 +282,12 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   const int64_t P = (int64_t)g.H * g.W;
   const int S = g.S;
   int kernels = 0;
+  const int slot = p->ring ? (int)(p->n_exec % p->ring) : 0;
+  auto mark = [&](int stage) -> cudaError_t {
+    if (!p->ring) return cudaSuccess;
+    return cudaEventRecord(p->ev[(size_t)slot * (VK_N_STAGES + 1) + stage], st);
+  };
+  VK_CUDA(mark(0));
   if (!d.fit_variogram) {
     if (!models) return set_err(VK_E_INVALID_ARGUMENT, "models required when fit_variogram == 0");
     std::memcpy(p->h_models, models, (size_t)S * 3 * sizeof(double));
@@ -286,8 +296,9 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   }
   VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st));
   ++kernels;
+  VK_CUDA(mark(1));
   if (d.fit_variogram) {
-    if (!p->pairs_ready) {
+    if (!p->pairs_ready || (d.flags & VK_FLAG_REDRAW_PAIRS)) {
       const Pcg64 gen = pcg64_from_seed(d.seed);
       std::vector<int32_t> zoff;
       int32_t acc = 0;
@@ -305,6 +316,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       }
       p->pairs_ready = true;
     }
+    VK_CUDA(mark(2));
     BinsArgs ba;
     ba.known = known;
     ba.values = nullptr;
@@ -319,6 +331,8 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(launch_bins(ba, st));
     ++kernels;
   }
+  if (!d.fit_variogram) VK_CUDA(mark(2));
+  VK_CUDA(mark(3));
   FitArgs fa;
   fa.S = S;
   fa.n_bins = d.n_bins;
@@ -338,6 +352,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   fa.status = p->d_part_status;
   VK_CUDA(launch_fit(fa, st));
   ++kernels;
+  VK_CUDA(mark(4));
   SolveArgs sa;
   sa.n_sys = p->n_sys;
   sa.kind = d.kind;
@@ -360,6 +375,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   sa.max_n = p->max_n;
   VK_CUDA(launch_solve(sa, st));
   if (p->n_sys) ++kernels;
+  VK_CUDA(mark(5));
   PredictArgs pa;
   pa.known = known;
   pa.out = out;
@@ -394,7 +410,39 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(launch_predict_generic(pa, st));
     kernels += 1 + (pa.n_miss > 0);
   }
+  VK_CUDA(mark(6));
+  if (p->ring) ++p->n_exec;
   p->kernels = kernels;
+  return VK_OK;
+}
+
+int vk_plan_set_timing(vk_plan* p, int ring) {
+  if (!p || ring < 0) return set_err(VK_E_INVALID_ARGUMENT, "bad plan / ring");
+  for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+  p->ev.clear();
+  p->ring = 0;
+  p->n_exec = 0;
+  for (int i = 0; i < ring * (VK_N_STAGES + 1); ++i) {
+    cudaEvent_t e;
+    VK_CUDA(cudaEventCreate(&e));
+    p->ev.push_back(e);
+  }
+  p->ring = ring;
+  return VK_OK;
+}
+
+int vk_plan_stage_ms(vk_plan* p, int back, float* ms) {
+  if (!p || !ms) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  if (!p->ring) return set_err(VK_E_INVALID_ARGUMENT, "timing not enabled");
+  if (back < 0 || back >= p->ring || back >= p->n_exec) return set_err(VK_E_INVALID_ARGUMENT, "no such execute");
+  const int slot = (int)((p->n_exec - 1 - back) % p->ring);
+  cudaEvent_t* e = &p->ev[(size_t)slot * (VK_N_STAGES + 1)];
+  VK_CUDA(cudaEventSynchronize(e[VK_N_STAGES]));
+  for (int i = 0; i < VK_N_STAGES; ++i) {
+    float t = 0.f;
+    VK_CUDA(cudaEventElapsedTime(&t, e[i], e[i + 1]));
+    ms[i] = t;
+  }
   return VK_OK;
 }
 

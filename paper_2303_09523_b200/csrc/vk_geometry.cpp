@@ -66,7 +66,7 @@ int rank_of(const std::vector<std::vector<double>>& cols) {
 }  // namespace
 
 std::string build_geometry(int H, int W, int T, const int* known_z, int K, int S,
-                           int drift, Geometry* g) {
+                           int part_len, int drift, Geometry* g) {
   if (H < 1 || W < 1 || T < 1) return "Invalid: empty grid";
   if (K < 1) return "NoKnownNeighbors: grid has no known voxels at all";
   if (S < 1) return "Invalid: n_subparts must be >= 1";
@@ -76,8 +76,9 @@ std::string build_geometry(int H, int W, int T, const int* known_z, int K, int S
   }
   g->H = H; g->W = W; g->T = T; g->K = K; g->S = S;
   g->known_z.assign(known_z, known_z + K);
-  const int q = K / S;
+  const int q = part_len > 0 ? part_len : K / S;
   if (q < 1) return "Invalid: more sub-parts than known slices";
+  if ((int64_t)(S - 1) * q > K - 1) return "Invalid: part_len too large for the stack";
   std::vector<char> is_known(T, 0);
   for (int i = 0; i < K; ++i) is_known[known_z[i]] = 1;
 

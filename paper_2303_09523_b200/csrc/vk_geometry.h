@@ -62,6 +62,6 @@ struct Geometry {
 // Builds the geometry; returns "" on success or an error message.
 // Error prefixes: "NoKnownNeighbors:", "Unsupported:", "Invalid:".
 std::string build_geometry(int H, int W, int T, const int* known_z, int K, int S,
-                           int drift, Geometry* g);
+                           int part_len, int drift, Geometry* g);
 
 }  // namespace vk

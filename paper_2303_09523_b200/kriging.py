@@ -88,7 +88,7 @@ class KrigingPlan:
     def __init__(self, height, width, depth, known_z, n_subparts=1,
                  kind="exponential", drift="linear", accum="fp64", fit=True,
                  n_bins=15, max_pairs=100_000, seed=0, force_generic=False,
-                 part_len=0):
+                 part_len=0, redraw_pairs=False):
         if callable(drift):
             raise DeviceUnsupported("a callable drift cannot cross the C ABI; "
                                     "use 'linear' or 'constant'")
@@ -111,9 +111,8 @@ class KrigingPlan:
             kz.ctypes.data_as(C.POINTER(C.c_int32)), self.n_subparts,
             _lib.KIND_IDS[kind], _lib.DRIFT_IDS[drift], _lib.ACCUM_IDS[accum],
             int(n_bins), int(max_pairs), int(seed), int(bool(fit)),
-            _lib.FLAG_FORCE_GENERIC if force_generic else 0)
-        if part_len:
-            raise DeviceUnsupported("explicit part_len is not supported")
+            (_lib.FLAG_FORCE_GENERIC if force_generic else 0)
+            | (_lib.FLAG_REDRAW_PAIRS if redraw_pairs else 0), int(part_len))
         handle = C.c_void_p()
         raise_for_status(self.lib.vk_plan_create(C.byref(desc), C.byref(handle)))
         self._h = handle
@@ -167,6 +166,16 @@ class KrigingPlan:
         ctx = f"sub-part {failed.value}" if failed.value >= 0 and self.n_subparts > 1 else ""
         raise_for_status(code, ctx)
         return models, lohi
+
+    def set_timing(self, ring: int = 1) -> None:
+        """Record per-stage CUDA events for the last ``ring`` executes."""
+        raise_for_status(self.lib.vk_plan_set_timing(self._h, int(ring)))
+
+    def stage_ms(self, back: int = 0) -> dict:
+        """Per-stage device times (ms) of the execute ``back`` calls ago."""
+        ms = np.zeros(_lib.N_STAGES, dtype=np.float32)
+        raise_for_status(self.lib.vk_plan_stage_ms(self._h, int(back), ms.ctypes.data))
+        return dict(zip(_lib.STAGES, map(float, ms)))
 
     def systems(self):
         """Solved stencils: (weights [n,128], variance [n], ids [n,4])."""

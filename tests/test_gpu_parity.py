@@ -11,6 +11,12 @@ pytestmark = pytest.mark.gpu
 
 TOL64 = 1e-6
 TOL32 = 1e-3
+# End-to-end bound when the device also fits the variogram.  scipy's TRF stops
+# on ftol inside flat valleys, so the reference itself moves by up to ~8e-6 of
+# the range when only libm's exp changes at the ulp level (see
+# tests/test_fit_fuzz.py and DESIGN.md "Fit parity"); the kriging itself is
+# held to TOL64 with the oracle's models.
+FIT_FUZZ = 5e-5
 
 
 def _rng(a):
@@ -86,7 +92,17 @@ def test_fast_matches_generic_and_oracle(cuda, W):
     ref, rvar, rmodels = O.reconstruct_zparts(ks, cfg.factor, cfg.n_subparts,
                                               return_variance=True)
     err = np.abs(oa.astype(np.float64) - ref).max() / _rng(ks)
+    assert err <= FIT_FUZZ, err
+    # strict kriging parity with the oracle's own models
+    c = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts,
+                     fit=False)
+    oc, vc = c.run(kd, return_variance=True, models=rmodels)
+    c.finish()
+    oc = oc.cpu().numpy()
+    assert np.array_equal(oc[::cfg.factor], ks)
+    err = np.abs(oc.astype(np.float64) - ref).max() / _rng(ks)
     assert err <= TOL64, err
+    assert np.allclose(vc.cpu().numpy(), rvar, rtol=1e-7, atol=1e-9 * max(m.sill for m in rmodels))
 
 
 def test_c1_head_pipeline(cuda):
@@ -102,12 +118,18 @@ def test_c1_head_pipeline(cuda):
     got = out.cpu().numpy()
     assert np.array_equal(got[::cfg.factor], ks)
     err = np.abs(got.astype(np.float64) - ref).max() / _rng(ks)
-    assert err <= TOL64, err
+    assert err <= FIT_FUZZ, err
     assert np.abs(np.rint(got) - np.rint(ref)).max() <= 1
     for m, r in zip(models, rmodels):
-        assert abs(m.nugget - r.nugget) <= 1e-5 * r.sill
-        assert abs(m.sill - r.sill) <= 1e-5 * r.sill
+        assert abs(m.nugget - r.nugget) <= 1e-4 * r.sill
+        assert abs(m.sill - r.sill) <= 1e-4 * r.sill
         assert abs(m.range_len - r.range_len) <= 1e-3 * r.range_len
+    zf = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts,
+                      fit=False)
+    of, _ = zf.run(torch.from_numpy(ks).cuda(), models=rmodels)
+    zf.finish()
+    err = np.abs(of.cpu().numpy().astype(np.float64) - ref).max() / _rng(ks)
+    assert err <= TOL64, err
 
 
 def test_fp32_accumulation(cuda):
