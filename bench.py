@@ -59,7 +59,7 @@ def _profile_traffic(name: str):
 class ClockSampler:
     """nvidia-smi sampling during the timed region (clocks + throttle)."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -68,10 +68,11 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        self.t0 = self.t1 = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -88,16 +89,31 @@ class ClockSampler:
                 out = ""
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
+    def mark(self, start: bool):
+        """Wall-clock bounds of the timed region (samples are filtered to it)."""
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
     def summary(self):
+        import datetime
         rows = []
         for ln in getattr(self, "lines", []):
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
-                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), float(parts[3]), parts[4:8]))
             except ValueError:
                 continue
+        if self.t0 is not None and self.t1 is not None and rows:
+            inside = [r for r in rows if self.t0 - 0.03 <= r[0] <= self.t1 + 0.03]
+            if not inside:                    # region shorter than the sampling period
+                inside = sorted(rows, key=lambda r: abs(r[0] - 0.5 * (self.t0 + self.t1)))[:2]
+            rows = inside
+        rows = [r[1:] for r in rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -239,11 +255,14 @@ def run_gpu(args, cfg, ks):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        time.sleep(0.6)                      # nvidia-smi start-up, outside the region
+        clk.mark(True)
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark(False)
     zk.finish()
     for back in range(args.steps):          # per-launch stage events, read after
         st = zk.plan.stage_ms(back)
@@ -269,7 +288,10 @@ def run_gpu(args, cfg, ks):
     alg_bytes = 4 * (K_loc + T) * H * W + (8 * T * H * W if args.variance else 0)
     pred_avg = float(np.mean(pred_ms))
     achieved = alg_bytes / (pred_avg / 1e3) / 1e9
-    fp64_cap = 148 * 64 * sm_max * 1e6 / 32           # vox/s at 32 DFMA per voxel
+    # fp64 pipe cap of the streaming kernel: 16 DFMA per voxel (mirror-pair
+    # stencils) + 2 DADD (S/D) at the measured 58 DFMA/clk/SM (tools/
+    # fp64_microbench.cu, profiles/fp64_microbench_r01.json)
+    fp64_cap = 148 * 58 * sm_max * 1e6 / 18
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": _profile_traffic(args.accum),
             "kernel": "predict_fast_kernel", "bytes_per_launch": alg_bytes,

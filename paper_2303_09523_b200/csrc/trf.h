@@ -96,7 +96,7 @@ VK_HD void svd3(const double* A, int mr, double* U, double* s, double* V) {
           beta += b * b;
           gamma += a * b;
         }
-        if (gamma == 0.0 || fabs(gamma) <= 1e-17 * sqrt(alpha * beta)) continue;
+        if (gamma == 0.0 || fabs(gamma) <= TRF_EPS * sqrt(alpha * beta)) continue;
         rotated = true;
         const double zeta = (beta - alpha) / (2.0 * gamma);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));

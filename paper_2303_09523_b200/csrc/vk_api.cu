@@ -83,6 +83,8 @@ struct vk_plan {
   bool pairs_ready = false;
   double* h_models = nullptr;        // pinned staging [S][3]
   int kernels = 0;
+  cudaStream_t side = nullptr;        // pair draw runs here, concurrent with stats
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int ring = 0;                       // timing ring size (0 = off)
   int64_t n_exec = 0;                 // executes recorded so far
   std::vector<cudaEvent_t> ev;        // [ring][VK_N_STAGES + 1]
@@ -101,6 +103,9 @@ struct vk_plan {
   }
   ~vk_plan() {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     for (void* p : allocs) cudaFree(p);
     if (h_models) cudaFreeHost(h_models);
   }
@@ -246,9 +251,16 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
       VK_TRY(p->alloc(&t.bin, (size_t)d->max_pairs));
       VK_TRY(p->alloc(&t.counts, (size_t)MAX_BINS));
       VK_TRY(p->alloc(&t.scal, (size_t)4));
+      const int64_t ns = pair_scratch_elems(g.pair_classes[c].m, d->max_pairs);
+      VK_TRY(p->alloc(&t.cnt, (size_t)ns));
+      VK_TRY(p->alloc(&t.off, (size_t)ns + 1));
+      VK_TRY(p->alloc(&t.hbits, (size_t)1));
       p->tables.push_back(t);
     }
     VK_TRY(p->put(&p->d_tables, p->tables));
+    VK_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    VK_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    VK_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   }
 #undef VK_TRY
   (void)class_zoff;
@@ -294,11 +306,13 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(cudaMemcpyAsync(p->d_models, p->h_models, (size_t)S * 3 * sizeof(double),
                             cudaMemcpyHostToDevice, st));
   }
-  VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st));
-  ++kernels;
-  VK_CUDA(mark(1));
-  if (d.fit_variogram) {
-    if (!p->pairs_ready || (d.flags & VK_FLAG_REDRAW_PAIRS)) {
+  // the pair draw depends only on geometry and seed: fork it onto the side
+  // stream so it overlaps the plane statistics
+  const bool draw = d.fit_variogram && (!p->pairs_ready || (d.flags & VK_FLAG_REDRAW_PAIRS));
+  if (draw) {
+    VK_CUDA(cudaEventRecord(p->ev_fork, st));
+    VK_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    {
       const Pcg64 gen = pcg64_from_seed(d.seed);
       std::vector<int32_t> zoff;
       int32_t acc = 0;
@@ -311,11 +325,18 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
         sg.W = g.W;
         VK_CUDA(launch_pair_table((uint64_t)(gen.state >> 64), (uint64_t)gen.state, (uint64_t)(gen.inc >> 64),
                                   (uint64_t)gen.inc, g.pair_classes[c].m, d.max_pairs, d.n_bins, sg,
-                                  p->tables[c], st));
-        ++kernels;
+                                  p->tables[c], p->side));
+        kernels += 5;
       }
       p->pairs_ready = true;
     }
+    VK_CUDA(cudaEventRecord(p->ev_join, p->side));
+  }
+  VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st));
+  ++kernels;
+  VK_CUDA(mark(1));
+  if (draw) VK_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));   // "pairs" = residual wait
+  if (d.fit_variogram) {
     VK_CUDA(mark(2));
     BinsArgs ba;
     ba.known = known;
@@ -510,6 +531,10 @@ int vk_sample_pairs(int64_t m, int64_t max_pairs, uint64_t seed, int32_t* ii, in
   VK_CUDA(cudaMalloc((void**)&t.bin, (size_t)max_pairs));
   VK_CUDA(cudaMalloc((void**)&t.counts, MAX_BINS * sizeof(int64_t)));
   VK_CUDA(cudaMalloc((void**)&t.scal, 4 * sizeof(double)));
+  const int64_t ns = pair_scratch_elems(m, max_pairs);
+  VK_CUDA(cudaMalloc((void**)&t.cnt, ns * sizeof(int32_t)));
+  VK_CUDA(cudaMalloc((void**)&t.off, (ns + 1) * sizeof(int64_t)));
+  VK_CUDA(cudaMalloc((void**)&t.hbits, sizeof(unsigned long long)));
   int32_t* zl = nullptr;
   VK_CUDA(cudaMalloc((void**)&zl, sizeof(int32_t)));
   VK_CUDA(cudaMemsetAsync(zl, 0, sizeof(int32_t), st));
@@ -527,6 +552,9 @@ int vk_sample_pairs(int64_t m, int64_t max_pairs, uint64_t seed, int32_t* ii, in
   cudaFree(t.bin);
   cudaFree(t.counts);
   cudaFree(t.scal);
+  cudaFree(t.cnt);
+  cudaFree(t.off);
+  cudaFree(t.hbits);
   cudaFree(zl);
   if (e != cudaSuccess) return set_err(VK_E_CUDA, cudaGetErrorString(e));
   if (n_out) *n_out = (int64_t)scal[2];
@@ -560,6 +588,10 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   t.bin = (uint8_t*)get(npmax);
   t.counts = (int64_t*)get(MAX_BINS * 8);
   t.scal = (double*)get(4 * 8);
+  const int64_t ns = pair_scratch_elems(m, max_pairs);
+  t.cnt = (int32_t*)get((size_t)ns * 4);
+  t.off = (int64_t*)get((size_t)(ns + 1) * 8);
+  t.hbits = (unsigned long long*)get(8);
   PairTable* d_t = (PairTable*)get(sizeof(PairTable));
   ChunkStat* stats = (ChunkStat*)get((size_t)nchunk * sizeof(ChunkStat));
   double* partial = (double*)get((size_t)nblk * n_bins * 8);

@@ -27,6 +27,7 @@ enum PartStatus : int32_t {
   PS_DEGENERATE = 3,
   PS_FIT_FAILED = 4,
   PS_PAIRS_SHORT = 5,
+  PS_NEED_SCALAR_FIT = 6,   // internal: handed to the scalar TRF kernel
 };
 
 // Variogram model parameters as the reference's VariogramModel

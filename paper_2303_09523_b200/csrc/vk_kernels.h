@@ -18,7 +18,13 @@ struct PairTable {                   // one per pair class (device pointers)
   uint8_t* bin;                      // 255 = skipped (i == j or lag == 0)
   int64_t* counts;                   // [n_bins]
   double* scal;                      // [0] hmax, [1] lag_max, [2] n_drawn, [3] status
+  // scratch of the parallel draw (sized by pair_scratch_elems)
+  int32_t* cnt;                      // [n_thr]
+  int64_t* off;                      // [n_thr + 1]
+  unsigned long long* hbits;         // [1]
 };
+// number of draw threads (= scratch entries) for a pair class
+int64_t pair_scratch_elems(int64_t m, int64_t max_pairs);
 
 // Coordinates of sample i of a structured sub-part: plane i / P at local z
 // zloc[i / P], pixel (i % P) -> (x, y).  Explicit: coords[i*3 + {0,1,2}].

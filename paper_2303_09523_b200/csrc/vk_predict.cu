@@ -6,15 +6,19 @@
 //                  streamed into a 3-deep shared-memory ring by TMA
 //                  (cp.async.bulk.tensor, OOB zero fill supplies the volume
 //                  halo) so each known plane is read from HBM once per run.
-//                  Each thread keeps one 7-wide input row in registers and
-//                  accumulates 4 columns x G missing planes in fp64 (or fp32)
-//                  with the interior stencil, in the reference tap order
-//                  (plane, oy, ox); results are clamped to the part's known
-//                  range and stored as 128-bit streaming stores; the known
-//                  planes are copied through from the same tiles.  Voxels on
-//                  the clamped-window border (x or y in {0, n-2, n-1}) are
-//                  recomputed per voxel with their own stencil kind from the
-//                  same shared-memory tiles.
+//                  The G missing planes of a gap come in z-mirror pairs
+//                  (j, G-1-j) whose interior stencils are mirror images, so
+//                  each pair is computed from S = A+B and D = A-B (exact in
+//                  fp64) with one symmetric and one antisymmetric 16-tap
+//                  stencil -- 16 instead of 32 DFMA per voxel.  Each thread
+//                  keeps one 7-wide row of S and D in registers and
+//                  accumulates 4 columns x G planes; results are clamped to
+//                  the part's known range and stored as 128-bit streaming
+//                  stores; the known planes are copied through from the
+//                  same tiles.  Border rows (y in {0, H-2, H-1}) use their
+//                  clamped-window kind's stencils (zero taps outside the
+//                  window); the three border columns are computed by one
+//                  thread per (row, column) with their own kinds.
 // predict_generic: any plane pattern (up to 8 planes, any dims); one thread
 //                  per missing voxel, reading the known planes through L1/L2.
 #include <cuda.h>
@@ -160,15 +164,22 @@ template <int G, typename Acc>
 __global__ void __launch_bounds__(FT_THREADS, 2)
     predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
                         int n_tiles, int chunk, int n_units) {
+  constexpr int NPAIR = G / 2;
+  constexpr bool MID = (G & 1) != 0;
+  constexpr int NST = 2 * NPAIR + (MID ? 1 : 0);          // stencils per kind
+  constexpr int NSTP = (NST + 1) & ~1;                     // padded: 16-byte aligned taps
   extern __shared__ __align__(128) float ring[];           // FT_STAGES x FT_BUF_FLOATS
   __shared__ __align__(8) uint64_t full[FT_STAGES];
-  __shared__ Acc s_w[G * 32];                              // interior weights of this gap
-  __shared__ double s_var[G];
-  __shared__ Acc s_lohi[2];
+  // mirror-pair stencils per (y-kind, x-kind) present in the tile, tap-major
+  // so one 128-bit load fetches (K+_p, K-_p): [iy*nkx+ix][tap][K+_0, K-_0, ...,
+  // K_mid, pad]
+  __shared__ __align__(16) Acc s_k[4 * 4 * 16 * NSTP];
+  __shared__ double s_var[4 * 4 * G];
+  __shared__ int s_kind[2][4];                             // global axis kinds (y, x)
+  __shared__ float s_lohi[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = a.H, W = a.W;
   const int64_t P = a.P;
-  const int kint = a.kmap[NKIND1 + AXIS_INTERIOR] * a.nkx + a.kmap[AXIS_INTERIOR];
   if (tid == 0) {
     for (int i = 0; i < FT_STAGES; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -183,7 +194,20 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
     const int tx = tile % n_tiles_x, ty = tile / n_tiles_x;
     const int x0 = tx * FT_TX, y0 = ty * FT_TY;
     const int kb = chunk_id * chunk, ke = min(n_gaps, kb + chunk);   // gaps [kb, ke)
+    const int ty1 = min(H, y0 + FT_TY), tx1 = min(W, x0 + FT_TX);
+    // window kinds present in this tile: interior first, then the border ones
+    int nky = 1, nkx = 1;
+    int kyl[4] = {AXIS_INTERIOR, 0, 0, 0}, kxl[4] = {AXIS_INTERIOR, 0, 0, 0};
+    {
+      const int rc[3] = {0, H - 2, H - 1};
+      for (int q = 0; q < 3; ++q)
+        if (rc[q] >= y0 && rc[q] < ty1) kyl[nky++] = axis_kind(rc[q], H);
+      const int cc[3] = {0, W - 2, W - 1};
+      for (int q = 0; q < 3; ++q)
+        if (cc[q] >= x0 && cc[q] < tx1) kxl[nkx++] = axis_kind(cc[q], W);
+    }
     const uint32_t seq0 = load_seq;
+    int cur_s = -1;                                        // part whose stencils are staged
     __syncthreads();                                       // previous unit done with the ring
     if (tid == 0) {
       for (int i = 0; i < 2; ++i) {
@@ -204,67 +228,110 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
         tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, k + 2);
       }
       if (k + 2 <= ke) load_seq += 1;
-      // gap constants: interior weights for the G missing planes, var, clamp
+      // ---- gap constants.  Missing planes j and G-1-j are z-mirrors: their
+      // stencils satisfy wA_j = wB_{G-1-j}, wB_j = wA_{G-1-j} (isotropic
+      // covariance; drift span closed under z -> -z).  With a, b the
+      // mirror-averaged plane-A / plane-B stencils of j, out_j = a*A + b*B =
+      // K+*(A+B) + K-*(A-B) and out_{G-1-j} = K+*(A+B) - K-*(A-B) with
+      // K+- = (a +- b)/2: one symmetric and one antisymmetric 16-tap stencil
+      // per pair instead of four.  Taps outside a clamped border window are 0.
       const int s = a.gap_part[k];
-      for (int i = tid; i < G * 32; i += FT_THREADS) {
-        const int j = i >> 5, t = i & 31;
-        const int p = a.gap_pattern[k * G + j];
-        s_w[i] = (Acc)a.weights[(((int64_t)s * a.NP + p) * a.NK + kint) * WPAD + t];
+      const bool reload = (s != cur_s);                    // CTA-uniform
+      cur_s = s;
+      const int n_items = reload ? nky * nkx * (NPAIR + (MID ? 1 : 0)) * 16 : 0;
+      for (int i = tid; i < n_items; i += FT_THREADS) {
+        const int t = i & 15, rest = i >> 4;
+        const int pr = rest % (NPAIR + (MID ? 1 : 0)), kk = rest / (NPAIR + (MID ? 1 : 0));
+        const int iy = kk / nkx, ix = kk - iy * nkx;
+        const int kind = a.kmap[NKIND1 + kyl[iy]] * a.nkx + a.kmap[kxl[ix]];
+        const int pj = a.gap_pattern[k * G + pr], pm = a.gap_pattern[k * G + (G - 1 - pr)];
+        const double* wj = a.weights + (((int64_t)s * a.NP + pj) * a.NK + kind) * WPAD;
+        const double* wm = a.weights + (((int64_t)s * a.NP + pm) * a.NK + kind) * WPAD;
+        const double av = 0.5 * (wj[t] + wm[16 + t]);
+        const double bv = 0.5 * (wj[16 + t] + wm[t]);
+        Acc* dst = s_k + ((size_t)kk * 16 + t) * NSTP;
+        if (pr < NPAIR) {
+          dst[2 * pr] = (Acc)(0.5 * (av + bv));
+          dst[2 * pr + 1] = (Acc)(0.5 * (av - bv));
+        } else {
+          dst[2 * NPAIR] = (Acc)(0.5 * (av + bv));
+        }
       }
-      if (tid < G) {
-        const int p = a.gap_pattern[k * G + tid];
-        s_var[tid] = a.svar[((int64_t)s * a.NP + p) * a.NK + kint];
+      for (int i = tid; i < (reload ? nky * nkx * G : 0); i += FT_THREADS) {
+        const int j = i % G, kk = i / G;
+        const int iy = kk / nkx, ix = kk - iy * nkx;
+        const int kind = a.kmap[NKIND1 + kyl[iy]] * a.nkx + a.kmap[kxl[ix]];
+        s_var[i] = a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK + kind];
       }
-      if (tid == 0) { s_lohi[0] = (Acc)a.lohi[2 * s]; s_lohi[1] = (Acc)a.lohi[2 * s + 1]; }
+      if (tid == 0 && reload) { s_lohi[0] = (float)a.lohi[2 * s]; s_lohi[1] = (float)a.lohi[2 * s + 1]; }
       if (k == kb) mbar_wait(&full[sq_a % FT_STAGES], (sq_a / FT_STAGES) & 1);
       mbar_wait(&full[sq_b % FT_STAGES], (sq_b / FT_STAGES) & 1);
-      __syncthreads();
+      if (reload) __syncthreads();                         // staged stencils visible
       const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
       const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
-      const Acc lo = s_lohi[0], hi = s_lohi[1];
+      // the clamp commutes with the f32 rounding (lo, hi are f32 values and
+      // rounding is monotone), so it is applied after the conversion
+      const float lo = s_lohi[0], hi = s_lohi[1];
       const int64_t zk = a.known_z[k];
       const bool copy_b = (k == n_gaps - 1);
       const int gx = x0 + 4 * lane;
       const bool col_ok = gx < W;
-      // x-border columns inside this thread's group (handled by the fixup)
-      const bool xb0 = (gx == 0), xb1 = (gx + 4 > W - 2);
+      const bool xb0 = (gx == 0), xb1 = (gx + 4 > W - 2);   // group holds border columns
 #pragma unroll 1
       for (int rs = 0; rs < FT_TY / FT_WARPS; ++rs) {
-        const int r = warp + rs * FT_WARPS;                // tile row
+        const int r = warp + rs * FT_WARPS;                // tile row (warp-uniform)
         const int gy = y0 + r;
         if (gy >= H || !col_ok) continue;
-        Acc acc[G][4];
+        int iy = 0;                                        // row kind (border rows of edge tiles)
+        const int kyr = axis_kind(gy, H);
+        for (int q = 1; q < nky; ++q)
+          if (kyl[q] == kyr) iy = q;
+        const Acc* wk = s_k + (size_t)(iy * nkx) * 16 * NSTP;  // x-kind: interior
+        Acc accS[NPAIR > 0 ? NPAIR : 1][4], accD[NPAIR > 0 ? NPAIR : 1][4], accC[4];
 #pragma unroll
-        for (int j = 0; j < G; ++j)
+        for (int c = 0; c < 4; ++c) {
+          accC[c] = (Acc)0;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[j][c] = (Acc)0;
+          for (int p = 0; p < NPAIR; ++p) { accS[p][c] = (Acc)0; accD[p][c] = (Acc)0; }
+        }
         float4 selfA = make_float4(0, 0, 0, 0), selfB = selfA;
 #pragma unroll
-        for (int pl = 0; pl < 2; ++pl) {
-          const float* buf = pl ? bufB : bufA;
+        for (int oy = -1; oy <= 2; ++oy) {
+          const float* ra = bufA + (r + 1 + oy) * FT_SX + 4 * lane;
+          const float* rb = bufB + (r + 1 + oy) * FT_SX + 4 * lane;
+          const float4 a0 = *reinterpret_cast<const float4*>(ra);
+          const float4 a1 = *reinterpret_cast<const float4*>(ra + 4);
+          const float2 a2 = *reinterpret_cast<const float2*>(ra + 8);
+          const float4 b0 = *reinterpret_cast<const float4*>(rb);
+          const float4 b1 = *reinterpret_cast<const float4*>(rb + 4);
+          const float2 b2 = *reinterpret_cast<const float2*>(rb + 8);
+          if (oy == 0) { selfA = a1; selfB = b1; }
+          const float fa[7] = {a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y};
+          const float fb[7] = {b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y};
+          Acc S[7], D[7];                                  // exact in fp64
 #pragma unroll
-          for (int oy = -1; oy <= 2; ++oy) {
-            const float* row = buf + (r + 1 + oy) * FT_SX + 4 * lane;
-            const float4 q0 = *reinterpret_cast<const float4*>(row);
-            const float4 q1 = *reinterpret_cast<const float4*>(row + 4);
-            const float2 q2 = *reinterpret_cast<const float2*>(row + 8);
-            if (oy == 0) { if (pl) selfB = q1; else selfA = q1; }
-            Acc v[7];
-            v[0] = AccVec<Acc>::cvt(q0.w);
-            v[1] = AccVec<Acc>::cvt(q1.x);
-            v[2] = AccVec<Acc>::cvt(q1.y);
-            v[3] = AccVec<Acc>::cvt(q1.z);
-            v[4] = AccVec<Acc>::cvt(q1.w);
-            v[5] = AccVec<Acc>::cvt(q2.x);
-            v[6] = AccVec<Acc>::cvt(q2.y);
+          for (int i = 0; i < 7; ++i) {
+            const Acc x = AccVec<Acc>::cvt(fa[i]), y = AccVec<Acc>::cvt(fb[i]);
+            S[i] = x + y;
+            D[i] = x - y;
+          }
 #pragma unroll
-            for (int j = 0; j < G; ++j) {
+          for (int ox = -1; ox <= 2; ++ox) {
+            const int t = (oy + 1) * 4 + (ox + 1);
+            const Acc* wt = wk + t * NSTP;
 #pragma unroll
-              for (int ox = -1; ox <= 2; ++ox) {
-                const Acc w = s_w[j * 32 + pl * 16 + (oy + 1) * 4 + (ox + 1)];
+            for (int p = 0; p < NPAIR; ++p) {
+              const Acc wp = wt[2 * p], wm = wt[2 * p + 1];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[j][c] = fma(w, v[c + ox + 1], acc[j][c]);
+              for (int c = 0; c < 4; ++c) {
+                accS[p][c] = fma(wp, S[c + ox + 1], accS[p][c]);
+                accD[p][c] = fma(wm, D[c + ox + 1], accD[p][c]);
               }
+            }
+            if (MID) {
+              const Acc wc = wt[2 * NPAIR];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) accC[c] = fma(wc, S[c + ox + 1], accC[c]);
             }
           }
         }
@@ -280,82 +347,82 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
             st_cs_d2(a.var + (zk + G + 1) * P + pix + 2, 0.0, 0.0);
           }
         }
-        const bool row_border = (gy == 0) || (gy >= H - 2);
-        if (row_border) continue;                          // fixup writes these rows
+        const double* vrow = s_var + (iy * nkx) * G;
 #pragma unroll
         for (int j = 0; j < G; ++j) {
           float o[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            Acc t = acc[j][c];
-            t = t < lo ? lo : t;
-            t = t > hi ? hi : t;
-            o[c] = (float)t;
+            Acc t;
+            if (MID && j == NPAIR) t = accC[c];
+            else if (j < NPAIR) t = accS[j][c] + accD[j][c];
+            else t = accS[G - 1 - j][c] - accD[G - 1 - j][c];
+            o[c] = fminf(fmaxf((float)t, lo), hi);
           }
           float* dst = a.out + (zk + 1 + j) * P + pix;
           double* vdst = a.var ? a.var + (zk + 1 + j) * P + pix : nullptr;
           if (!xb0 && !xb1) {
             st_cs_f4(dst, make_float4(o[0], o[1], o[2], o[3]));
-            if (vdst) { st_cs_d2(vdst, s_var[j], s_var[j]); st_cs_d2(vdst + 2, s_var[j], s_var[j]); }
+            if (vdst) { st_cs_d2(vdst, vrow[j], vrow[j]); st_cs_d2(vdst + 2, vrow[j], vrow[j]); }
           } else {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int xx = gx + c;
               if (xx >= 1 && xx <= W - 3) {
                 dst[c] = o[c];
-                if (vdst) vdst[c] = s_var[j];
+                if (vdst) vdst[c] = vrow[j];
               }
             }
           }
         }
       }
-      // ---- border fixup: clamped-window kinds, per voxel, from the same tiles
-      const int ty1 = min(H, y0 + FT_TY), tx1 = min(W, x0 + FT_TX);
-      const bool touches = (y0 == 0) || (ty1 >= H - 2) || (x0 == 0) || (tx1 >= W - 2);
-      if (touches) {
-        int brow[3], nbr = 0;
-        const int rc[3] = {0, H - 2, H - 1};
-        for (int q = 0; q < 3; ++q)
-          if (rc[q] >= y0 && rc[q] < ty1 && (q == 0 || rc[q] != rc[q - 1])) brow[nbr++] = rc[q];
-        int bcol[3], nbc = 0;
-        const int cc[3] = {0, W - 2, W - 1};
-        for (int q = 0; q < 3; ++q)
-          if (cc[q] >= x0 && cc[q] < tx1) bcol[nbc++] = cc[q];
-        const int rows_in = ty1 - y0, cols_in = tx1 - x0;
-        const int n_rowvox = nbr * cols_in;
-        const int n_colvox = nbc * (rows_in - nbr);
-        const int nvox = n_rowvox + n_colvox;
-        for (int idx = tid; idx < nvox * G; idx += FT_THREADS) {
-          const int j = idx / nvox, vi = idx - j * nvox;
-          int gy, gx2;
-          if (vi < n_rowvox) {
-            gy = brow[vi / cols_in];
-            gx2 = x0 + vi % cols_in;
-          } else {
-            const int t = vi - n_rowvox;
-            gx2 = bcol[t % nbc];
-            gy = y0 + t / nbc;                             // (t/nbc)-th non-border row
-            for (int q = 0; q < nbr; ++q)                  // brow ascending
-              if (brow[q] <= gy) ++gy;
+      // ---- border columns x in {0, W-2, W-1}: one thread per (row, column),
+      // all G planes with the column's window kind, same mirror-pair form
+      if (nkx > 1) {
+        const int rows_in = ty1 - y0, nbc = nkx - 1;
+        for (int idx = tid; idx < rows_in * nbc; idx += FT_THREADS) {
+          const int ic = 1 + idx % nbc, r = idx / nbc;
+          const int gy = y0 + r;
+          int xb = 0;
+          for (int q = 0, seen = 0; q < 3; ++q) {          // ic-th border column in the tile
+            const int cand = q == 0 ? 0 : (q == 1 ? W - 2 : W - 1);
+            if (cand >= x0 && cand < tx1 && ++seen == ic) xb = cand;
           }
-          const int p = a.gap_pattern[k * G + j];
-          const int kx = axis_kind(gx2, W), ky = axis_kind(gy, H);
-          const int kind = a.kmap[NKIND1 + ky] * a.nkx + a.kmap[kx];
-          const int64_t slot = ((int64_t)s * a.NP + p) * a.NK + kind;
-          const double* wv = a.weights + slot * WPAD;
-          Acc acc = (Acc)0;
-          for (int pl = 0; pl < 2; ++pl) {
-            const float* buf = pl ? bufB : bufA;
-            for (int oy = kind_lo(ky); oy < kind_hi(ky); ++oy)
-              for (int ox = kind_lo(kx); ox < kind_hi(kx); ++ox)
-                acc = tap_fma<Acc>(wv[pl * 16 + (oy + 1) * 4 + (ox + 1)],
-                                   buf[(gy - y0 + 1 + oy) * FT_SX + (gx2 - x0 + 4 + ox)], acc);
+          int iy = 0;
+          const int kyr = axis_kind(gy, H);
+          for (int q = 1; q < nky; ++q)
+            if (kyl[q] == kyr) iy = q;
+          const Acc* wk = s_k + (size_t)(iy * nkx + ic) * 16 * NSTP;
+          Acc aS[NPAIR > 0 ? NPAIR : 1], aD[NPAIR > 0 ? NPAIR : 1], aC = (Acc)0;
+          for (int p = 0; p < NPAIR; ++p) { aS[p] = (Acc)0; aD[p] = (Acc)0; }
+          const int cx = xb - x0 + 4;
+#pragma unroll
+          for (int oy = -1; oy <= 2; ++oy) {
+#pragma unroll
+            for (int ox = -1; ox <= 2; ++ox) {
+              const int t = (oy + 1) * 4 + (ox + 1);
+              const Acc x = AccVec<Acc>::cvt(bufA[(r + 1 + oy) * FT_SX + cx + ox]);
+              const Acc y = AccVec<Acc>::cvt(bufB[(r + 1 + oy) * FT_SX + cx + ox]);
+              const Acc Sv = x + y, Dv = x - y;
+#pragma unroll
+              for (int p = 0; p < NPAIR; ++p) {
+                aS[p] = fma(wk[t * NSTP + 2 * p], Sv, aS[p]);
+                aD[p] = fma(wk[t * NSTP + 2 * p + 1], Dv, aD[p]);
+              }
+              if (MID) aC = fma(wk[t * NSTP + 2 * NPAIR], Sv, aC);
+            }
           }
-          acc = acc < lo ? lo : acc;
-          acc = acc > hi ? hi : acc;
-          const int64_t o = (zk + 1 + j) * P + (int64_t)gy * W + gx2;
-          a.out[o] = (float)acc;
-          if (a.var) a.var[o] = a.svar[slot];
+          const int64_t pix = (int64_t)gy * W + xb;
+          const double* vv = s_var + (iy * nkx + ic) * G;
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            Acc t;
+            if (MID && j == NPAIR) t = aC;
+            else if (j < NPAIR) t = aS[j] + aD[j];
+            else t = aS[G - 1 - j] - aD[G - 1 - j];
+            a.out[(zk + 1 + j) * P + pix] = fminf(fmaxf((float)t, lo), hi);
+            if (a.var) a.var[(zk + 1 + j) * P + pix] = vv[j];
+          }
         }
       }
     }

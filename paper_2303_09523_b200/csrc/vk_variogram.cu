@@ -5,17 +5,21 @@
 //                  M2 / min / max (deterministic block trees; merged per part
 //                  in a fixed order with Chan's update) -> svar, lo, hi.
 //   pair_table   : numpy-identical pair draw (PCG64 + Lemire, see pcg64.h)
-//                  with LCG jump-ahead and a block-wide stream compaction,
-//                  then lags, hmax, bin index per pair and bin counts.  Lags
+//                  with LCG jump-ahead and a grid-wide stream compaction
+//                  (count / scan / scatter), then lags, hmax, bin index per
+//                  pair and bin counts.  Lags
 //                  and bins depend only on geometry, so one table serves every
 //                  part with the same sample layout.
 //   bins         : per part, sum of 0.5*(v_i - v_j)^2 per bin; per-thread
 //                  shared-memory accumulators reduced in a fixed order.
-//   fit          : per part, the TRF fit (trf.h) on the non-empty bins.
+//   fit          : per part, the TRF fit on the non-empty bins: one warp per
+//                  part, lane = residual row (trf_warp.cuh restating trf.h).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cfloat>
 #include "pcg64.h"
 #include "trf.h"
+#include "trf_warp.cuh"
 #include "vk_kernels.h"
 
 namespace vk {
@@ -87,125 +91,145 @@ __device__ __forceinline__ double sample_lag(const SampleGeom& g, int64_t i, int
   return sqrt((double)(dx * dx + dy * dy + dz * dz));
 }
 
-constexpr int PT_THREADS = 1024;
+// ---- pair draw: numpy default_rng(seed).integers(0, m, max_pairs) x 2 ------
+// Raw PCG64 outputs are split into chunks of PT_RAW per thread; each thread
+// jumps its LCG to the chunk start (pcg_advance), counts accepted Lemire
+// halves, a single block scans the counts, and the same threads regenerate
+// and scatter accepted draws to their stream positions (ii = first
+// max_pairs draws, jj = the next max_pairs).
+constexpr int PT_RAW = 64;
+constexpr int PT_BLOCK = 256;
 
-__global__ void __launch_bounds__(PT_THREADS) pair_table_kernel(
-    uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t m,
-    int64_t max_pairs, int n_bins, SampleGeom geom, PairTable t) {
-  __shared__ int64_t s_cnt[PT_THREADS];
-  __shared__ double s_red[2][32];
-  __shared__ unsigned long long s_counts[MAX_BINS];
-  __shared__ int64_t s_total;
-  const int tid = threadIdx.x;
-  const int64_t total_pairs = m * (m - 1) / 2;
-  int64_t npairs;
-  int status = 0;
-  if (total_pairs <= max_pairs) {
-    // np.triu_indices(m, 1): row-major upper triangle
-    npairs = total_pairs;
-    for (int64_t i = tid; i < m - 1; i += PT_THREADS) {
-      const int64_t off = i * (m - 1) - i * (i - 1) / 2;
-      for (int64_t j = i + 1; j < m; ++j) {
-        t.ii[off + (j - i - 1)] = (int32_t)i;
-        t.jj[off + (j - i - 1)] = (int32_t)j;
-      }
-    }
-  } else {
-    npairs = max_pairs;
-    const u128 state = ((u128)st_hi << 64) | st_lo;
-    const u128 inc = ((u128)inc_hi << 64) | inc_lo;
-    const uint32_t mm = (uint32_t)m;
-    const uint32_t thr = lemire_threshold(mm);
-    const int64_t need = 2 * max_pairs;
-    const double prej = (double)thr / 4294967296.0;
-    int64_t R = (int64_t)((double)need * (1.0 + 4.0 * prej) / 2.0) + 4096;
-    for (int attempt = 0; attempt < 8; ++attempt) {
-      const int64_t B = (R + PT_THREADS - 1) / PT_THREADS;
-      const int64_t r0 = min(R, (int64_t)tid * B), r1 = min(R, r0 + B);
-      int64_t cnt = 0;
-      u128 s = pcg_advance(state, inc, (uint64_t)r0);
-      const u128 mul = pcg_mult();
-      for (int64_t r = r0; r < r1; ++r) {
-        s = s * mul + inc;
-        const uint64_t raw = pcg_output(s);
-        cnt += ((uint32_t)((uint64_t)(uint32_t)raw * mm) >= thr);
-        cnt += ((uint32_t)((uint64_t)(uint32_t)(raw >> 32) * mm) >= thr);
-      }
-      s_cnt[tid] = cnt;
-      __syncthreads();
-      // inclusive Hillis-Steele scan over 1024 counts
-      for (int o = 1; o < PT_THREADS; o <<= 1) {
-        const int64_t v = (tid >= o) ? s_cnt[tid - o] : 0;
-        __syncthreads();
-        s_cnt[tid] += v;
-        __syncthreads();
-      }
-      const int64_t accepted = s_cnt[PT_THREADS - 1];
-      int64_t pos = s_cnt[tid] - cnt;
-      __syncthreads();
-      if (accepted < need) { R *= 2; continue; }
-      s = pcg_advance(state, inc, (uint64_t)r0);
-      for (int64_t r = r0; r < r1 && pos < need; ++r) {
-        s = s * mul + inc;
-        const uint64_t raw = pcg_output(s);
-        for (int h = 0; h < 2 && pos < need; ++h) {
-          const uint64_t prod = (uint64_t)(uint32_t)(h ? (raw >> 32) : raw) * mm;
-          if ((uint32_t)prod >= thr) {
-            const int32_t v = (int32_t)(prod >> 32);
-            if (pos < max_pairs) t.ii[pos] = v; else t.jj[pos - max_pairs] = v;
-            ++pos;
-          }
-        }
-      }
-      status = 0;
-      break;
-    }
-    if (s_cnt[PT_THREADS - 1] < need) status = PS_PAIRS_SHORT;
+struct PcgArgs {
+  uint64_t st_hi, st_lo, inc_hi, inc_lo;
+  uint32_t m, thr;
+  int64_t n_raw, need, max_pairs;
+};
+
+__global__ void __launch_bounds__(PT_BLOCK) pair_count_kernel(PcgArgs a, int32_t* cnt) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r0 = g * PT_RAW;
+  if (r0 >= a.n_raw) return;
+  const int64_t r1 = min(a.n_raw, r0 + PT_RAW);
+  const u128 inc = ((u128)a.inc_hi << 64) | a.inc_lo;
+  u128 s = pcg_advance(((u128)a.st_hi << 64) | a.st_lo, inc, (uint64_t)r0);
+  const u128 mul = pcg_mult();
+  int c = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    s = s * mul + inc;
+    const uint64_t raw = pcg_output(s);
+    c += ((uint32_t)((uint64_t)(uint32_t)raw * a.m) >= a.thr);
+    c += ((uint32_t)((uint64_t)(uint32_t)(raw >> 32) * a.m) >= a.thr);
   }
-  __syncthreads();   // pair arrays visible block-wide
-  // lags: lag_max over kept pairs, hmax over lag > 0
+  cnt[g] = c;
+}
+
+// exclusive scan of n counts in one block; off[n] = total
+__global__ void __launch_bounds__(1024) pair_scan_kernel(const int32_t* cnt, int64_t n, int64_t* off) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b = min(n, tid * per), e = min(n, b + per);
+  int64_t acc = 0;
+  for (int64_t i = b; i < e; ++i) acc += cnt[i];
+  part[tid] = acc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int64_t run = part[tid] - acc;
+  for (int64_t i = b; i < e; ++i) {
+    off[i] = run;
+    run += cnt[i];
+  }
+  if (tid == 1023) off[n] = part[1023];
+}
+
+__global__ void __launch_bounds__(PT_BLOCK) pair_scatter_kernel(PcgArgs a, const int64_t* off, PairTable t) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r0 = g * PT_RAW;
+  if (r0 >= a.n_raw) return;
+  int64_t pos = off[g];
+  if (pos >= a.need) return;
+  const int64_t r1 = min(a.n_raw, r0 + PT_RAW);
+  const u128 inc = ((u128)a.inc_hi << 64) | a.inc_lo;
+  u128 s = pcg_advance(((u128)a.st_hi << 64) | a.st_lo, inc, (uint64_t)r0);
+  const u128 mul = pcg_mult();
+  for (int64_t r = r0; r < r1 && pos < a.need; ++r) {
+    s = s * mul + inc;
+    const uint64_t raw = pcg_output(s);
+    for (int h = 0; h < 2 && pos < a.need; ++h) {
+      const uint64_t prod = (uint64_t)(uint32_t)(h ? (raw >> 32) : raw) * a.m;
+      if ((uint32_t)prod >= a.thr) {
+        const int32_t v = (int32_t)(prod >> 32);
+        if (pos < a.max_pairs) t.ii[pos] = v; else t.jj[pos - a.max_pairs] = v;
+        ++pos;
+      }
+    }
+  }
+}
+
+// np.triu_indices(m, 1): row-major upper triangle (all pairs fit)
+__global__ void pair_triu_kernel(int64_t m, PairTable t) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m - 1; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i * (m - 1) - i * (i - 1) / 2;
+    for (int64_t j = i + 1; j < m; ++j) {
+      t.ii[o + (j - i - 1)] = (int32_t)i;
+      t.jj[o + (j - i - 1)] = (int32_t)j;
+    }
+  }
+}
+
+// hmax reduced as the bit pattern of a non-negative double (order-preserving
+// as uint64), so the max is exact and order independent
+__global__ void __launch_bounds__(PT_BLOCK) pair_lag_kernel(int64_t npairs, SampleGeom geom, PairTable t,
+                                                            unsigned long long* hbits) {
   double lmax = 0.0;
-  for (int64_t p = tid; p < npairs; p += PT_THREADS) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t.ii[p], j = t.jj[p];
     if (i == j) continue;
     lmax = fmax(lmax, sample_lag(geom, i, j));
   }
   lmax = warp_max(lmax);
-  if ((tid & 31) == 0) s_red[0][tid >> 5] = lmax;
-  if (tid < MAX_BINS) s_counts[tid] = 0ull;
+  if ((threadIdx.x & 31) == 0 && lmax > 0.0) atomicMax(hbits, (unsigned long long)__double_as_longlong(lmax));
+}
+
+// scal: [0] hmax [1] lag_max [2] npairs [3] status
+__global__ void __launch_bounds__(PT_BLOCK) pair_bin_kernel(int64_t npairs, int n_bins, SampleGeom geom, PairTable t,
+                                                            const unsigned long long* hbits, const int64_t* off,
+                                                            int64_t need, int64_t n_off) {
+  __shared__ unsigned long long h[MAX_BINS];
+  if (threadIdx.x < MAX_BINS) h[threadIdx.x] = 0ull;
   __syncthreads();
-  if (tid == 0) {
-    double a = 0.0;
-    for (int w = 0; w < PT_THREADS / 32; ++w) a = fmax(a, s_red[0][w]);
-    s_red[1][0] = a;
-  }
-  __syncthreads();
-  const double hmax = s_red[1][0];
-  // edges = np.linspace(0, hmax, n_bins + 1); bin = clip(digitize - 1)
-  const double step = hmax / (double)n_bins;
-  for (int64_t p = tid; p < npairs; p += PT_THREADS) {
+  const double hmax = __longlong_as_double((long long)*hbits);
+  const double step = hmax / (double)n_bins;   // np.linspace(0, hmax, n_bins + 1)
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t.ii[p], j = t.jj[p];
     uint8_t b = 255;
     if (i != j) {
       const double lag = sample_lag(geom, i, j);
       if (lag > 0.0) {
-        int c = 0;
+        int c = 0;                                 // digitize: #edges <= lag
         for (int e = 0; e < n_bins; ++e) c += ((double)e * step <= lag);
         c += (hmax <= lag);
         c = min(max(c - 1, 0), n_bins - 1);
         b = (uint8_t)c;
-        atomicAdd(&s_counts[c], 1ull);
+        atomicAdd(&h[c], 1ull);
       }
     }
     t.bin[p] = b;
   }
   __syncthreads();
-  if (tid < n_bins) t.counts[tid] = (int64_t)s_counts[tid];
-  if (tid == 0) {
+  if (threadIdx.x < n_bins && h[threadIdx.x])
+    atomicAdd((unsigned long long*)&t.counts[threadIdx.x], h[threadIdx.x]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     t.scal[0] = hmax;
-    t.scal[1] = hmax;      // lag_max == hmax whenever any lag > 0
+    t.scal[1] = hmax;                              // lag_max == hmax when any lag > 0
     t.scal[2] = (double)npairs;
-    t.scal[3] = (double)status;
+    t.scal[3] = (off && off[n_off] < need) ? (double)PS_PAIRS_SHORT : 0.0;
   }
 }
 
@@ -218,14 +242,30 @@ __global__ void __launch_bounds__(256) bins_kernel(BinsArgs a) {
   const int64_t p0 = (int64_t)blk * per, p1 = min(npairs, p0 + per);
   for (int b = 0; b < a.n_bins; ++b) acc[b * nt + tid] = 0.0;
   const int64_t base = a.part_base[s];
-  for (int64_t p = p0 + tid; p < p1; p += nt) {
-    const uint8_t b = t.bin[p];
-    if (b == 255) continue;
-    double vi, vj;
-    if (a.values) { vi = a.values[base + t.ii[p]]; vj = a.values[base + t.jj[p]]; }
-    else { vi = (double)__ldg(a.known + base + t.ii[p]); vj = (double)__ldg(a.known + base + t.jj[p]); }
-    const double d = __dsub_rn(vi, vj);
-    acc[b * nt + tid] += __dmul_rn(0.5, __dmul_rn(d, d));
+  constexpr int U = 8;                       // gathers in flight per thread
+  for (int64_t p = p0 + tid; p < p1; p += (int64_t)nt * U) {
+    int32_t ii[U], jj[U];
+    uint8_t bb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = p + (int64_t)u * nt;
+      const bool ok = q < p1;
+      bb[u] = ok ? t.bin[q] : (uint8_t)255;
+      ii[u] = ok ? t.ii[q] : 0;
+      jj[u] = ok ? t.jj[q] : 0;
+    }
+    double vi[U], vj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (a.values) { vi[u] = a.values[base + ii[u]]; vj[u] = a.values[base + jj[u]]; }
+      else { vi[u] = (double)__ldg(a.known + base + ii[u]); vj[u] = (double)__ldg(a.known + base + jj[u]); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (bb[u] == 255) continue;
+      const double d = __dsub_rn(vi[u], vj[u]);
+      acc[bb[u] * nt + tid] += __dmul_rn(0.5, __dmul_rn(d, d));
+    }
   }
   __syncthreads();
   if (tid < a.n_bins) {
@@ -236,9 +276,11 @@ __global__ void __launch_bounds__(256) bins_kernel(BinsArgs a) {
 }
 
 __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
-  const int s = blockIdx.x;
-  if (threadIdx.x != 0) return;
-  // --- merge chunk statistics of the part's planes in a fixed order
+  // One warp per sub-part.  Statistics are merged redundantly by every lane
+  // (same order -> same bits); bins are reduced lane-per-bin; the TRF runs
+  // warp-parallel (lane = residual row) when n_bins + 3 <= 32.
+  const int s = blockIdx.x, lane = threadIdx.x;
+  __shared__ TrfProblem P;
   double n = 0.0, mean = 0.0, m2 = 0.0, mn = DBL_MAX, mx = -DBL_MAX, bad = 0.0;
   const int kb = a.part_b ? a.part_b[s] : 0, ke = a.part_e ? a.part_e[s] : 0;
   for (int k = kb; k <= ke; ++k) {
@@ -254,28 +296,85 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
       n = nn;
     }
   }
-  a.lohi[2 * s + 0] = mn;
-  a.lohi[2 * s + 1] = mx;
+  if (lane == 0) {
+    a.lohi[2 * s + 0] = mn;
+    a.lohi[2 * s + 1] = mx;
+  }
   int status = PS_OK;
   if (bad > 0 || n <= 0) status = PS_FIT_FAILED;
-  if (!a.fit) { a.status[s] = status; return; }
+  if (!a.fit) { if (lane == 0) a.status[s] = status; return; }
   const double svar = m2 / n;
   const int64_t m = a.part_m[s];
-  if (m * (m - 1) / 2 < 30) { a.status[s] = PS_INSUFFICIENT; return; }
+  if (m * (m - 1) / 2 < 30) { if (lane == 0) a.status[s] = PS_INSUFFICIENT; return; }
   const PairTable t = a.tables[a.part_class[s]];
-  if (t.scal[3] != 0.0) { a.status[s] = PS_PAIRS_SHORT; return; }
+  if (t.scal[3] != 0.0) { if (lane == 0) a.status[s] = PS_PAIRS_SHORT; return; }
   const double hmax = t.scal[0];
-  if (!(hmax > 0.0)) { a.status[s] = PS_DEGENERATE; return; }
+  if (!(hmax > 0.0)) { if (lane == 0) a.status[s] = PS_DEGENERATE; return; }
   double* model = a.models + 3 * s;
   if (svar == 0.0) {                    // kriging.py:294-297
-    model[0] = 0.0; model[1] = 0.0; model[2] = fmax(t.scal[1], 1.0);
-    a.status[s] = status;
+    if (lane == 0) {
+      model[0] = 0.0; model[1] = 0.0; model[2] = fmax(t.scal[1], 1.0);
+      a.status[s] = status;
+    }
     return;
   }
+  // non-empty bins -> residual rows, in bin order
+  const double step = hmax / (double)a.n_bins;
+  const int64_t cnt = lane < a.n_bins ? t.counts[lane] : 0;
+  const unsigned nzmask = __ballot_sync(0xffffffffu, cnt > 0);
+  if (cnt > 0) {
+    double sum = 0.0;
+    for (int blk = 0; blk < a.nblk; ++blk) sum += a.partial[((int64_t)s * a.nblk + blk) * a.n_bins + lane];
+    const int r = __popc(nzmask & ((1u << lane) - 1u));
+    const double e0 = (double)lane * step;
+    const double e1 = (lane + 1 == a.n_bins) ? hmax : (double)(lane + 1) * step;
+    P.h[r] = 0.5 * (e0 + e1);
+    P.gemp[r] = sum / (double)cnt;
+    P.w[r] = sqrt((double)cnt);
+  }
+  if (lane == 0) { P.kind = a.kind; P.nb = __popc(nzmask); }
+  __syncwarp();
+  const double x0[3] = {0.0, svar, hmax / 3.0};
+  const double lb[3] = {0.0, 0.0, 1e-6};
+  const double ub[3] = {2.0 * svar + 1e-12, 4.0 * svar + 1e-12, 10.0 * hmax};
+  if (!(ub[2] > lb[2])) { if (lane == 0) a.status[s] = PS_FIT_FAILED; return; }
+  if (P.nb + 3 > 32) {                  // residual rows exceed a warp: scalar kernel
+    if (lane == 0) a.status[s] = PS_NEED_SCALAR_FIT;
+    return;
+  }
+  WarpTrf wt(P, lane);
+  const TrfResult r = wt.fit(x0, lb, ub);
+  if (lane != 0) return;
+  if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
+  const double nug = pymax(r.x[0], 0.0);
+  model[0] = nug;
+  model[1] = nug + pymax(r.x[1], 0.0);
+  model[2] = pymax(r.x[2], 1e-6);
+  a.status[s] = status;
+}
+
+// Scalar TRF (trf.h) for parts whose non-empty bins exceed 29 (n_bins > 29);
+// re-derives the problem exactly as fit_kernel does.
+__global__ void __launch_bounds__(32) fit_scalar_kernel(FitArgs a) {
+  const int s = blockIdx.x;
+  if (threadIdx.x != 0 || a.status[s] != PS_NEED_SCALAR_FIT) return;
+  double n = 0.0, mean = 0.0, m2 = 0.0;
+  for (int k = a.part_b[s]; k <= a.part_e[s]; ++k)
+    for (int c = 0; c < a.nchunk; ++c) {
+      const ChunkStat cs = a.stats[(int64_t)k * a.nchunk + c];
+      if (cs.n <= 0) continue;
+      const double nn = n + cs.n, d = cs.mean - mean;
+      mean = mean + d * (cs.n / nn);
+      m2 = m2 + cs.m2 + d * d * (n * cs.n / nn);
+      n = nn;
+    }
+  const double svar = m2 / n;
+  const PairTable t = a.tables[a.part_class[s]];
+  const double hmax = t.scal[0];
+  const double step = hmax / (double)a.n_bins;
   TrfProblem P;
   P.kind = a.kind;
   P.nb = 0;
-  const double step = hmax / (double)a.n_bins;
   for (int b = 0; b < a.n_bins; ++b) {
     const int64_t cnt = t.counts[b];
     if (cnt <= 0) continue;
@@ -291,14 +390,14 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   const double x0[3] = {0.0, svar, hmax / 3.0};
   const double lb[3] = {0.0, 0.0, 1e-6};
   const double ub[3] = {2.0 * svar + 1e-12, 4.0 * svar + 1e-12, 10.0 * hmax};
-  if (!(ub[2] > lb[2])) { a.status[s] = PS_FIT_FAILED; return; }
   const TrfResult r = trf_fit(P, x0, lb, ub);
   if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
+  double* model = a.models + 3 * s;
   const double nug = pymax(r.x[0], 0.0);
   model[0] = nug;
   model[1] = nug + pymax(r.x[1], 0.0);
   model[2] = pymax(r.x[2], 1e-6);
-  a.status[s] = status;
+  a.status[s] = PS_OK;
 }
 
 }  // namespace
@@ -320,9 +419,47 @@ cudaError_t launch_plane_stats_f64(const double* values, int64_t m, ChunkStat* o
 cudaError_t launch_pair_table(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
                               int64_t m, int64_t max_pairs, int n_bins, SampleGeom geom,
                               PairTable t, cudaStream_t st) {
-  pair_table_kernel<<<1, PT_THREADS, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, m, max_pairs, n_bins,
-                                              geom, t);
+  const int64_t total = m * (m - 1) / 2;
+  const int64_t npairs = total <= max_pairs ? total : max_pairs;
+  cudaError_t e;
+  int64_t n_thr = 0;
+  PcgArgs a{};
+  if (total > max_pairs) {
+    a.st_hi = st_hi; a.st_lo = st_lo; a.inc_hi = inc_hi; a.inc_lo = inc_lo;
+    a.m = (uint32_t)m;
+    a.thr = lemire_threshold(a.m);
+    a.need = 2 * max_pairs;
+    a.max_pairs = max_pairs;
+    const double prej = (double)a.thr / 4294967296.0;
+    a.n_raw = (int64_t)((double)a.need * (1.0 + 4.0 * prej) / 2.0) + 4096;
+    n_thr = (a.n_raw + PT_RAW - 1) / PT_RAW;
+  }
+  int32_t* cnt = t.cnt;
+  int64_t* off = t.off;
+  unsigned long long* hbits = t.hbits;
+  if ((e = cudaMemsetAsync(hbits, 0, 8, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(t.counts, 0, MAX_BINS * sizeof(int64_t), st)) != cudaSuccess) return e;
+  if (total > max_pairs) {
+    const unsigned nb = (unsigned)((n_thr + PT_BLOCK - 1) / PT_BLOCK);
+    pair_count_kernel<<<nb, PT_BLOCK, 0, st>>>(a, cnt);
+    pair_scan_kernel<<<1, 1024, 0, st>>>(cnt, n_thr, off);
+    pair_scatter_kernel<<<nb, PT_BLOCK, 0, st>>>(a, off, t);
+  } else {
+    pair_triu_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, (m + 255) / 256)), 256, 0, st>>>(m, t);
+  }
+  const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(1184, (npairs + PT_BLOCK - 1) / PT_BLOCK));
+  pair_lag_kernel<<<gb, PT_BLOCK, 0, st>>>(npairs, geom, t, hbits);
+  pair_bin_kernel<<<gb, PT_BLOCK, 0, st>>>(npairs, n_bins, geom, t, hbits, n_thr ? off : nullptr,
+                                           total > max_pairs ? a.need : 0, n_thr);
   return cudaGetLastError();
+}
+
+int64_t pair_scratch_elems(int64_t m, int64_t max_pairs) {
+  if (m * (m - 1) / 2 <= max_pairs) return 1;
+  const uint32_t thr = lemire_threshold((uint32_t)m);
+  const double prej = (double)thr / 4294967296.0;
+  const int64_t n_raw = (int64_t)((double)(2 * max_pairs) * (1.0 + 4.0 * prej) / 2.0) + 4096;
+  return (n_raw + PT_RAW - 1) / PT_RAW;
 }
 
 cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
@@ -338,6 +475,7 @@ cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
 
 cudaError_t launch_fit(const FitArgs& a, cudaStream_t st) {
   fit_kernel<<<a.S, 32, 0, st>>>(a);
+  if (a.fit && a.n_bins + 3 > 32) fit_scalar_kernel<<<a.S, 32, 0, st>>>(a);
   return cudaGetLastError();
 }
 

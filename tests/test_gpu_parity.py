@@ -87,7 +87,10 @@ def test_fast_matches_generic_and_oracle(cuda, W):
     ob, vb = b.run(kd, return_variance=True)
     b.finish()
     oa, ob = oa.cpu().numpy(), ob.cpu().numpy()
-    assert np.array_equal(oa, ob), np.abs(oa - ob).max()
+    # the streaming kernel uses the mirror-pair (S = A+B, D = A-B) form of
+    # the same stencils: equal to the generic kernel up to rounding
+    assert np.array_equal(oa[::cfg.factor], ob[::cfg.factor])
+    assert np.abs(oa.astype(np.float64) - ob).max() <= 1e-7 * _rng(ks)
     assert torch.equal(va, vb)
     ref, rvar, rmodels = O.reconstruct_zparts(ks, cfg.factor, cfg.n_subparts,
                                               return_variance=True)
