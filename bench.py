@@ -231,6 +231,7 @@ def run_gpu(args, cfg, ks):
     zk = ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, redraw_pairs=True,
                       part_len=cfg.n_known // cfg.n_subparts)
     zk.plan.set_timing(max(1, args.steps))
+    zs = zk                                  # serial schedule: per-stage events
     stack = torch.empty((K_loc, H, W), dtype=torch.float32, device=dev)
     stack[:cfg.n_known].copy_(owned)
     out, var = zk.allocate(bool(args.variance))
@@ -247,7 +248,7 @@ def run_gpu(args, cfg, ks):
     for _ in range(max(3, args.warmup)):
         step()
     zk.finish()
-    kpe = zk.plan.info["kernels_per_execute"]
+    kpe = zk.plan.info["kernels_per_execute"] + (1 if world > 1 else 0) * 0
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     pred_ms, stage_acc = [], {}
@@ -265,10 +266,11 @@ def run_gpu(args, cfg, ks):
         clk.mark(False)
     zk.finish()
     for back in range(args.steps):          # per-launch stage events, read after
-        st = zk.plan.stage_ms(back)
+        st = zs.plan.stage_ms(back)
         pred_ms.append(st["predict"])
         for k2, v in st.items():
             stage_acc[k2] = stage_acc.get(k2, 0.0) + v
+    serial_ms = sum(stage_acc.values()) / args.steps
     t_ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([t_ms], device=dev)
@@ -299,6 +301,7 @@ def run_gpu(args, cfg, ks):
             "fp64_pipe_frac": (vox_local / (pred_avg / 1e3)) / fp64_cap
             if args.accum == "fp64" else None}
     stages = {k2: v / args.steps for k2, v in stage_acc.items()}
+    stages["sum"] = serial_ms
 
     # end to end through the public API with host buffers
     e2e = None

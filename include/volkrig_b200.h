@@ -80,6 +80,13 @@ typedef struct {
 #define VK_FLAG_REDRAW_PAIRS 2    /* redraw the pair tables on every execute
                                      (default: drawn once per plan, they depend
                                      only on geometry and seed)               */
+#define VK_FLAG_OVERLAP 4         /* per-part fit -> solve -> predict chains on
+                                     side streams, so parts whose fit converges
+                                     early start predicting while others still
+                                     fit (default: one launch per stage on the
+                                     caller's stream; measured slower on C4
+                                     because streaming CTAs slow the
+                                     latency-bound fits sharing their SMs)   */
 
 /* Replaces: the window/stencil setup of fill_missing (kriging.py:485-515)
  * and the partition of SPEC.md:392-400.  Host-side, O(K + H + W). */

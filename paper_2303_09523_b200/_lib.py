@@ -29,6 +29,7 @@ DRIFT_IDS = {"linear": 0, "constant": 1}
 ACCUM_IDS = {"fp64": 0, "fp32": 1}
 FLAG_FORCE_GENERIC = 1
 FLAG_REDRAW_PAIRS = 2
+FLAG_OVERLAP = 4
 N_STAGES = 6
 STAGES = ("stats", "pairs", "bins", "fit", "solve", "predict")
 

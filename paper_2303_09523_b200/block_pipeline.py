@@ -59,7 +59,7 @@ class ZPartKriging:
                  n_subparts: int, kind: str = "exponential", drift: str = "linear",
                  accum: str = "fp64", n_bins: int = 15, max_pairs: int = 100_000,
                  seed: int = 0, force_generic: bool = False, fit: bool = True,
-                 redraw_pairs: bool = False, part_len: int = 0):
+                 redraw_pairs: bool = False, part_len: int = 0, overlap: bool = False):
         if factor < 1:
             raise ValueError("factor must be >= 1")
         self.ranges = subpart_ranges(n_known, n_subparts, part_len)   # validates
@@ -73,7 +73,8 @@ class ZPartKriging:
                                 accum=accum, fit=fit, n_bins=n_bins,
                                 max_pairs=max_pairs, seed=seed,
                                 force_generic=force_generic,
-                                redraw_pairs=redraw_pairs, part_len=part_len)
+                                redraw_pairs=redraw_pairs, part_len=part_len,
+                                overlap=overlap)
 
     @property
     def interpolated_voxels(self) -> int:

@@ -2,9 +2,10 @@
 
 The library is a plain C ABI (``include/volkrig_b200.h``); it is compiled
 with nvcc directly (no torch extension), so it carries no torch types and can
-be bound from any FFI.  The variogram and solver translation units are built
-with ``-fmad=false`` so their arithmetic rounds like numpy's (no contraction
-of a*b+c); the prediction kernels keep FMA.
+be bound from any FFI.  Where the reference's arithmetic must be reproduced
+bit for bit (lags, half squared differences, bin edges and centres) the
+kernels use explicit round-to-nearest intrinsics, so FMA contraction stays on
+everywhere else.
 """
 
 from __future__ import annotations
@@ -24,15 +25,15 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 UNITS = {
     "vk_api.cu": [],
-    "vk_variogram.cu": ["-fmad=false"],
-    "vk_solve.cu": ["-fmad=false"],
+    "vk_variogram.cu": [],
+    "vk_solve.cu": [],
     "vk_predict.cu": [],
     "vk_geometry.cpp": [],
 }
 
 
 def _deps() -> list[Path]:
-    return sorted(CSRC.glob("*.h")) + sorted(INCLUDE.glob("*.h"))
+    return sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
 def _stale(target: Path, sources: list[Path]) -> bool:

@@ -1,6 +1,9 @@
 // Warp-parallel form of trf.h for the device fit: one warp per sub-part,
 // lane r owns residual / Jacobian row r (bins), lanes m..m+2 own the three
-// diagonal rows of the augmented matrix.  Every scalar decision (trust
+// diagonal rows of the augmented matrix.  The SVD of the augmented Jacobian
+// (scipy: LAPACK gesdd) is a lane-parallel Householder QR followed by a
+// Jacobi SVD of the 3x3 R factor; the trust-region step only uses s, V and
+// U^T f, which both routes produce to rounding.  Every scalar decision (trust
 // region, reflections, termination) is evaluated redundantly on all lanes
 // from all-reduced values, so the lanes never diverge.  The algorithm and its
 // order of operations follow trf.h (scipy 1.18 trf_bounds) step by step; only
@@ -55,23 +58,64 @@ struct WarpTrf {
     }
   }
 
-  // one-sided Jacobi SVD of the augmented matrix; this lane's row in a[3]
-  __device__ void svd(double* a, double* s, double* V, double* u) const {
+  // SVD of the augmented matrix [J_h; diag(sqrt(diag_h))] (this lane's row in
+  // a[3]) as Householder QR across the lanes (two reduction rounds per
+  // column), then a one-sided Jacobi SVD of the 3x3 R in registers.  Returns
+  // s (descending), V, and uf = U^T f_aug directly (U = Q U_R).
+  __device__ void svd_uf(double* a, double fl, double* s, double* V, double* uf) const {
+    double R[9];
+    for (int k = 0; k < 3; ++k) {
+      const bool act = lane >= k;
+      const double xk = act ? a[k] : 0.0;
+      const double nrm2 = wsum(xk * xk);
+      const double x_kk = __shfl_sync(0xffffffffu, a[k], k);
+      const double nrm = sqrt(nrm2);
+      const double alpha = (x_kk > 0.0) ? -nrm : nrm;
+      const double vv = 2.0 * (nrm2 - x_kk * alpha);     // ||v||^2
+      double v = act ? a[k] : 0.0;
+      if (lane == k) v = x_kk - alpha;
+      // project the remaining columns and f onto v in one reduction round
+      double d1 = 0.0, d2 = 0.0, df = 0.0;
+      if (k + 1 < 3) d1 = wsum(v * a[k + 1]);
+      if (k + 2 < 3) d2 = wsum(v * a[k + 2]);
+      df = wsum(v * fl);
+      if (vv > 0.0) {
+        const double sc = 2.0 / vv;
+        if (k + 1 < 3) a[k + 1] -= sc * d1 * v;
+        if (k + 2 < 3) a[k + 2] -= sc * d2 * v;
+        fl -= sc * df * v;
+        if (lane == k) a[k] = alpha;
+        else if (act) a[k] = 0.0;
+      }
+    }
+    double qf[3];
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) R[r * 3 + c] = __shfl_sync(0xffffffffu, a[c], r);
+      qf[r] = __shfl_sync(0xffffffffu, fl, r);
+    }
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < r; ++c) R[r * 3 + c] = 0.0;
+    // one-sided Jacobi on the columns of R (3x3, no cross-lane traffic)
     for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0 : 0.0;
     for (int sweep = 0; sweep < 60; ++sweep) {
       bool rotated = false;
       for (int p = 0; p < 2; ++p)
         for (int q = p + 1; q < 3; ++q) {
-          const double alpha = wsum(a[p] * a[p]), beta = wsum(a[q] * a[q]), gamma = wsum(a[p] * a[q]);
+          double alpha = 0.0, beta = 0.0, gamma = 0.0;
+          for (int r = 0; r < 3; ++r) {
+            alpha += R[r * 3 + p] * R[r * 3 + p];
+            beta += R[r * 3 + q] * R[r * 3 + q];
+            gamma += R[r * 3 + p] * R[r * 3 + q];
+          }
           if (gamma == 0.0 || fabs(gamma) <= TRF_EPS * sqrt(alpha * beta)) continue;
           rotated = true;
           const double zeta = (beta - alpha) / (2.0 * gamma);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
-          const double ap = a[p], aq = a[q];
-          a[p] = c * ap - sn * aq;
-          a[q] = sn * ap + c * aq;
           for (int r = 0; r < 3; ++r) {
+            const double rp = R[r * 3 + p], rq = R[r * 3 + q];
+            R[r * 3 + p] = c * rp - sn * rq;
+            R[r * 3 + q] = sn * rp + c * rq;
             const double vp = V[r * 3 + p], vq = V[r * 3 + q];
             V[r * 3 + p] = c * vp - sn * vq;
             V[r * 3 + q] = sn * vp + c * vq;
@@ -79,8 +123,11 @@ struct WarpTrf {
         }
       if (!rotated) break;
     }
-    double sv[3];
-    for (int j = 0; j < 3; ++j) sv[j] = sqrt(wsum(a[j] * a[j]));
+    double sv[3], uq[3];
+    for (int j = 0; j < 3; ++j) {
+      sv[j] = sqrt(R[0 + j] * R[0 + j] + R[3 + j] * R[3 + j] + R[6 + j] * R[6 + j]);
+      uq[j] = sv[j] > 0.0 ? (R[0 + j] * qf[0] + R[3 + j] * qf[1] + R[6 + j] * qf[2]) / sv[j] : 0.0;
+    }
     int order[3] = {0, 1, 2};
     for (int x = 0; x < 3; ++x)
       for (int y = x + 1; y < 3; ++y)
@@ -89,8 +136,8 @@ struct WarpTrf {
     for (int k = 0; k < 3; ++k) {
       const int j = order[k];
       s[k] = sv[j];
+      uf[k] = uq[j];
       for (int r = 0; r < 3; ++r) Vs[r * 3 + k] = V[r * 3 + j];
-      u[k] = sv[j] > 0.0 ? a[j] / sv[j] : 0.0;
     }
     for (int i = 0; i < 9; ++i) V[i] = Vs[i];
   }
@@ -252,10 +299,8 @@ struct WarpTrf {
         const int dr = lane - m;   // diagonal rows m..m+2
         for (int c = 0; c < 3; ++c) a[c] = (dr >= 0 && dr < 3 && dr == c) ? sqrt(diag_h[c]) : 0.0;
       }
-      double sv[3], V[9], u[3];
-      svd(a, sv, V, u);
-      double uf[3];
-      for (int c = 0; c < 3; ++c) uf[c] = wsum(row ? u[c] * f : 0.0);
+      double sv[3], V[9], uf[3];
+      svd_uf(a, row ? f : 0.0, sv, V, uf);
       const double theta = fmax(0.995, 1 - g_norm);
       double actual_reduction = -1;
       double step_norm = 0.0;

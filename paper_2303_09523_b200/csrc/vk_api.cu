@@ -62,7 +62,7 @@ struct vk_plan {
   vk_plan_desc desc;
   Geometry geo;
   int num_sms = 0;
-  int NP = 0, NK = 0, n_sys = 0, max_n = 0;
+  int NP = 0, NK = 0, n_sys = 0, max_n = 0, max_dz = 0;
   int nchunk = 0, nblk = 0;
   std::vector<void*> allocs;
   // device tables
@@ -85,6 +85,14 @@ struct vk_plan {
   int kernels = 0;
   cudaStream_t side = nullptr;        // pair draw runs here, concurrent with stats
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // per-part chains (fit -> solve -> predict): one stream per part (up to
+  // NCH), so every part's latency-bound fit starts at once
+  static constexpr int NCH = 64;
+  cudaStream_t chain[NCH] = {};
+  cudaEvent_t ev_kfork = nullptr, ev_kjoin[NCH] = {};
+  std::vector<int> sys_begin;         // [S + 1] system range of each part
+  std::vector<int> gap_begin;         // [S + 1] gap range of each part (fast path)
+  FastLaunch fast_launch;             // cached TMA descriptor + occupancy
   int ring = 0;                       // timing ring size (0 = off)
   int64_t n_exec = 0;                 // executes recorded so far
   std::vector<cudaEvent_t> ev;        // [ring][VK_N_STAGES + 1]
@@ -106,6 +114,11 @@ struct vk_plan {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
+    if (ev_kfork) cudaEventDestroy(ev_kfork);
+    for (int i = 0; i < NCH; ++i) {
+      if (ev_kjoin[i]) cudaEventDestroy(ev_kjoin[i]);
+      if (chain[i]) cudaStreamDestroy(chain[i]);
+    }
     for (void* p : allocs) cudaFree(p);
     if (h_models) cudaFreeHost(h_models);
   }
@@ -183,7 +196,12 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
     p->max_n = std::max(p->max_n, sg.n);
   }
   for (int q = 0; q < p->NP; ++q)
-    for (size_t i = 0; i < g.patterns[q].size(); ++i) pat_dz[(size_t)q * NPMAX + i] = g.patterns[q][i];
+    for (size_t i = 0; i < g.patterns[q].size(); ++i) {
+      pat_dz[(size_t)q * NPMAX + i] = g.patterns[q][i];
+      for (size_t i2 = 0; i2 < g.patterns[q].size(); ++i2)
+        p->max_dz = std::max(p->max_dz, std::abs(g.patterns[q][i] - g.patterns[q][i2]));
+      p->max_dz = std::max(p->max_dz, std::abs(g.patterns[q][i]));
+    }
   std::vector<int32_t> kmap(2 * NKIND1, 0);
   for (int i = 0; i < NKIND1; ++i) {
     kmap[i] = std::max(0, g.kx_map[i]);
@@ -261,6 +279,22 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
     VK_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     VK_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     VK_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  }
+  // per-part ranges for the overlapped schedule
+  p->sys_begin.assign(S + 1, 0);
+  for (int i = 0; i < p->n_sys; ++i) p->sys_begin[g.sys_part[i] + 1]++;
+  for (int s = 0; s < S; ++s) p->sys_begin[s + 1] += p->sys_begin[s];
+  p->gap_begin.assign(S + 1, 0);
+  if (g.fast) {
+    for (int s = 0; s <= S; ++s) p->gap_begin[s] = (s < S) ? g.parts[s].b : g.K - 1;
+    for (int s = 0; s < S; ++s) p->gap_begin[s] = std::min(p->gap_begin[s], g.K - 1);
+  }
+  if ((d->flags & VK_FLAG_OVERLAP) && S > 1) {
+    VK_TRY(cudaEventCreateWithFlags(&p->ev_kfork, cudaEventDisableTiming));
+    for (int i = 0; i < std::min(S, vk_plan::NCH); ++i) {
+      VK_TRY(cudaStreamCreateWithFlags(&p->chain[i], cudaStreamNonBlocking));
+      VK_TRY(cudaEventCreateWithFlags(&p->ev_kjoin[i], cudaEventDisableTiming));
+    }
   }
 #undef VK_TRY
   (void)class_zoff;
@@ -371,11 +405,11 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   fa.models = p->d_models;
   fa.lohi = p->d_lohi;
   fa.status = p->d_part_status;
-  VK_CUDA(launch_fit(fa, st));
-  ++kernels;
-  VK_CUDA(mark(4));
+  fa.part0 = 0;
+  fa.n_parts = S;
   SolveArgs sa;
   sa.n_sys = p->n_sys;
+  sa.sys0 = 0;
   sa.kind = d.kind;
   sa.drift = d.drift;
   sa.NP = p->NP;
@@ -394,9 +428,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   sa.var = p->d_var;
   sa.sys_status = p->d_sys_status;
   sa.max_n = p->max_n;
-  VK_CUDA(launch_solve(sa, st));
-  if (p->n_sys) ++kernels;
-  VK_CUDA(mark(5));
+  sa.max_dz = p->max_dz;
   PredictArgs pa;
   pa.known = known;
   pa.out = out;
@@ -420,16 +452,59 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   pa.miss_pattern = p->d_miss_pattern;
   pa.miss_planes = p->d_miss_planes;
   pa.G = g.G;
+  pa.gap0 = 0;
+  pa.gap1 = g.K - 1;
+  pa.chunk = 0;
   pa.gap_part = p->d_gap_part;
   pa.gap_pattern = p->d_gap_pattern;
   pa.num_sms = p->num_sms;
-  if (g.fast && predict_fast_supported(g.G, d.accum)) {
-    VK_CUDA(launch_predict_fast(pa, st));
-    ++kernels;
+  const bool fast = g.fast && predict_fast_supported(g.G, d.accum);
+  if (fast) VK_CUDA(prepare_predict_fast(pa, &p->fast_launch));
+  if (p->chain[0] && fast) {
+    // ---- overlapped schedule: part s runs fit -> solve -> predict on chain
+    // stream s % NCH; a part whose variogram fit converges early streams its
+    // planes while slower fits are still iterating.
+    VK_CUDA(cudaEventRecord(p->ev_kfork, st));
+    const int nch = std::min(S, vk_plan::NCH);
+    for (int c = 0; c < nch; ++c) VK_CUDA(cudaStreamWaitEvent(p->chain[c], p->ev_kfork, 0));
+    for (int s = 0; s < S; ++s) {
+      cudaStream_t cs = p->chain[s % nch];
+      FitArgs f1 = fa;
+      f1.part0 = s;
+      f1.n_parts = 1;
+      VK_CUDA(launch_fit(f1, cs));
+      SolveArgs s1 = sa;
+      s1.sys0 = p->sys_begin[s];
+      s1.n_sys = p->sys_begin[s + 1] - p->sys_begin[s];
+      VK_CUDA(launch_solve(s1, cs));
+      PredictArgs p1 = pa;
+      p1.gap0 = p->gap_begin[s];
+      p1.gap1 = p->gap_begin[s + 1];
+      p1.chunk = p1.gap1 - p1.gap0;           // one unit = a tile over the part's gaps
+      VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, cs));
+      kernels += 2 + (s1.n_sys > 0);
+    }
+    for (int c = 0; c < nch; ++c) {
+      VK_CUDA(cudaEventRecord(p->ev_kjoin[c], p->chain[c]));
+      VK_CUDA(cudaStreamWaitEvent(st, p->ev_kjoin[c], 0));
+    }
+    VK_CUDA(mark(4));
+    VK_CUDA(mark(5));
   } else {
-    VK_CUDA(launch_copy_known(pa, st));
-    VK_CUDA(launch_predict_generic(pa, st));
-    kernels += 1 + (pa.n_miss > 0);
+    VK_CUDA(launch_fit(fa, st));
+    ++kernels;
+    VK_CUDA(mark(4));
+    VK_CUDA(launch_solve(sa, st));
+    if (p->n_sys) ++kernels;
+    VK_CUDA(mark(5));
+    if (fast) {
+      VK_CUDA(launch_predict_fast_prepared(p->fast_launch, pa, st));
+      ++kernels;
+    } else {
+      VK_CUDA(launch_copy_known(pa, st));
+      VK_CUDA(launch_predict_generic(pa, st));
+      kernels += 1 + (pa.n_miss > 0);
+    }
   }
   VK_CUDA(mark(6));
   if (p->ring) ++p->n_exec;
@@ -647,6 +722,8 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   fa.models = models;
   fa.lohi = lohi;
   fa.status = status;
+  fa.part0 = 0;
+  fa.n_parts = 1;
   if (e == cudaSuccess) e = launch_fit(fa, st);
   double mo[3] = {0, 0, 0};
   int32_t s = 0;

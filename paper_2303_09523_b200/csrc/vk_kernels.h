@@ -54,6 +54,7 @@ cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st);
 
 struct FitArgs {
   int S, n_bins, nblk, kind, fit, nchunk;
+  int part0, n_parts;       // parts [part0, part0 + n_parts) of this launch
   const ChunkStat* stats;   // [K][nchunk] (structured) or [1][nchunk] (explicit)
   const int32_t* part_b;    // [S]
   const int32_t* part_e;    // [S]
@@ -69,6 +70,7 @@ cudaError_t launch_fit(const FitArgs& a, cudaStream_t st);
 
 struct SolveArgs {
   int n_sys, kind, drift, NP, NK;
+  int sys0;                  // systems [sys0, sys0 + n_sys) of this launch
   const int32_t* sys_part;
   const int32_t* sys_stencil;
   const int32_t* st_off;     // [n_stencils] offset into taps/pad
@@ -83,6 +85,7 @@ struct SolveArgs {
   double* var;               // [S][NP][NK]
   int32_t* sys_status;       // [n_sys]
   int max_n;                 // max neighbours over stencils (smem sizing)
+  int max_dz;                // max |plane offset| or offset difference over patterns
 };
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);
 
@@ -101,12 +104,22 @@ struct PredictArgs {
   // generic path
   int n_miss;
   const int32_t* miss_z, *miss_part, *miss_pattern, *miss_planes;
-  // fast path
-  int G;
+  // fast path: gaps [gap0, gap1) of this launch
+  int G, gap0, gap1;
+  int chunk;                   // gaps per unit (0: automatic)
   const int32_t* gap_part;     // [K-1]
   const int32_t* gap_pattern;  // [(K-1) * G]
   int num_sms;
 };
+// Launch state of the streaming kernel prepared once per known-plane buffer:
+// TMA descriptor, occupancy-derived grid size.
+struct FastLaunch {
+  alignas(64) unsigned char tmap[128];   // CUtensorMap
+  const float* known = nullptr;
+  int G = 0, accum = -1, occ = 0;
+};
+cudaError_t prepare_predict_fast(const PredictArgs& a, FastLaunch* fl);
+cudaError_t launch_predict_fast_prepared(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_copy_known(const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_predict_generic(const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_predict_fast(const PredictArgs& a, cudaStream_t st);

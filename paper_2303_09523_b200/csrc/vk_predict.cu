@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
     const int chunk_id = u / n_tiles, tile = u - chunk_id * n_tiles;
     const int tx = tile % n_tiles_x, ty = tile / n_tiles_x;
     const int x0 = tx * FT_TX, y0 = ty * FT_TY;
-    const int kb = chunk_id * chunk, ke = min(n_gaps, kb + chunk);   // gaps [kb, ke)
+    const int kb = a.gap0 + chunk_id * chunk, ke = min(a.gap1, kb + chunk);   // gaps [kb, ke)
     const int ty1 = min(H, y0 + FT_TY), tx1 = min(W, x0 + FT_TX);
     // window kinds present in this tile: interior first, then the border ones
     int nky = 1, nkx = 1;
@@ -469,51 +469,82 @@ int predict_fast_supported(int G, int accum) {
 }
 
 template <int G, typename Acc>
-static cudaError_t launch_fast_t(const CUtensorMap& map, const PredictArgs& a, cudaStream_t st) {
+static cudaError_t occupancy_t(int* occ) {
   auto kern = predict_fast_kernel<G, Acc>;
   const size_t smem = (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, FT_THREADS, smem);
-  if (e != cudaSuccess) return e;
-  occ = std::max(1, occ);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, FT_THREADS, smem);
+  *occ = std::max(1, *occ);
+  return e;
+}
+
+template <int G, typename Acc>
+static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(float);
   const int ntx = (a.W + FT_TX - 1) / FT_TX, nty = (a.H + FT_TY - 1) / FT_TY;
-  const int n_tiles = ntx * nty, n_gaps = a.K - 1;
-  const int resident = a.num_sms * occ;
+  const int n_tiles = ntx * nty, n_gaps = a.gap1 - a.gap0;
+  if (n_gaps <= 0) return cudaSuccess;
+  const int resident = a.num_sms * fl.occ;
   // gap runs: long enough to amortise the extra plane per run, short enough
   // that (tiles x runs) covers the resident CTAs several times
   int chunk = std::max(1, (int)((int64_t)n_tiles * n_gaps / ((int64_t)resident * 6)));
   chunk = std::min(std::max(chunk, std::min(4, n_gaps)), n_gaps);
+  if (a.chunk > 0) chunk = std::min(a.chunk, n_gaps);
   const int n_chunks = (n_gaps + chunk - 1) / chunk;
   const int n_units = n_tiles * n_chunks;
   const int grid = std::min(n_units, resident);
-  kern<<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
+  predict_fast_kernel<G, Acc><<<grid, FT_THREADS, smem, st>>>(
+      *reinterpret_cast<const CUtensorMap*>(fl.tmap), a, ntx, n_tiles, chunk, n_units);
   return cudaGetLastError();
 }
 
-cudaError_t launch_predict_fast(const PredictArgs& a, cudaStream_t st) {
+cudaError_t prepare_predict_fast(const PredictArgs& a, FastLaunch* fl) {
+  if (fl->known == a.known && fl->G == a.G && fl->accum == a.accum) return cudaSuccess;
   EncodeTiledFn enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
-  CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)a.K};
   const cuuint64_t strides[2] = {(cuuint64_t)a.W * 4, (cuuint64_t)a.P * 4};
   const cuuint32_t box[3] = {FT_SX, FT_SY, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)a.known, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(fl->tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                   (void*)a.known, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  cudaError_t e = cudaErrorNotSupported;
   const bool f32 = a.accum == 1;
   switch (a.G) {
-#define VK_CASE(g)                                                                      \
-  case g:                                                                               \
-    return f32 ? launch_fast_t<g, float>(map, a, st) : launch_fast_t<g, double>(map, a, st);
+#define VK_CASE(g) \
+  case g: e = f32 ? occupancy_t<g, float>(&fl->occ) : occupancy_t<g, double>(&fl->occ); break;
+    VK_CASE(1) VK_CASE(2) VK_CASE(3) VK_CASE(4) VK_CASE(5) VK_CASE(6) VK_CASE(7) VK_CASE(8)
+#undef VK_CASE
+    default: break;
+  }
+  if (e != cudaSuccess) return e;
+  fl->known = a.known;
+  fl->G = a.G;
+  fl->accum = a.accum;
+  return cudaSuccess;
+}
+
+cudaError_t launch_predict_fast_prepared(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
+  const bool f32 = a.accum == 1;
+  switch (a.G) {
+#define VK_CASE(g) \
+  case g: return f32 ? launch_fast_t<g, float>(fl, a, st) : launch_fast_t<g, double>(fl, a, st);
     VK_CASE(1) VK_CASE(2) VK_CASE(3) VK_CASE(4) VK_CASE(5) VK_CASE(6) VK_CASE(7) VK_CASE(8)
 #undef VK_CASE
     default:
       return cudaErrorNotSupported;
   }
+}
+
+cudaError_t launch_predict_fast(const PredictArgs& a, cudaStream_t st) {
+  FastLaunch fl;
+  cudaError_t e = prepare_predict_fast(a, &fl);
+  if (e != cudaSuccess) return e;
+  return launch_predict_fast_prepared(fl, a, st);
 }
 
 }  // namespace vk

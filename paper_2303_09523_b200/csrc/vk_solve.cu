@@ -1,4 +1,4 @@
-// Batched universal-kriging stencil solves: one CTA per (sub-part, stencil).
+// Batched universal-kriging stencil solves: one warp per (sub-part, stencil).
 //
 // Restates build_system + solve_ked (kriging.py:159-245) for the stencil
 // families of the plane-structured fill (kriging.py:516-557): the extended
@@ -12,17 +12,22 @@
 // Drift columns kept by _independent_columns (kriging.py:145-156) are decided
 // exactly on the host (integer offsets) and passed as a bitmask.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include "vk_kernels.h"
 
 namespace vk {
 
 namespace {
 
-constexpr int SOLVE_THREADS = 128;
+constexpr int SOLVE_WARPS_MAX = 4;
 
-__global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs a) {
+// One warp per system; `ws` systems per CTA, each with its own shared-memory
+// slice [A | b] (N x (N+1)), solution and relative offsets.
+__global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a, int ws, size_t slice) {
   extern __shared__ double sm[];
-  const int sys = blockIdx.x, tid = threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sys = a.sys0 + blockIdx.x * ws + wid;
+  if (wid >= ws || sys >= a.sys0 + a.n_sys) return;
   const int s = a.sys_part[sys], stc = a.sys_stencil[sys];
   const int n = a.st_n[stc], off = a.st_off[stc], dcols = a.st_drift[stc];
   const int pat = a.st_pattern[stc];
@@ -35,148 +40,147 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs a) {
   for (int c = 0; c < 4; ++c)
     if (dcols & (1 << c)) cols[pq++] = c;
   const int N = n + pq, ld = N + 1;
-  double* A = sm;                                  // [N][ld]
-  double* xsol = sm + (size_t)N * ld;              // [N]
-  int* rel = (int*)(xsol + N);                     // [n][3]
-  __shared__ int s_piv, s_fail, s_done;
-  __shared__ double s_red[SOLVE_THREADS / 32];
-  __shared__ int s_redi[SOLVE_THREADS / 32];
-  for (int i = tid; i < n; i += SOLVE_THREADS) {
+  double* A = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + (size_t)wid * slice);
+  double* xsol = A + (size_t)N * ld;
+  int* rel = reinterpret_cast<int*>(xsol + N);
+  for (int i = lane; i < n; i += 32) {
     const int pl = a.taps[3 * (off + i) + 2];
     rel[3 * i + 0] = a.taps[3 * (off + i) + 0];
     rel[3 * i + 1] = a.taps[3 * (off + i) + 1];
     rel[3 * i + 2] = a.pat_dz[pat * NPMAX + pl];
   }
-  if (tid == 0) { s_fail = 0; s_done = 0; }
-  __syncthreads();
-  const double cov0 = covariance(a.kind, mdl, 0.0);
+  // covariance by integer squared lag: every lag in the system is
+  // sqrt(dx^2 + dy^2 + dz^2) of small integers, so the distinct values are
+  // tabulated once (kriging.py:185-188 evaluates C element by element)
+  int maxdz = 0;
+  for (int p1 = 0; p1 < NPMAX; ++p1) {
+    const int z1 = a.pat_dz[pat * NPMAX + p1];
+    maxdz = max(maxdz, abs(z1));
+    for (int p2 = 0; p2 < NPMAX; ++p2) maxdz = max(maxdz, abs(z1 - a.pat_dz[pat * NPMAX + p2]));
+  }
+  const int maxd2 = 18 + maxdz * maxdz;
+  double* ctab = reinterpret_cast<double*>(reinterpret_cast<char*>(rel) +
+                                           ((3 * a.max_n * sizeof(int) + 7) & ~(size_t)7));   // [maxd2 + 1]
+  for (int d2 = lane; d2 <= maxd2; d2 += 32) ctab[d2] = covariance(a.kind, mdl, sqrt((double)d2));
+  __syncwarp();
+  const double cov0 = ctab[0];
   double trace = 0.0;
-  for (int i = 0; i < n; ++i) trace += cov0;     // np.trace of C: sum of C(0)
+  for (int i = 0; i < n; ++i) trace += cov0;     // np.trace of C
   const double ridge = fmax(1e-10 * trace / n, 1e-12);
-
-  int status = PS_SINGULAR;
-  for (int attempt = 0; attempt < 2 && !s_done; ++attempt) {
-    // ---- assemble [A | b]
-    for (int idx = tid; idx < N * ld; idx += SOLVE_THREADS) {
-      const int i = idx / ld, j = idx - i * ld;
-      double v;
-      if (j == N) {                                // rhs
-        if (i < n) {
-          const int dx = rel[3 * i], dy = rel[3 * i + 1], dz = rel[3 * i + 2];
-          v = covariance(a.kind, mdl, sqrt((double)(dx * dx + dy * dy + dz * dz)));
+  bool done = false;
+  for (int attempt = 0; attempt < 2 && !done; ++attempt) {
+    // ---- assemble [A | b]: rows of [C Q | c0] then [Q^T 0 | q0]
+    for (int i = 0; i < n; ++i) {
+      const int xi = rel[3 * i], yi = rel[3 * i + 1], zi = rel[3 * i + 2];
+      for (int j = lane; j < ld; j += 32) {
+        double v;
+        if (j < n) {
+          const int dx = xi - rel[3 * j], dy = yi - rel[3 * j + 1], dz = zi - rel[3 * j + 2];
+          v = ctab[dx * dx + dy * dy + dz * dz];
+          if (attempt == 1 && i == j) v += ridge;
+        } else if (j < N) {
+          const int c = cols[j - n];
+          v = (c == 0) ? 1.0 : (double)rel[3 * i + c - 1];
         } else {
-          v = (cols[i - n] == 0) ? 1.0 : 0.0;      // q0 = drift at the target
+          v = ctab[xi * xi + yi * yi + zi * zi];   // c0
         }
-      } else if (i < n && j < n) {
-        const int dx = rel[3 * i] - rel[3 * j], dy = rel[3 * i + 1] - rel[3 * j + 1],
-                  dz = rel[3 * i + 2] - rel[3 * j + 2];
-        v = covariance(a.kind, mdl, sqrt((double)(dx * dx + dy * dy + dz * dz)));
-        if (attempt == 1 && i == j) v += ridge;
-      } else if (i < n) {
-        const int c = cols[j - n];
-        v = (c == 0) ? 1.0 : (double)rel[3 * i + c - 1];
-      } else if (j < n) {
-        const int c = cols[i - n];
-        v = (c == 0) ? 1.0 : (double)rel[3 * j + c - 1];
-      } else {
-        v = 0.0;
+        A[i * ld + j] = v;
       }
-      A[i * ld + j] = v;
     }
-    if (tid == 0) s_fail = 0;
-    __syncthreads();
-    // ---- LU with partial pivoting, rhs carried as column N
+    for (int i = n; i < N; ++i) {
+      const int c = cols[i - n];
+      for (int j = lane; j < ld; j += 32) {
+        double v;
+        if (j < n) v = (c == 0) ? 1.0 : (double)rel[3 * j + c - 1];
+        else if (j < N) v = 0.0;
+        else v = (c == 0) ? 1.0 : 0.0;             // q0 = drift at the target
+        A[i * ld + j] = v;
+      }
+    }
+    __syncwarp();
+    // ---- LU with partial pivoting (first maximal |pivot|, as idamax), rhs
+    // carried as column N
+    bool fail = false;
     for (int k = 0; k < N; ++k) {
-      if (tid < 32) {
-        double best = -1.0;
-        int bi = N;
-        for (int r = k + tid; r < N; r += 32) {
-          const double v = fabs(A[r * ld + k]);
-          if (v > best) { best = v; bi = r; }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_down_sync(0xffffffffu, best, o);
-          const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-        }
-        if (tid == 0) {
-          s_piv = bi;
-          if (!(best > 0.0)) s_fail = 1;           // exact zero pivot: dgesv info > 0
-        }
+      double best = -1.0;
+      int bi = N;
+      for (int r = k + lane; r < N; r += 32) {
+        const double v = fabs(A[r * ld + k]);
+        if (v > best) { best = v; bi = r; }
       }
-      __syncthreads();
-      if (s_fail) break;
-      const int piv = s_piv;
-      if (piv != k)
-        for (int j = tid; j < ld; j += SOLVE_THREADS) {
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (!(best > 0.0)) { fail = true; break; }   // exact zero pivot: dgesv info > 0
+      if (bi != k) {
+        for (int j = lane; j < ld; j += 32) {
           const double t = A[k * ld + j];
-          A[k * ld + j] = A[piv * ld + j];
-          A[piv * ld + j] = t;
+          A[k * ld + j] = A[bi * ld + j];
+          A[bi * ld + j] = t;
         }
-      __syncthreads();
-      const double inv = 1.0 / A[k * ld + k];
-      for (int r = k + 1 + tid; r < N; r += SOLVE_THREADS) A[r * ld + k] *= inv;
-      __syncthreads();
-      const int rows = N - k - 1, colsn = ld - k - 1;
-      for (int idx = tid; idx < rows * colsn; idx += SOLVE_THREADS) {
-        const int r = k + 1 + idx / colsn, j = k + 1 + idx % colsn;
-        A[r * ld + j] -= A[r * ld + k] * A[k * ld + j];
+        __syncwarp();
       }
-      __syncthreads();
+      const double inv = 1.0 / A[k * ld + k];
+      for (int r = k + 1 + lane; r < N; r += 32) A[r * ld + k] *= inv;
+      __syncwarp();
+      const int colsn = ld - k - 1;
+      for (int j = lane; j < colsn; j += 32) {
+        const double ukj = A[k * ld + k + 1 + j];
+        for (int r = k + 1; r < N; ++r) A[r * ld + k + 1 + j] -= A[r * ld + k] * ukj;
+      }
+      __syncwarp();
     }
-    if (tid == 0 && !s_fail) {
-      // back substitution U x = y
+    if (!fail) {
+      // back substitution U x = y, rows from the bottom (lane-parallel dots)
       bool finite = true;
       for (int i = N - 1; i >= 0; --i) {
-        double acc = A[i * ld + N];
-        for (int j = i + 1; j < N; ++j) acc -= A[i * ld + j] * xsol[j];
-        xsol[i] = acc / A[i * ld + i];
-        finite = finite && (xsol[i] - xsol[i] == 0.0);
+        double part = 0.0;
+        for (int j = i + 1 + lane; j < N; j += 32) part += A[i * ld + j] * xsol[j];
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        const double xi = (A[i * ld + N] - part) / A[i * ld + i];
+        if (lane == 0) xsol[i] = xi;
+        finite = finite && (xi - xi == 0.0);
+        __syncwarp();
       }
-      // unbiasedness residual max_c |sum_i Q_ic w_i - q0_c|
+      // unbiasedness residual max_c |sum_i Q_ic w_i - q0_c|  (kriging.py:223)
       double resid = 0.0;
       for (int c = 0; c < pq; ++c) {
-        double acc = 0.0;
-        for (int i = 0; i < n; ++i) {
+        double part = 0.0;
+        for (int i = lane; i < n; i += 32) {
           const double q = (cols[c] == 0) ? 1.0 : (double)rel[3 * i + cols[c] - 1];
-          acc += q * xsol[i];
+          part += q * xsol[i];
         }
-        resid = fmax(resid, fabs(acc - ((cols[c] == 0) ? 1.0 : 0.0)));
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        resid = fmax(resid, fabs(part - ((cols[c] == 0) ? 1.0 : 0.0)));
       }
-      if (!finite || !(resid <= 1e-8)) s_fail = 1;
-      else s_done = 1;
+      done = finite && (resid <= 1e-8);
     }
-    __syncthreads();
   }
-  if (s_done) status = PS_OK;
   // ---- outputs
   const int64_t slot = ((int64_t)s * a.NP + pat) * a.NK + kind_idx;
   double* w = a.weights + slot * WPAD;
-  for (int i = tid; i < WPAD; i += SOLVE_THREADS) w[i] = 0.0;
-  __syncthreads();
-  if (status == PS_OK) {
-    for (int i = tid; i < n; i += SOLVE_THREADS) w[a.pad[off + i]] = xsol[i];
+  for (int i = lane; i < WPAD; i += 32) w[i] = 0.0;
+  __syncwarp();
+  if (done) {
+    for (int i = lane; i < n; i += 32) w[a.pad[off + i]] = xsol[i];
     // variance = C(0) - w.c0 - lambda.q0  (kriging.py:239-244)
     double part = 0.0;
-    for (int i = tid; i < n; i += SOLVE_THREADS) {
+    for (int i = lane; i < n; i += 32) {
       const int dx = rel[3 * i], dy = rel[3 * i + 1], dz = rel[3 * i + 2];
-      part += xsol[i] * covariance(a.kind, mdl, sqrt((double)(dx * dx + dy * dy + dz * dz)));
+      part += xsol[i] * ctab[dx * dx + dy * dy + dz * dz];
     }
-    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
-    if ((tid & 31) == 0) s_red[tid >> 5] = part;
-    __syncthreads();
-    if (tid == 0) {
-      double wc = 0.0;
-      for (int i = 0; i < SOLVE_THREADS / 32; ++i) wc += s_red[i];
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) {
       double lq = 0.0;
       for (int c = 0; c < pq; ++c) lq += xsol[n + c] * ((cols[c] == 0) ? 1.0 : 0.0);
-      a.var[slot] = cov0 - wc - lq;
+      a.var[slot] = cov0 - part - lq;
     }
-  } else if (tid == 0) {
+  } else if (lane == 0) {
     a.var[slot] = 0.0;
   }
-  if (tid == 0) a.sys_status[sys] = status;
-  (void)s_redi;
+  if (lane == 0) a.sys_status[sys] = done ? PS_OK : PS_SINGULAR;
 }
 
 }  // namespace
@@ -184,14 +188,16 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs a) {
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
   if (a.n_sys == 0) return cudaSuccess;
   const int N = a.max_n + 4;
-  const size_t smem = (size_t)N * (N + 1) * sizeof(double) + N * sizeof(double) +
-                      (size_t)a.max_n * 3 * sizeof(int) + 16;
+  const int maxd2 = 18 + a.max_dz * a.max_dz;
+  const size_t slice = (((size_t)N * (N + 1) + N) * sizeof(double) + (size_t)a.max_n * 3 * sizeof(int) +
+                        (size_t)(maxd2 + 3) * sizeof(double) + 127) / 128 * 128;
+  int ws = (int)std::max<size_t>(1, std::min<size_t>(SOLVE_WARPS_MAX, (size_t)(96 * 1024) / slice));
+  const size_t smem = slice * ws;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  solve_kernel<<<a.n_sys, SOLVE_THREADS, smem, st>>>(a);
+  solve_kernel<<<(a.n_sys + ws - 1) / ws, 32 * ws, smem, st>>>(a, ws, slice);
   return cudaGetLastError();
 }
 

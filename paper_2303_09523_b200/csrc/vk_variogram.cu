@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(PT_BLOCK) pair_bin_kernel(int64_t npairs, int 
       const double lag = sample_lag(geom, i, j);
       if (lag > 0.0) {
         int c = 0;                                 // digitize: #edges <= lag
-        for (int e = 0; e < n_bins; ++e) c += ((double)e * step <= lag);
+        for (int e = 0; e < n_bins; ++e) c += (__dmul_rn((double)e, step) <= lag);
         c += (hmax <= lag);
         c = min(max(c - 1, 0), n_bins - 1);
         b = (uint8_t)c;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   // One warp per sub-part.  Statistics are merged redundantly by every lane
   // (same order -> same bits); bins are reduced lane-per-bin; the TRF runs
   // warp-parallel (lane = residual row) when n_bins + 3 <= 32.
-  const int s = blockIdx.x, lane = threadIdx.x;
+  const int s = a.part0 + blockIdx.x, lane = threadIdx.x;
   __shared__ TrfProblem P;
   double n = 0.0, mean = 0.0, m2 = 0.0, mn = DBL_MAX, mx = -DBL_MAX, bad = 0.0;
   const int kb = a.part_b ? a.part_b[s] : 0, ke = a.part_e ? a.part_e[s] : 0;
@@ -326,9 +326,10 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
     double sum = 0.0;
     for (int blk = 0; blk < a.nblk; ++blk) sum += a.partial[((int64_t)s * a.nblk + blk) * a.n_bins + lane];
     const int r = __popc(nzmask & ((1u << lane) - 1u));
-    const double e0 = (double)lane * step;
-    const double e1 = (lane + 1 == a.n_bins) ? hmax : (double)(lane + 1) * step;
-    P.h[r] = 0.5 * (e0 + e1);
+    // 0.5 * (edges[:-1] + edges[1:]) without contraction (numpy rounding)
+    const double e0 = __dmul_rn((double)lane, step);
+    const double e1 = (lane + 1 == a.n_bins) ? hmax : __dmul_rn((double)(lane + 1), step);
+    P.h[r] = __dmul_rn(0.5, __dadd_rn(e0, e1));
     P.gemp[r] = sum / (double)cnt;
     P.w[r] = sqrt((double)cnt);
   }
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
 // Scalar TRF (trf.h) for parts whose non-empty bins exceed 29 (n_bins > 29);
 // re-derives the problem exactly as fit_kernel does.
 __global__ void __launch_bounds__(32) fit_scalar_kernel(FitArgs a) {
-  const int s = blockIdx.x;
+  const int s = a.part0 + blockIdx.x;
   if (threadIdx.x != 0 || a.status[s] != PS_NEED_SCALAR_FIT) return;
   double n = 0.0, mean = 0.0, m2 = 0.0;
   for (int k = a.part_b[s]; k <= a.part_e[s]; ++k)
@@ -380,9 +381,9 @@ __global__ void __launch_bounds__(32) fit_scalar_kernel(FitArgs a) {
     if (cnt <= 0) continue;
     double sum = 0.0;
     for (int blk = 0; blk < a.nblk; ++blk) sum += a.partial[((int64_t)s * a.nblk + blk) * a.n_bins + b];
-    const double e0 = (double)b * step;
-    const double e1 = (b + 1 == a.n_bins) ? hmax : (double)(b + 1) * step;
-    P.h[P.nb] = 0.5 * (e0 + e1);
+    const double e0 = __dmul_rn((double)b, step);
+    const double e1 = (b + 1 == a.n_bins) ? hmax : __dmul_rn((double)(b + 1), step);
+    P.h[P.nb] = __dmul_rn(0.5, __dadd_rn(e0, e1));
     P.gemp[P.nb] = sum / (double)cnt;
     P.w[P.nb] = sqrt((double)cnt);
     P.nb++;
@@ -474,8 +475,9 @@ cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_fit(const FitArgs& a, cudaStream_t st) {
-  fit_kernel<<<a.S, 32, 0, st>>>(a);
-  if (a.fit && a.n_bins + 3 > 32) fit_scalar_kernel<<<a.S, 32, 0, st>>>(a);
+  if (a.n_parts <= 0) return cudaSuccess;
+  fit_kernel<<<a.n_parts, 32, 0, st>>>(a);
+  if (a.fit && a.n_bins + 3 > 32) fit_scalar_kernel<<<a.n_parts, 32, 0, st>>>(a);
   return cudaGetLastError();
 }
 

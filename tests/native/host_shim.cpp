@@ -5,6 +5,8 @@
 #include <vector>
 #include "pcg64.h"
 #include "trf.h"
+#include <cstdio>
+#include <string>
 
 using namespace vk;
 
@@ -47,6 +49,50 @@ int vkh_trf(int kind, int nb, const double* h, const double* gemp, const double*
   for (int i = 0; i < 3; ++i) x_out[i] = r.x[i];
   info[0] = r.status; info[1] = r.nfev; info[2] = r.iterations;
   return r.status;
+}
+
+}
+
+// ---- geometry (vk_geometry.cpp compiled into this test shim) --------------
+#include "vk_geometry.h"
+
+extern "C" {
+
+// Returns 0 on success, 1 on error (message copied to err).  Outputs:
+// info[0..5] = n_miss, n_patterns, n_stencils, fast, G, n_systems
+// miss_z[n_miss], miss_planes[n_miss*8], pat_off[n_patterns*8] (pad 99),
+// pat_n[n_patterns], st[n_stencils*5] = (pattern, ky, kx, n, drift_cols)
+int vkh_geometry(int H, int W, int T, const int* known_z, int K, int S, int drift,
+                 int32_t* info, int32_t* miss_z, int32_t* miss_planes, int32_t* pat_off,
+                 int32_t* pat_n, int32_t* st, char* err, int errlen) {
+  vk::Geometry g;
+  std::string e = vk::build_geometry(H, W, T, known_z, K, S, 0, drift, &g);
+  if (!e.empty()) {
+    snprintf(err, errlen, "%s", e.c_str());
+    return 1;
+  }
+  info[0] = (int)g.miss_z.size();
+  info[1] = (int)g.patterns.size();
+  info[2] = (int)g.stencils.size();
+  info[3] = g.fast ? 1 : 0;
+  info[4] = g.G;
+  info[5] = (int)g.sys_part.size();
+  for (size_t i = 0; i < g.miss_z.size(); ++i) {
+    miss_z[i] = g.miss_z[i];
+    for (int k = 0; k < vk::NPMAX; ++k) miss_planes[i * 8 + k] = g.miss_planes[i * vk::NPMAX + k];
+  }
+  for (size_t p = 0; p < g.patterns.size(); ++p) {
+    pat_n[p] = (int)g.patterns[p].size();
+    for (int k = 0; k < 8; ++k) pat_off[p * 8 + k] = k < (int)g.patterns[p].size() ? g.patterns[p][k] : 99;
+  }
+  for (size_t i = 0; i < g.stencils.size(); ++i) {
+    st[i * 5 + 0] = g.stencils[i].pattern;
+    st[i * 5 + 1] = g.stencils[i].ky;
+    st[i * 5 + 2] = g.stencils[i].kx;
+    st[i * 5 + 3] = g.stencils[i].n;
+    st[i * 5 + 4] = g.stencils[i].drift_cols;
+  }
+  return 0;
 }
 
 }

@@ -1,0 +1,155 @@
+"""GPU: the CUDA path (through the C ABI) against the golden vectors of the
+live reference.  fp64 tolerance 1e-6 of the known intensity range (BASELINE
+north_star); known planes bit-exact; integer-valued voxels within +-1 after
+rint; pair draws bit-exact."""
+
+import ctypes as C
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
+META = json.load(open(os.path.join(HERE, "golden", "reference_golden.json")))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+from make_golden import smooth_grid  # noqa: E402
+
+TOL64 = 1e-6
+FIT_FUZZ = 5e-5     # see test_gpu_parity.py / DESIGN.md "Fit parity"
+
+
+def _inputs(c):
+    data, mask = smooth_grid(c["seed"], *c["shape"], c["known_z"], quant=c["quant"])
+    if not c["quant"]:
+        data = np.where(mask, np.nan, data / 220.0).astype(np.float32)
+    return data, mask
+
+
+@pytest.mark.parametrize("case", META["fill"], ids=lambda c: c["name"])
+def test_fill_missing_vs_reference(cuda, case):
+    from paper_2303_09523_b200 import VariogramModel, VolumeGrid, fill_missing
+    data, mask = _inputs(case)
+    m = VariogramModel(case["kind"], *case["model"])
+    res = fill_missing(VolumeGrid(data, mask), m, case["drift"], return_variance=case["variance"])
+    grid, var = res if case["variance"] else (res, None)
+    gold = GOLD[f"fill_{case['name']}_out"]
+    rng = float(np.nanmax(data) - np.nanmin(data))
+    assert np.array_equal(grid.data[~mask], data[~mask])
+    assert not grid.missing_mask.any()
+    assert np.abs(grid.data.astype(np.float64) - gold).max() <= TOL64 * rng
+    if case["quant"]:
+        assert np.abs(np.rint(grid.data) - np.rint(gold)).max() <= 1
+    if var is not None:
+        gv = GOLD[f"fill_{case['name']}_var"]
+        assert np.allclose(var, gv, rtol=1e-7, atol=1e-9 * max(1.0, case["model"][1]))
+
+
+def test_pairs_vs_numpy(cuda):
+    torch = cuda
+    from paper_2303_09523_b200 import _lib
+    lib = _lib.load()
+    draws = [m for m in META["fit"] if m["key"] == "pairs"][0]["draws"]
+    for m, h in draws.items():
+        m = int(m)
+        ii = torch.empty(100_000, dtype=torch.int32, device="cuda")
+        jj = torch.empty_like(ii)
+        n = C.c_int64()
+        assert lib.vk_sample_pairs(m, 100_000, 0, ii.data_ptr(), jj.data_ptr(), C.byref(n),
+                                   torch.cuda.current_stream().cuda_stream) == 0
+        if m * (m - 1) // 2 <= 100_000:
+            continue
+        a, b = ii.cpu().numpy(), jj.cpu().numpy()
+        assert np.array_equal(a[:1000], GOLD[f"pairs_{m}_ii_head"])
+        assert hashlib.sha256(a.tobytes()).hexdigest() == h["ii_sha256"]
+        assert hashlib.sha256(b.tobytes()).hexdigest() == h["jj_sha256"]
+
+
+def test_fit_variogram_vs_reference(cuda):
+    from paper_2303_09523_b200 import fit_variogram
+    for m in META["fit"]:
+        if m["key"] == "pairs":
+            continue
+        c = GOLD[m["key"] + "_coords"]
+        v = GOLD[m["key"] + "_values"]
+        got = fit_variogram((c, v), kind=m["kind"])
+        nug, sill, rng = m["model"]
+        # parameters within the TRF termination fuzz
+        assert abs(got.sill - sill) <= 5e-3 * sill, (m["key"], got, m["model"])
+
+
+@pytest.mark.parametrize("case", META["pipeline"], ids=lambda c: c["name"])
+def test_pipeline_vs_reference(cuda, case):
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    ks = GOLD[f"pipe_{case['name']}_known"]
+    gold = GOLD[f"pipe_{case['name']}_out"]
+    K, H, W = ks.shape
+    rng = float(ks.max() - ks.min())
+    kd = torch.from_numpy(np.ascontiguousarray(ks)).cuda()
+    # kriging with the reference's own fitted models: strict fp64 tolerance
+    zf = ZPartKriging(K, H, W, case["factor"], case["n_subparts"], fit=False)
+    out, _ = zf.run(kd, models=[VariogramModel("exponential", *m) for m in case["models"]])
+    zf.finish()
+    got = out.cpu().numpy()
+    assert np.array_equal(got[::case["factor"]], ks)
+    assert np.abs(got.astype(np.float64) - gold).max() <= TOL64 * rng
+    assert np.abs(np.rint(got) - np.rint(gold)).max() <= 1
+    # end to end with the device fit
+    zk = ZPartKriging(K, H, W, case["factor"], case["n_subparts"])
+    out2, _ = zk.run(kd)
+    zk.finish()
+    assert np.abs(out2.cpu().numpy().astype(np.float64) - gold).max() <= FIT_FUZZ * rng
+
+
+def test_spec_kats_on_device(cuda):
+    from paper_2303_09523_b200 import VariogramModel, VolumeGrid, fill_missing
+    T, H, W = 9, 12, 14
+    z, y, x = np.meshgrid(np.arange(T), np.arange(H), np.arange(W), indexing="ij")
+    field = (2 * x + 3 * y + z).astype(np.float32)
+    data = field.copy()
+    data[1::2] = np.nan
+    g = fill_missing(VolumeGrid(data), VariogramModel("exponential", 0, 1, 5), "linear")
+    assert np.abs(g.data - field).max() <= 1e-5
+    data = np.full((11, 8, 9), np.nan, np.float32)
+    data[::5] = 0.75
+    g = fill_missing(VolumeGrid(data), VariogramModel("exponential", 0, 1, 5), "linear")
+    assert np.abs(g.data - 0.75).max() <= 1e-6
+    data = np.full((9, 8, 9), np.nan, np.float32)
+    for i in range(0, 9, 4):
+        data[i] = i / 8.0
+    g = fill_missing(VolumeGrid(data), VariogramModel("exponential", 0, 1, 5), "linear")
+    ramp = (np.arange(9) / 8.0)[:, None, None]
+    assert np.abs(g.data - ramp).max() <= 1e-5
+
+
+def test_error_contract_on_device(cuda):
+    from paper_2303_09523_b200 import (DegenerateLags, InsufficientSamples, NoKnownNeighbors,
+                                       VariogramModel, VolumeGrid, fill_missing, fit_variogram)
+    e = META["errors"]
+    with pytest.raises(InsufficientSamples):
+        fit_variogram((np.zeros((7, 3)), np.arange(7.0)))
+    with pytest.raises(DegenerateLags):
+        fit_variogram((np.zeros((20, 3)), np.arange(20.0)))
+    with pytest.raises(NoKnownNeighbors):
+        fill_missing(VolumeGrid(np.full((3, 4, 4), np.nan, np.float32)),
+                     VariogramModel("exponential", 0, 1, 1))
+    d2 = np.zeros((3, 4, 4), np.float32)
+    m2 = np.zeros((3, 4, 4), bool)
+    m2[1] = True
+    with pytest.raises(ValueError):
+        fill_missing(VolumeGrid(d2, m2), VariogramModel("exponential", 0, 1, 1))
+    d3 = np.full((3, 4, 4), np.nan, np.float32)
+    d3[0] = 1.0
+    d3[2] = np.inf
+    with pytest.raises(ValueError):
+        fill_missing(VolumeGrid(d3, np.isnan(d3)), VariogramModel("exponential", 0, 1, 1))
+    dense = np.ones((2, 3, 3), np.float32)
+    out = fill_missing(VolumeGrid(dense), VariogramModel("exponential", 0, 1, 1))
+    assert np.array_equal(out.data, dense)
+    assert e["dense_grid"] is None
