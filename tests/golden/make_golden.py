@@ -29,6 +29,8 @@ from volkrig import kriging as K         # noqa: E402
 from volkrig import model as M           # noqa: E402
 
 from paper_2303_09523_b200.phantoms import known_slices, small_config  # noqa: E402
+sys.path.insert(0, HERE)
+from golden_inputs import smooth_grid  # noqa: E402
 
 
 def _env():
@@ -36,20 +38,6 @@ def _env():
     blas = npc.CONFIG.get("Build Dependencies", {}).get("blas", {})
     return {"numpy": np.__version__, "scipy": scipy.__version__,
             "blas": f"{blas.get('name')} {blas.get('version')}"}
-
-
-def smooth_grid(seed, T, H, W, known_z, quant=True):
-    """Seeded smooth random volume with NaN planes except known_z."""
-    r = np.random.default_rng(seed)
-    base = r.normal(size=(T, H, W)).cumsum(1).cumsum(2)
-    base = (base - base.min()) / (base.max() - base.min()) * 200 + 20
-    if quant:
-        base = np.rint(base)
-    data = base.astype(np.float32)
-    mask = np.ones(data.shape, bool)
-    mask[list(known_z)] = False
-    data[mask] = np.nan
-    return data, mask
 
 
 FILL_CASES = [

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
 META = json.load(open(os.path.join(HERE, "golden", "reference_golden.json")))
 sys.path.insert(0, os.path.join(HERE, "golden"))
-from make_golden import smooth_grid  # noqa: E402
+from golden_inputs import smooth_grid  # noqa: E402
 
 TOL64 = 1e-6
 FIT_FUZZ = 5e-5     # see test_gpu_parity.py / DESIGN.md "Fit parity"

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
 META = json.load(open(os.path.join(HERE, "golden", "reference_golden.json")))
 sys.path.insert(0, os.path.join(HERE, "golden"))
-from make_golden import smooth_grid  # noqa: E402  (input regeneration only)
+from golden_inputs import smooth_grid  # noqa: E402  (input regeneration only)
 
 REF = "/root/reference/pkg/src"
 
