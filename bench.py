@@ -229,7 +229,7 @@ def run_gpu(args, cfg, ks):
     K_loc = cfg.n_known + int(has_halo)
     H, W, f = cfg.height, cfg.width, cfg.factor
     zk = ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, redraw_pairs=True,
-                      part_len=cfg.n_known // cfg.n_subparts)
+                      part_len=cfg.n_known // cfg.n_subparts, overlap=args.overlap)
     zk.plan.set_timing(max(1, args.steps))
     zs = zk                                  # serial schedule: per-stage events
     stack = torch.empty((K_loc, H, W), dtype=torch.float32, device=dev)
@@ -386,6 +386,8 @@ def main(argv=None):
     ap.add_argument("--variance", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--overlap", action="store_true",
+                    help="per-part fit->solve->predict chains on side streams")
     args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
 

@@ -152,9 +152,9 @@ VK_HD void lsq_trust_region(int m, const double* uf, const double* s, const doub
   auto phi_d = [&](double a, double& phi, double& dphi) {
     double q[3], s3 = 0.0;
     for (int i = 0; i < 3; ++i) {
-      const double den = s[i] * s[i] + a;
-      q[i] = suf[i] / den;
-      s3 += suf[i] * suf[i] / (den * den * den);
+      const double rden = 1.0 / (s[i] * s[i] + a);
+      q[i] = suf[i] * rden;
+      s3 += q[i] * q[i] * rden;                 // suf^2 / den^3
     }
     const double pn = vnorm(q, 3);
     phi = pn - Delta;

@@ -111,7 +111,7 @@ struct WarpTrf {
           rotated = true;
           const double zeta = (beta - alpha) / (2.0 * gamma);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+          const double c = rsqrt(1.0 + t * t), sn = c * t;
           for (int r = 0; r < 3; ++r) {
             const double rp = R[r * 3 + p], rq = R[r * 3 + q];
             R[r * 3 + p] = c * rp - sn * rq;

@@ -407,6 +407,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   fa.status = p->d_part_status;
   fa.part0 = 0;
   fa.n_parts = S;
+  fa.reserve_smem = 0;
   SolveArgs sa;
   sa.n_sys = p->n_sys;
   sa.sys0 = 0;
@@ -472,6 +473,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       FitArgs f1 = fa;
       f1.part0 = s;
       f1.n_parts = 1;
+      f1.reserve_smem = 160 * 1024;           // one fit per SM, no streaming CTA beside it
       VK_CUDA(launch_fit(f1, cs));
       SolveArgs s1 = sa;
       s1.sys0 = p->sys_begin[s];
@@ -724,6 +726,7 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   fa.status = status;
   fa.part0 = 0;
   fa.n_parts = 1;
+  fa.reserve_smem = 0;
   if (e == cudaSuccess) e = launch_fit(fa, st);
   double mo[3] = {0, 0, 0};
   int32_t s = 0;

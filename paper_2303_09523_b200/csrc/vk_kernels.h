@@ -55,6 +55,7 @@ cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st);
 struct FitArgs {
   int S, n_bins, nblk, kind, fit, nchunk;
   int part0, n_parts;       // parts [part0, part0 + n_parts) of this launch
+  int reserve_smem;         // dynamic smem to request (keeps co-resident CTAs off the SM)
   const ChunkStat* stats;   // [K][nchunk] (structured) or [1][nchunk] (explicit)
   const int32_t* part_b;    // [S]
   const int32_t* part_e;    // [S]

@@ -281,19 +281,40 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   // warp-parallel (lane = residual row) when n_bins + 3 <= 32.
   const int s = a.part0 + blockIdx.x, lane = threadIdx.x;
   __shared__ TrfProblem P;
+  // Chan merge of the part's chunk statistics: lanes merge strided chunks,
+  // then a butterfly merges lanes in a canonical (lower, upper) order so every
+  // lane ends with the same bits -- deterministic across runs.
   double n = 0.0, mean = 0.0, m2 = 0.0, mn = DBL_MAX, mx = -DBL_MAX, bad = 0.0;
   const int kb = a.part_b ? a.part_b[s] : 0, ke = a.part_e ? a.part_e[s] : 0;
-  for (int k = kb; k <= ke; ++k) {
-    for (int c = 0; c < a.nchunk; ++c) {
-      const ChunkStat cs = a.stats[(int64_t)k * a.nchunk + c];
-      bad += cs.bad;
-      if (cs.n <= 0) continue;
-      mn = fmin(mn, cs.mn);
-      mx = fmax(mx, cs.mx);
-      const double nn = n + cs.n, d = cs.mean - mean;
-      mean = mean + d * (cs.n / nn);
-      m2 = m2 + cs.m2 + d * d * (n * cs.n / nn);
-      n = nn;
+  const int n_items = (ke - kb + 1) * a.nchunk;
+  auto merge = [](double& na, double& ma, double& qa, double nb, double mb, double qb) {
+    if (nb <= 0) return;
+    if (na <= 0) { na = nb; ma = mb; qa = qb; return; }
+    const double nn = na + nb, d = mb - ma;
+    ma = ma + d * (nb / nn);
+    qa = qa + qb + d * d * (na * nb / nn);
+    na = nn;
+  };
+  for (int it = lane; it < n_items; it += 32) {
+    const ChunkStat cs = a.stats[(int64_t)kb * a.nchunk + it];
+    bad += cs.bad;
+    if (cs.n <= 0) continue;
+    mn = fmin(mn, cs.mn);
+    mx = fmax(mx, cs.mx);
+    merge(n, mean, m2, cs.n, cs.mean, cs.m2);
+  }
+  for (int o = 1; o < 32; o <<= 1) {
+    const double on = __shfl_xor_sync(0xffffffffu, n, o), om = __shfl_xor_sync(0xffffffffu, mean, o),
+                 oq = __shfl_xor_sync(0xffffffffu, m2, o);
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if (lane & o) {                       // (other, self): lower lane first
+      double nn = on, mm = om, qq = oq;
+      merge(nn, mm, qq, n, mean, m2);
+      n = nn; mean = mm; m2 = qq;
+    } else {
+      merge(n, mean, m2, on, om, oq);
     }
   }
   if (lane == 0) {
@@ -476,7 +497,16 @@ cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
 
 cudaError_t launch_fit(const FitArgs& a, cudaStream_t st) {
   if (a.n_parts <= 0) return cudaSuccess;
-  fit_kernel<<<a.n_parts, 32, 0, st>>>(a);
+  if (a.reserve_smem > 48 * 1024) {
+    static int set_to = 0;
+    if (set_to < a.reserve_smem) {
+      cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           a.reserve_smem);
+      if (e != cudaSuccess) return e;
+      set_to = a.reserve_smem;
+    }
+  }
+  fit_kernel<<<a.n_parts, 32, a.reserve_smem, st>>>(a);
   if (a.fit && a.n_bins + 3 > 32) fit_scalar_kernel<<<a.n_parts, 32, 0, st>>>(a);
   return cudaGetLastError();
 }
