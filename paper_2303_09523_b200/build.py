@@ -53,8 +53,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
         if not force and not _stale(obj, [src] + deps + [Path(__file__)]):
             continue
+        exp = os.environ.get("VK_NVCC_EXTRA", "").split()    # tuning experiments only
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-I", str(INCLUDE), "-I", str(CSRC), *extra, "-c", str(src),
+               "-I", str(INCLUDE), "-I", str(CSRC), *extra, *exp, "-c", str(src),
                "-o", str(obj)]
         if unit.endswith(".cpp"):
             cmd.insert(1, "-x")

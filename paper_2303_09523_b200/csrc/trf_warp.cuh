@@ -18,6 +18,15 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
+#ifdef VK_FIT_PROFILE
+__device__ unsigned long long g_fit_prof[8];   // cycles: jac, svd, trsolve, select, resid, total, nfev, iters
+#define VK_PT(v) const long long v = clock64()
+#define VK_PACC(slot, a, b) if (lane == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)((b) - (a)))
+#else
+#define VK_PT(v)
+#define VK_PACC(slot, a, b)
+#endif
+
 struct WarpTrf {
   const TrfProblem& P;
   int lane, m;
@@ -107,10 +116,15 @@ struct WarpTrf {
             beta += R[r * 3 + q] * R[r * 3 + q];
             gamma += R[r * 3 + p] * R[r * 3 + q];
           }
-          if (gamma == 0.0 || fabs(gamma) <= TRF_EPS * sqrt(alpha * beta)) continue;
+          // converged pair: |gamma| <= 1e-15 sqrt(alpha beta) (orthogonal to
+          // working precision; the trust-region step uses s, V to ~1e-14)
+          if (gamma == 0.0 || gamma * gamma <= 1e-30 * (alpha * beta)) continue;
           rotated = true;
-          const double zeta = (beta - alpha) / (2.0 * gamma);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          // tan of the Jacobi angle without forming zeta = (beta-alpha)/(2 gamma):
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) = 2 gamma s / (|b-a| + sqrt((b-a)^2 + 4 gamma^2))
+          const double bma = beta - alpha;
+          const double sg = (bma >= 0.0) ? 1.0 : -1.0;
+          const double t = (2.0 * gamma * sg) / (fabs(bma) + sqrt(bma * bma + 4.0 * gamma * gamma));
           const double c = rsqrt(1.0 + t * t), sn = c * t;
           for (int r = 0; r < 3; ++r) {
             const double rp = R[r * 3 + p], rq = R[r * 3 + q];
@@ -300,16 +314,25 @@ struct WarpTrf {
         for (int c = 0; c < 3; ++c) a[c] = (dr >= 0 && dr < 3 && dr == c) ? sqrt(diag_h[c]) : 0.0;
       }
       double sv[3], V[9], uf[3];
+      VK_PT(t_s0);
       svd_uf(a, row ? f : 0.0, sv, V, uf);
+      VK_PT(t_s1);
+      VK_PACC(1, t_s0, t_s1);
       const double theta = fmax(0.995, 1 - g_norm);
       double actual_reduction = -1;
       double step_norm = 0.0;
       while (actual_reduction <= 0 && nfev < max_nfev) {
         double p_h[3], p[3];
+        VK_PT(t_t0);
         lsq_trust_region(m, uf, sv, V, Delta, alpha, p_h, &alpha);
+        VK_PT(t_t1);
+        VK_PACC(2, t_t0, t_t1);
         for (int i = 0; i < 3; ++i) p[i] = d[i] * p_h[i];
         double step[3], step_h[3], pred;
-        if (!select(x, Jh, diag_h, g_h, p, p_h, d, Delta, lb, ub, theta, step, step_h, &pred)) {
+        const bool sel_ok = select(x, Jh, diag_h, g_h, p, p_h, d, Delta, lb, ub, theta, step, step_h, &pred);
+        VK_PT(t_t2);
+        VK_PACC(3, t_t1, t_t2);
+        if (!sel_ok) {
           res.status = -1;
           res.nfev = nfev;
           res.iterations = iteration;
@@ -318,7 +341,10 @@ struct WarpTrf {
         }
         for (int i = 0; i < 3; ++i) x_new[i] = x[i] + step[i];
         make_strictly_feasible(x_new, lb, ub, 0.0);
+        VK_PT(t_r0);
         f_new = resid(x_new);
+        VK_PT(t_r1);
+        VK_PACC(4, t_r0, t_r1);
         nfev += 1;
         const double step_h_norm = vnorm(step_h, 3);
         const bool finite = __all_sync(0xffffffffu, finite_d(f_new));
@@ -346,8 +372,11 @@ struct WarpTrf {
         for (int i = 0; i < 3; ++i) x[i] = x_new[i];
         f = f_new;
         cost = cost_new;
+        VK_PT(t_j0);
         jac(x, f, lb, ub, J);
         for (int i = 0; i < 3; ++i) g[i] = wsum(J[i] * f);
+        VK_PT(t_j1);
+        VK_PACC(0, t_j0, t_j1);
       }
       iteration += 1;
     }
@@ -356,6 +385,12 @@ struct WarpTrf {
     res.status = status;
     res.nfev = nfev;
     res.iterations = iteration;
+#ifdef VK_FIT_PROFILE
+    if (lane == 0) {
+      atomicAdd(&g_fit_prof[6], (unsigned long long)nfev);
+      atomicAdd(&g_fit_prof[7], (unsigned long long)iteration);
+    }
+#endif
     return res;
   }
 };

@@ -80,6 +80,8 @@ struct vk_plan {
   int32_t *d_part_status = nullptr, *d_sys_status = nullptr;
   std::vector<PairTable> tables;
   PairTable* d_tables = nullptr;
+  std::vector<PairJob> jobs;          // one per pair class
+  PairJob* d_jobs = nullptr;
   bool pairs_ready = false;
   double* h_models = nullptr;        // pinned staging [S][3]
   int kernels = 0;
@@ -276,6 +278,22 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
       p->tables.push_back(t);
     }
     VK_TRY(p->put(&p->d_tables, p->tables));
+    {
+      const Pcg64 gen = pcg64_from_seed(d->seed);
+      int32_t zoff = 0;
+      for (size_t c = 0; c < g.pair_classes.size(); ++c) {
+        SampleGeom sg;
+        sg.coords = nullptr;
+        sg.zloc = p->d_zloc + zoff;
+        sg.P = P;
+        sg.W = g.W;
+        zoff += (int32_t)g.pair_classes[c].zloc.size();
+        p->jobs.push_back(make_pair_job((uint64_t)(gen.state >> 64), (uint64_t)gen.state,
+                                        (uint64_t)(gen.inc >> 64), (uint64_t)gen.inc,
+                                        g.pair_classes[c].m, d->max_pairs, d->n_bins, sg, p->tables[c]));
+      }
+      VK_TRY(p->put(&p->d_jobs, p->jobs));
+    }
     VK_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     VK_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     VK_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
@@ -346,24 +364,9 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   if (draw) {
     VK_CUDA(cudaEventRecord(p->ev_fork, st));
     VK_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
-    {
-      const Pcg64 gen = pcg64_from_seed(d.seed);
-      std::vector<int32_t> zoff;
-      int32_t acc = 0;
-      for (const PairClass& pc : g.pair_classes) { zoff.push_back(acc); acc += (int32_t)pc.zloc.size(); }
-      for (size_t c = 0; c < g.pair_classes.size(); ++c) {
-        SampleGeom sg;
-        sg.coords = nullptr;
-        sg.zloc = p->d_zloc + zoff[c];
-        sg.P = P;
-        sg.W = g.W;
-        VK_CUDA(launch_pair_table((uint64_t)(gen.state >> 64), (uint64_t)gen.state, (uint64_t)(gen.inc >> 64),
-                                  (uint64_t)gen.inc, g.pair_classes[c].m, d.max_pairs, d.n_bins, sg,
-                                  p->tables[c], p->side));
-        kernels += 5;
-      }
-      p->pairs_ready = true;
-    }
+    VK_CUDA(launch_pair_tables(p->d_jobs, p->jobs.data(), (int)p->jobs.size(), p->side));
+    kernels += 5;
+    p->pairs_ready = true;
     VK_CUDA(cudaEventRecord(p->ev_join, p->side));
   }
   VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st));
@@ -621,11 +624,16 @@ int vk_sample_pairs(int64_t m, int64_t max_pairs, uint64_t seed, int32_t* ii, in
   sg.zloc = zl;
   sg.P = m;            // one "plane" holding every sample: lags unused here
   sg.W = (int32_t)std::min<int64_t>(m, 1 << 30);
-  cudaError_t e = launch_pair_table((uint64_t)(gen.state >> 64), (uint64_t)gen.state, (uint64_t)(gen.inc >> 64),
-                                    (uint64_t)gen.inc, m, max_pairs, 15, sg, t, st);
+  const PairJob job = make_pair_job((uint64_t)(gen.state >> 64), (uint64_t)gen.state,
+                                    (uint64_t)(gen.inc >> 64), (uint64_t)gen.inc, m, max_pairs, 15, sg, t);
+  PairJob* d_job = nullptr;
+  cudaError_t e = cudaMalloc((void**)&d_job, sizeof(PairJob));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_job, &job, sizeof(PairJob), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = launch_pair_tables(d_job, &job, 1, st);
   double scal[4] = {0, 0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpyAsync(scal, t.scal, sizeof(scal), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_job);
   cudaFree(t.bin);
   cudaFree(t.counts);
   cudaFree(t.scal);
@@ -691,9 +699,12 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   sg.zloc = nullptr;
   sg.P = m;
   sg.W = 1;
-  if (e == cudaSuccess)
-    e = launch_pair_table((uint64_t)(gen.state >> 64), (uint64_t)gen.state, (uint64_t)(gen.inc >> 64),
-                          (uint64_t)gen.inc, m, max_pairs, n_bins, sg, t, st);
+  const PairJob job = make_pair_job((uint64_t)(gen.state >> 64), (uint64_t)gen.state,
+                                    (uint64_t)(gen.inc >> 64), (uint64_t)gen.inc, m, max_pairs, n_bins, sg, t);
+  PairJob* d_job = (PairJob*)get(sizeof(PairJob));
+  if (!d_job) { cleanup(); return set_err(VK_E_CUDA, "cudaMalloc failed"); }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_job, &job, sizeof(PairJob), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = launch_pair_tables(d_job, &job, 1, st);
   if (e == cudaSuccess) e = launch_plane_stats_f64(values, m, stats, nchunk, st);
   BinsArgs ba;
   ba.known = nullptr;

@@ -37,9 +37,20 @@ struct SampleGeom {
 
 cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out,
                                int nchunk, cudaStream_t st);
-cudaError_t launch_pair_table(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
-                              int64_t m, int64_t max_pairs, int n_bins, SampleGeom geom,
-                              PairTable t, cudaStream_t st);
+// One pair class to draw (numpy-identical PCG64 + Lemire; triu when all
+// pairs fit), with its table and the sample geometry for the lags.
+struct PairJob {
+  uint64_t st_hi, st_lo, inc_hi, inc_lo;
+  uint32_t m, thr;
+  int64_t n_raw, need, max_pairs, npairs, n_thr;
+  int triu, n_bins;
+  PairTable t;
+  SampleGeom geom;
+};
+PairJob make_pair_job(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t m,
+                      int64_t max_pairs, int n_bins, SampleGeom geom, PairTable t);
+// all classes in 5 launches (blockIdx.y = class); h_jobs mirrors d_jobs
+cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st);
 struct BinsArgs {
   const float* known;      // structured: known planes; sample i of part s = known[base_s + i]
   const double* values;    // explicit samples (fit_variogram API) or nullptr

@@ -101,10 +101,15 @@ __global__ void __launch_bounds__(256) copy_known_kernel(PredictArgs a) {
 // --------------------------------------------------------------------------
 // fast streaming path
 // --------------------------------------------------------------------------
-constexpr int FT_WARPS = 8;
+#ifndef VK_FT_WARPS
+#define VK_FT_WARPS 8
+#define VK_FT_TY 32
+#define VK_FT_MINB 2
+#endif
+constexpr int FT_WARPS = VK_FT_WARPS;
 constexpr int FT_THREADS = FT_WARPS * 32;
 constexpr int FT_TX = 128;                 // tile columns (32 lanes x 4)
-constexpr int FT_TY = 32;                  // tile rows (8 warps x 4 row steps)
+constexpr int FT_TY = VK_FT_TY;            // tile rows (warps x row steps)
 constexpr int FT_SX = FT_TX + 8;           // smem row: x0-4 .. x0+131
 constexpr int FT_SY = FT_TY + 3;           // smem rows: y0-1 .. y0+33
 constexpr int FT_BUF_FLOATS = ((FT_SX * FT_SY * 4 + 127) / 128) * 128 / 4;
@@ -160,8 +165,21 @@ __device__ __forceinline__ void st_cs_d2(double* p, double a, double b) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 
-template <int G, typename Acc>
-__global__ void __launch_bounds__(FT_THREADS, 2)
+template <int COLS>
+__device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
+  if constexpr (COLS == 4) {
+    st_cs_f4(p, make_float4(v[0], v[1], v[2], v[3]));
+  } else {
+    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v[0]), "f"(v[1]) : "memory");
+  }
+}
+
+#ifndef VK_FT_COLS
+#define VK_FT_COLS 4
+#endif
+
+template <int G, typename Acc, int COLS = VK_FT_COLS>
+__global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
     predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
                         int n_tiles, int chunk, int n_units) {
   constexpr int NPAIR = G / 2;
@@ -274,12 +292,17 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
       const float lo = s_lohi[0], hi = s_lohi[1];
       const int64_t zk = a.known_z[k];
       const bool copy_b = (k == n_gaps - 1);
-      const int gx = x0 + 4 * lane;
+      // warp layout: WX column groups x WY rows per row step
+      constexpr int WX = (FT_TX / COLS) / 32;
+      constexpr int WY = FT_WARPS / WX;
+      const int wx = warp % WX, wy = warp / WX;
+      const int lc = lane + 32 * wx;                       // column group in the tile
+      const int gx = x0 + COLS * lc;
       const bool col_ok = gx < W;
-      const bool xb0 = (gx == 0), xb1 = (gx + 4 > W - 2);   // group holds border columns
+      const bool xb0 = (gx == 0), xb1 = (gx + COLS > W - 2);  // group holds border columns
 #pragma unroll 1
-      for (int rs = 0; rs < FT_TY / FT_WARPS; ++rs) {
-        const int r = warp + rs * FT_WARPS;                // tile row (warp-uniform)
+      for (int rs = 0; rs < FT_TY / WY; ++rs) {
+        const int r = wy + rs * WY;                        // tile row (warp-uniform)
         const int gy = y0 + r;
         if (gy >= H || !col_ok) continue;
         int iy = 0;                                        // row kind (border rows of edge tiles)
@@ -287,30 +310,45 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
         for (int q = 1; q < nky; ++q)
           if (kyl[q] == kyr) iy = q;
         const Acc* wk = s_k + (size_t)(iy * nkx) * 16 * NSTP;  // x-kind: interior
-        Acc accS[NPAIR > 0 ? NPAIR : 1][4], accD[NPAIR > 0 ? NPAIR : 1][4], accC[4];
+        Acc accS[NPAIR > 0 ? NPAIR : 1][COLS], accD[NPAIR > 0 ? NPAIR : 1][COLS], accC[COLS];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < COLS; ++c) {
           accC[c] = (Acc)0;
 #pragma unroll
           for (int p = 0; p < NPAIR; ++p) { accS[p][c] = (Acc)0; accD[p][c] = (Acc)0; }
         }
-        float4 selfA = make_float4(0, 0, 0, 0), selfB = selfA;
+        float selfA[COLS], selfB[COLS];
 #pragma unroll
         for (int oy = -1; oy <= 2; ++oy) {
-          const float* ra = bufA + (r + 1 + oy) * FT_SX + 4 * lane;
-          const float* rb = bufB + (r + 1 + oy) * FT_SX + 4 * lane;
-          const float4 a0 = *reinterpret_cast<const float4*>(ra);
-          const float4 a1 = *reinterpret_cast<const float4*>(ra + 4);
-          const float2 a2 = *reinterpret_cast<const float2*>(ra + 8);
-          const float4 b0 = *reinterpret_cast<const float4*>(rb);
-          const float4 b1 = *reinterpret_cast<const float4*>(rb + 4);
-          const float2 b2 = *reinterpret_cast<const float2*>(rb + 8);
-          if (oy == 0) { selfA = a1; selfB = b1; }
-          const float fa[7] = {a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y};
-          const float fb[7] = {b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y};
-          Acc S[7], D[7];                                  // exact in fp64
+          const float* ra = bufA + (r + 1 + oy) * FT_SX + COLS * lc;
+          const float* rb = bufB + (r + 1 + oy) * FT_SX + COLS * lc;
+          float fa[COLS + 3], fb[COLS + 3];
+          if constexpr (COLS == 4) {
+            const float4 a0 = *reinterpret_cast<const float4*>(ra);
+            const float4 a1 = *reinterpret_cast<const float4*>(ra + 4);
+            const float2 a2 = *reinterpret_cast<const float2*>(ra + 8);
+            const float4 b0 = *reinterpret_cast<const float4*>(rb);
+            const float4 b1 = *reinterpret_cast<const float4*>(rb + 4);
+            const float2 b2 = *reinterpret_cast<const float2*>(rb + 8);
+            fa[0] = a0.w; fa[1] = a1.x; fa[2] = a1.y; fa[3] = a1.z; fa[4] = a1.w; fa[5] = a2.x; fa[6] = a2.y;
+            fb[0] = b0.w; fb[1] = b1.x; fb[2] = b1.y; fb[3] = b1.z; fb[4] = b1.w; fb[5] = b2.x; fb[6] = b2.y;
+          } else {
+            const float a0 = ra[3];
+            const float2 a1 = *reinterpret_cast<const float2*>(ra + 4);
+            const float2 a2 = *reinterpret_cast<const float2*>(ra + 6);
+            const float b0 = rb[3];
+            const float2 b1 = *reinterpret_cast<const float2*>(rb + 4);
+            const float2 b2 = *reinterpret_cast<const float2*>(rb + 6);
+            fa[0] = a0; fa[1] = a1.x; fa[2] = a1.y; fa[3] = a2.x; fa[4] = a2.y;
+            fb[0] = b0; fb[1] = b1.x; fb[2] = b1.y; fb[3] = b2.x; fb[4] = b2.y;
+          }
+          if (oy == 0) {
 #pragma unroll
-          for (int i = 0; i < 7; ++i) {
+            for (int c = 0; c < COLS; ++c) { selfA[c] = fa[c + 1]; selfB[c] = fb[c + 1]; }
+          }
+          Acc S[COLS + 3], D[COLS + 3];                    // exact in fp64
+#pragma unroll
+          for (int i = 0; i < COLS + 3; ++i) {
             const Acc x = AccVec<Acc>::cvt(fa[i]), y = AccVec<Acc>::cvt(fb[i]);
             S[i] = x + y;
             D[i] = x - y;
@@ -323,7 +361,7 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
             for (int p = 0; p < NPAIR; ++p) {
               const Acc wp = wt[2 * p], wm = wt[2 * p + 1];
 #pragma unroll
-              for (int c = 0; c < 4; ++c) {
+              for (int c = 0; c < COLS; ++c) {
                 accS[p][c] = fma(wp, S[c + ox + 1], accS[p][c]);
                 accD[p][c] = fma(wm, D[c + ox + 1], accD[p][c]);
               }
@@ -331,28 +369,25 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
             if (MID) {
               const Acc wc = wt[2 * NPAIR];
 #pragma unroll
-              for (int c = 0; c < 4; ++c) accC[c] = fma(wc, S[c + ox + 1], accC[c]);
+              for (int c = 0; c < COLS; ++c) accC[c] = fma(wc, S[c + ox + 1], accC[c]);
             }
           }
         }
         const int64_t pix = (int64_t)gy * W + gx;
         // known planes pass through bit-exactly (kriging.py:481)
-        st_cs_f4(a.out + zk * P + pix, selfA);
-        if (copy_b) st_cs_f4(a.out + (zk + G + 1) * P + pix, selfB);
+        st_cs_cols<COLS>(a.out + zk * P + pix, selfA);
+        if (copy_b) st_cs_cols<COLS>(a.out + (zk + G + 1) * P + pix, selfB);
         if (a.var) {
-          st_cs_d2(a.var + zk * P + pix, 0.0, 0.0);
-          st_cs_d2(a.var + zk * P + pix + 2, 0.0, 0.0);
-          if (copy_b) {
-            st_cs_d2(a.var + (zk + G + 1) * P + pix, 0.0, 0.0);
-            st_cs_d2(a.var + (zk + G + 1) * P + pix + 2, 0.0, 0.0);
-          }
+          for (int c = 0; c < COLS; ++c) a.var[zk * P + pix + c] = 0.0;
+          if (copy_b)
+            for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
         }
         const double* vrow = s_var + (iy * nkx) * G;
 #pragma unroll
         for (int j = 0; j < G; ++j) {
-          float o[4];
+          float o[COLS];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < COLS; ++c) {
             Acc t;
             if (MID && j == NPAIR) t = accC[c];
             else if (j < NPAIR) t = accS[j][c] + accD[j][c];
@@ -362,11 +397,12 @@ __global__ void __launch_bounds__(FT_THREADS, 2)
           float* dst = a.out + (zk + 1 + j) * P + pix;
           double* vdst = a.var ? a.var + (zk + 1 + j) * P + pix : nullptr;
           if (!xb0 && !xb1) {
-            st_cs_f4(dst, make_float4(o[0], o[1], o[2], o[3]));
-            if (vdst) { st_cs_d2(vdst, vrow[j], vrow[j]); st_cs_d2(vdst + 2, vrow[j], vrow[j]); }
+            st_cs_cols<COLS>(dst, o);
+            if (vdst)
+              for (int c = 0; c < COLS; ++c) vdst[c] = vrow[j];
           } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < COLS; ++c) {
               const int xx = gx + c;
               if (xx >= 1 && xx <= W - 3) {
                 dst[c] = o[c];

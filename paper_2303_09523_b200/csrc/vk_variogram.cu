@@ -48,14 +48,34 @@ __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ 
   const T* p = data + (int64_t)k * P;
   const double shift = (beg < end) ? (double)p[beg] : 0.0;
   double s1 = 0.0, s2 = 0.0, mn = DBL_MAX, mx = -DBL_MAX, bad = 0.0;
-  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    const double v = (double)p[i];
-    if (!(v - v == 0.0)) { bad += 1.0; continue; }
+  auto take = [&](double v) {
+    if (!(v - v == 0.0)) { bad += 1.0; return; }
     const double d = v - shift;
     s1 += d;
     s2 = fma(d, d, s2);
     mn = fmin(mn, v);
     mx = fmax(mx, v);
+  };
+  const bool vec = sizeof(T) == 4 && ((P & 3) == 0) && ((end - beg) & 3) == 0;
+  if (vec) {
+    // 128-bit loads, 4 in flight per thread
+    const float4* q = reinterpret_cast<const float4*>(p + beg);
+    const int64_t n4 = (end - beg) >> 2;
+    for (int64_t i = threadIdx.x; i < n4; i += 4 * (int64_t)blockDim.x) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t k = i + (int64_t)u * blockDim.x;
+        v[u] = k < n4 ? __ldg(q + k) : make_float4(NAN, NAN, NAN, NAN);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + (int64_t)u * blockDim.x >= n4) continue;
+        take(v[u].x); take(v[u].y); take(v[u].z); take(v[u].w);
+      }
+    }
+  } else {
+    for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) take((double)p[i]);
   }
   __shared__ double sh[5][8];
   s1 = warp_sum(s1); s2 = warp_sum(s2); bad = warp_sum(bad);
@@ -96,42 +116,46 @@ __device__ __forceinline__ double sample_lag(const SampleGeom& g, int64_t i, int
 // jumps its LCG to the chunk start (pcg_advance), counts accepted Lemire
 // halves, a single block scans the counts, and the same threads regenerate
 // and scatter accepted draws to their stream positions (ii = first
-// max_pairs draws, jj = the next max_pairs).
-constexpr int PT_RAW = 64;
+// max_pairs draws, jj = the next max_pairs).  All pair classes of a plan are
+// drawn by the same launches (blockIdx.y = class).
+constexpr int PT_RAW = 16;
 constexpr int PT_BLOCK = 256;
 
-struct PcgArgs {
-  uint64_t st_hi, st_lo, inc_hi, inc_lo;
-  uint32_t m, thr;
-  int64_t n_raw, need, max_pairs;
-};
-
-__global__ void __launch_bounds__(PT_BLOCK) pair_count_kernel(PcgArgs a, int32_t* cnt) {
+__global__ void __launch_bounds__(PT_BLOCK) pair_count_kernel(const PairJob* jobs) {
+  const PairJob& J = jobs[blockIdx.y];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g == 0) {                                   // per-class accumulators start at zero
+    *J.t.hbits = 0ull;
+    for (int b = 0; b < MAX_BINS; ++b) J.t.counts[b] = 0;
+  }
+  if (J.triu) return;
   const int64_t r0 = g * PT_RAW;
-  if (r0 >= a.n_raw) return;
-  const int64_t r1 = min(a.n_raw, r0 + PT_RAW);
-  const u128 inc = ((u128)a.inc_hi << 64) | a.inc_lo;
-  u128 s = pcg_advance(((u128)a.st_hi << 64) | a.st_lo, inc, (uint64_t)r0);
+  if (r0 >= J.n_raw) return;
+  const int64_t r1 = min(J.n_raw, r0 + PT_RAW);
+  const u128 inc = ((u128)J.inc_hi << 64) | J.inc_lo;
+  u128 s = pcg_advance(((u128)J.st_hi << 64) | J.st_lo, inc, (uint64_t)r0);
   const u128 mul = pcg_mult();
   int c = 0;
   for (int64_t r = r0; r < r1; ++r) {
     s = s * mul + inc;
     const uint64_t raw = pcg_output(s);
-    c += ((uint32_t)((uint64_t)(uint32_t)raw * a.m) >= a.thr);
-    c += ((uint32_t)((uint64_t)(uint32_t)(raw >> 32) * a.m) >= a.thr);
+    c += ((uint32_t)((uint64_t)(uint32_t)raw * J.m) >= J.thr);
+    c += ((uint32_t)((uint64_t)(uint32_t)(raw >> 32) * J.m) >= J.thr);
   }
-  cnt[g] = c;
+  J.t.cnt[g] = c;
 }
 
-// exclusive scan of n counts in one block; off[n] = total
-__global__ void __launch_bounds__(1024) pair_scan_kernel(const int32_t* cnt, int64_t n, int64_t* off) {
+// exclusive scan of the per-thread counts in one block per class; off[n] = total
+__global__ void __launch_bounds__(1024) pair_scan_kernel(const PairJob* jobs) {
+  const PairJob& J = jobs[blockIdx.x];
+  if (J.triu) return;
   __shared__ int64_t part[1024];
   const int tid = threadIdx.x;
+  const int64_t n = J.n_thr;
   const int64_t per = (n + 1023) / 1024;
   const int64_t b = min(n, tid * per), e = min(n, b + per);
   int64_t acc = 0;
-  for (int64_t i = b; i < e; ++i) acc += cnt[i];
+  for (int64_t i = b; i < e; ++i) acc += J.t.cnt[i];
   part[tid] = acc;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
@@ -142,75 +166,77 @@ __global__ void __launch_bounds__(1024) pair_scan_kernel(const int32_t* cnt, int
   }
   int64_t run = part[tid] - acc;
   for (int64_t i = b; i < e; ++i) {
-    off[i] = run;
-    run += cnt[i];
+    J.t.off[i] = run;
+    run += J.t.cnt[i];
   }
-  if (tid == 1023) off[n] = part[1023];
+  if (tid == 1023) J.t.off[n] = part[1023];
 }
 
-__global__ void __launch_bounds__(PT_BLOCK) pair_scatter_kernel(PcgArgs a, const int64_t* off, PairTable t) {
+__global__ void __launch_bounds__(PT_BLOCK) pair_scatter_kernel(const PairJob* jobs) {
+  const PairJob& J = jobs[blockIdx.y];
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (J.triu) {
+    // np.triu_indices(m, 1): row-major upper triangle (all pairs fit)
+    const int64_t m = J.m;
+    for (int64_t i = g; i < m - 1; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t o = i * (m - 1) - i * (i - 1) / 2;
+      for (int64_t j = i + 1; j < m; ++j) {
+        J.t.ii[o + (j - i - 1)] = (int32_t)i;
+        J.t.jj[o + (j - i - 1)] = (int32_t)j;
+      }
+    }
+    return;
+  }
   const int64_t r0 = g * PT_RAW;
-  if (r0 >= a.n_raw) return;
-  int64_t pos = off[g];
-  if (pos >= a.need) return;
-  const int64_t r1 = min(a.n_raw, r0 + PT_RAW);
-  const u128 inc = ((u128)a.inc_hi << 64) | a.inc_lo;
-  u128 s = pcg_advance(((u128)a.st_hi << 64) | a.st_lo, inc, (uint64_t)r0);
+  if (r0 >= J.n_raw) return;
+  int64_t pos = J.t.off[g];
+  if (pos >= J.need) return;
+  const int64_t r1 = min(J.n_raw, r0 + PT_RAW);
+  const u128 inc = ((u128)J.inc_hi << 64) | J.inc_lo;
+  u128 s = pcg_advance(((u128)J.st_hi << 64) | J.st_lo, inc, (uint64_t)r0);
   const u128 mul = pcg_mult();
-  for (int64_t r = r0; r < r1 && pos < a.need; ++r) {
+  for (int64_t r = r0; r < r1 && pos < J.need; ++r) {
     s = s * mul + inc;
     const uint64_t raw = pcg_output(s);
-    for (int h = 0; h < 2 && pos < a.need; ++h) {
-      const uint64_t prod = (uint64_t)(uint32_t)(h ? (raw >> 32) : raw) * a.m;
-      if ((uint32_t)prod >= a.thr) {
+    for (int h = 0; h < 2 && pos < J.need; ++h) {
+      const uint64_t prod = (uint64_t)(uint32_t)(h ? (raw >> 32) : raw) * J.m;
+      if ((uint32_t)prod >= J.thr) {
         const int32_t v = (int32_t)(prod >> 32);
-        if (pos < a.max_pairs) t.ii[pos] = v; else t.jj[pos - a.max_pairs] = v;
+        if (pos < J.max_pairs) J.t.ii[pos] = v; else J.t.jj[pos - J.max_pairs] = v;
         ++pos;
       }
     }
   }
 }
 
-// np.triu_indices(m, 1): row-major upper triangle (all pairs fit)
-__global__ void pair_triu_kernel(int64_t m, PairTable t) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m - 1; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = i * (m - 1) - i * (i - 1) / 2;
-    for (int64_t j = i + 1; j < m; ++j) {
-      t.ii[o + (j - i - 1)] = (int32_t)i;
-      t.jj[o + (j - i - 1)] = (int32_t)j;
-    }
-  }
-}
-
 // hmax reduced as the bit pattern of a non-negative double (order-preserving
 // as uint64), so the max is exact and order independent
-__global__ void __launch_bounds__(PT_BLOCK) pair_lag_kernel(int64_t npairs, SampleGeom geom, PairTable t,
-                                                            unsigned long long* hbits) {
+__global__ void __launch_bounds__(PT_BLOCK) pair_lag_kernel(const PairJob* jobs) {
+  const PairJob& J = jobs[blockIdx.y];
   double lmax = 0.0;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t.ii[p], j = t.jj[p];
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < J.npairs; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = J.t.ii[p], j = J.t.jj[p];
     if (i == j) continue;
-    lmax = fmax(lmax, sample_lag(geom, i, j));
+    lmax = fmax(lmax, sample_lag(J.geom, i, j));
   }
   lmax = warp_max(lmax);
-  if ((threadIdx.x & 31) == 0 && lmax > 0.0) atomicMax(hbits, (unsigned long long)__double_as_longlong(lmax));
+  if ((threadIdx.x & 31) == 0 && lmax > 0.0) atomicMax(J.t.hbits, (unsigned long long)__double_as_longlong(lmax));
 }
 
 // scal: [0] hmax [1] lag_max [2] npairs [3] status
-__global__ void __launch_bounds__(PT_BLOCK) pair_bin_kernel(int64_t npairs, int n_bins, SampleGeom geom, PairTable t,
-                                                            const unsigned long long* hbits, const int64_t* off,
-                                                            int64_t need, int64_t n_off) {
+__global__ void __launch_bounds__(PT_BLOCK) pair_bin_kernel(const PairJob* jobs) {
+  const PairJob& J = jobs[blockIdx.y];
   __shared__ unsigned long long h[MAX_BINS];
   if (threadIdx.x < MAX_BINS) h[threadIdx.x] = 0ull;
   __syncthreads();
-  const double hmax = __longlong_as_double((long long)*hbits);
+  const int n_bins = J.n_bins;
+  const double hmax = __longlong_as_double((long long)*J.t.hbits);
   const double step = hmax / (double)n_bins;   // np.linspace(0, hmax, n_bins + 1)
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t.ii[p], j = t.jj[p];
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < J.npairs; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = J.t.ii[p], j = J.t.jj[p];
     uint8_t b = 255;
     if (i != j) {
-      const double lag = sample_lag(geom, i, j);
+      const double lag = sample_lag(J.geom, i, j);
       if (lag > 0.0) {
         int c = 0;                                 // digitize: #edges <= lag
         for (int e = 0; e < n_bins; ++e) c += (__dmul_rn((double)e, step) <= lag);
@@ -220,16 +246,16 @@ __global__ void __launch_bounds__(PT_BLOCK) pair_bin_kernel(int64_t npairs, int 
         atomicAdd(&h[c], 1ull);
       }
     }
-    t.bin[p] = b;
+    J.t.bin[p] = b;
   }
   __syncthreads();
   if (threadIdx.x < n_bins && h[threadIdx.x])
-    atomicAdd((unsigned long long*)&t.counts[threadIdx.x], h[threadIdx.x]);
+    atomicAdd((unsigned long long*)&J.t.counts[threadIdx.x], h[threadIdx.x]);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    t.scal[0] = hmax;
-    t.scal[1] = hmax;                              // lag_max == hmax when any lag > 0
-    t.scal[2] = (double)npairs;
-    t.scal[3] = (off && off[n_off] < need) ? (double)PS_PAIRS_SHORT : 0.0;
+    J.t.scal[0] = hmax;
+    J.t.scal[1] = hmax;                              // lag_max == hmax when any lag > 0
+    J.t.scal[2] = (double)J.npairs;
+    J.t.scal[3] = (!J.triu && J.t.off[J.n_thr] < J.need) ? (double)PS_PAIRS_SHORT : 0.0;
   }
 }
 
@@ -365,7 +391,10 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
     return;
   }
   WarpTrf wt(P, lane);
+  VK_PT(t_f0);
   const TrfResult r = wt.fit(x0, lb, ub);
+  VK_PT(t_f1);
+  VK_PACC(5, t_f0, t_f1);
   if (lane != 0) return;
   if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
   const double nug = pymax(r.x[0], 0.0);
@@ -424,6 +453,17 @@ __global__ void __launch_bounds__(32) fit_scalar_kernel(FitArgs a) {
 
 }  // namespace
 
+#ifdef VK_FIT_PROFILE
+extern "C" int vk_debug_fit_profile(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_fit_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_fit_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
 cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out, int nchunk,
                                cudaStream_t st) {
   dim3 grid(nchunk, K);
@@ -438,42 +478,26 @@ cudaError_t launch_plane_stats_f64(const double* values, int64_t m, ChunkStat* o
   return cudaGetLastError();
 }
 
-cudaError_t launch_pair_table(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
-                              int64_t m, int64_t max_pairs, int n_bins, SampleGeom geom,
-                              PairTable t, cudaStream_t st) {
+PairJob make_pair_job(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t m,
+                      int64_t max_pairs, int n_bins, SampleGeom geom, PairTable t) {
+  PairJob J{};
+  J.st_hi = st_hi; J.st_lo = st_lo; J.inc_hi = inc_hi; J.inc_lo = inc_lo;
+  J.t = t;
+  J.geom = geom;
+  J.n_bins = n_bins;
+  J.max_pairs = max_pairs;
   const int64_t total = m * (m - 1) / 2;
-  const int64_t npairs = total <= max_pairs ? total : max_pairs;
-  cudaError_t e;
-  int64_t n_thr = 0;
-  PcgArgs a{};
-  if (total > max_pairs) {
-    a.st_hi = st_hi; a.st_lo = st_lo; a.inc_hi = inc_hi; a.inc_lo = inc_lo;
-    a.m = (uint32_t)m;
-    a.thr = lemire_threshold(a.m);
-    a.need = 2 * max_pairs;
-    a.max_pairs = max_pairs;
-    const double prej = (double)a.thr / 4294967296.0;
-    a.n_raw = (int64_t)((double)a.need * (1.0 + 4.0 * prej) / 2.0) + 4096;
-    n_thr = (a.n_raw + PT_RAW - 1) / PT_RAW;
+  J.triu = total <= max_pairs;
+  J.npairs = J.triu ? total : max_pairs;
+  J.m = (uint32_t)m;
+  if (!J.triu) {
+    J.thr = lemire_threshold(J.m);
+    J.need = 2 * max_pairs;
+    const double prej = (double)J.thr / 4294967296.0;
+    J.n_raw = (int64_t)((double)J.need * (1.0 + 4.0 * prej) / 2.0) + 4096;
+    J.n_thr = (J.n_raw + PT_RAW - 1) / PT_RAW;
   }
-  int32_t* cnt = t.cnt;
-  int64_t* off = t.off;
-  unsigned long long* hbits = t.hbits;
-  if ((e = cudaMemsetAsync(hbits, 0, 8, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(t.counts, 0, MAX_BINS * sizeof(int64_t), st)) != cudaSuccess) return e;
-  if (total > max_pairs) {
-    const unsigned nb = (unsigned)((n_thr + PT_BLOCK - 1) / PT_BLOCK);
-    pair_count_kernel<<<nb, PT_BLOCK, 0, st>>>(a, cnt);
-    pair_scan_kernel<<<1, 1024, 0, st>>>(cnt, n_thr, off);
-    pair_scatter_kernel<<<nb, PT_BLOCK, 0, st>>>(a, off, t);
-  } else {
-    pair_triu_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, (m + 255) / 256)), 256, 0, st>>>(m, t);
-  }
-  const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(1184, (npairs + PT_BLOCK - 1) / PT_BLOCK));
-  pair_lag_kernel<<<gb, PT_BLOCK, 0, st>>>(npairs, geom, t, hbits);
-  pair_bin_kernel<<<gb, PT_BLOCK, 0, st>>>(npairs, n_bins, geom, t, hbits, n_thr ? off : nullptr,
-                                           total > max_pairs ? a.need : 0, n_thr);
-  return cudaGetLastError();
+  return J;
 }
 
 int64_t pair_scratch_elems(int64_t m, int64_t max_pairs) {
@@ -482,6 +506,24 @@ int64_t pair_scratch_elems(int64_t m, int64_t max_pairs) {
   const double prej = (double)thr / 4294967296.0;
   const int64_t n_raw = (int64_t)((double)(2 * max_pairs) * (1.0 + 4.0 * prej) / 2.0) + 4096;
   return (n_raw + PT_RAW - 1) / PT_RAW;
+}
+
+cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st) {
+  int64_t max_thr = 1, max_pairs = 1, max_m = 1;
+  for (int c = 0; c < n_jobs; ++c) {
+    max_thr = std::max(max_thr, h_jobs[c].n_thr);
+    max_pairs = std::max(max_pairs, h_jobs[c].npairs);
+    if (h_jobs[c].triu) max_m = std::max<int64_t>(max_m, h_jobs[c].m);
+  }
+  const unsigned nb = (unsigned)std::max<int64_t>((max_thr + PT_BLOCK - 1) / PT_BLOCK,
+                                                  std::min<int64_t>(1024, (max_m + PT_BLOCK - 1) / PT_BLOCK));
+  pair_count_kernel<<<dim3(nb, n_jobs), PT_BLOCK, 0, st>>>(d_jobs);
+  pair_scan_kernel<<<n_jobs, 1024, 0, st>>>(d_jobs);
+  pair_scatter_kernel<<<dim3(nb, n_jobs), PT_BLOCK, 0, st>>>(d_jobs);
+  const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(1184, (max_pairs + PT_BLOCK - 1) / PT_BLOCK));
+  pair_lag_kernel<<<dim3(gb, n_jobs), PT_BLOCK, 0, st>>>(d_jobs);
+  pair_bin_kernel<<<dim3(gb, n_jobs), PT_BLOCK, 0, st>>>(d_jobs);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
