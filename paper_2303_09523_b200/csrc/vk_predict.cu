@@ -23,6 +23,8 @@
 //                  per missing voxel, reading the known planes through L1/L2.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <type_traits>
 #include "vk_kernels.h"
 
 namespace vk {
@@ -504,20 +506,21 @@ int predict_fast_supported(int G, int accum) {
   return G >= 1 && G <= 8;
 }
 
+static size_t fast_smem() { return (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(float); }
+
 template <int G, typename Acc>
 static cudaError_t occupancy_t(int* occ) {
+  const size_t smem = fast_smem();
   auto kern = predict_fast_kernel<G, Acc>;
-  const size_t smem = (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, FT_THREADS, smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, FT_THREADS, smem);
   *occ = std::max(1, *occ);
   return e;
 }
 
 template <int G, typename Acc>
 static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(float);
+  const size_t smem = fast_smem();
   const int ntx = (a.W + FT_TX - 1) / FT_TX, nty = (a.H + FT_TY - 1) / FT_TY;
   const int n_tiles = ntx * nty, n_gaps = a.gap1 - a.gap0;
   if (n_gaps <= 0) return cudaSuccess;
@@ -530,8 +533,8 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   const int n_chunks = (n_gaps + chunk - 1) / chunk;
   const int n_units = n_tiles * n_chunks;
   const int grid = std::min(n_units, resident);
-  predict_fast_kernel<G, Acc><<<grid, FT_THREADS, smem, st>>>(
-      *reinterpret_cast<const CUtensorMap*>(fl.tmap), a, ntx, n_tiles, chunk, n_units);
+  const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(fl.tmap);
+  predict_fast_kernel<G, Acc><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
   return cudaGetLastError();
 }
 
