@@ -1,0 +1,179 @@
+"""GPU parity at BASELINE.json's full sizes (C1-C5 shapes), where running the
+oracle over whole volumes would take minutes to hours.  Checked instead:
+
+* sampled-voxel parity: for a few sub-parts, the oracle fits the variogram
+  (scipy TRF) and predicts a random sample of missing voxels with its own
+  stencil solves; the device, given those models, must agree at the fp64
+  gate (1e-6 of range) -- the oracle's per-voxel formula is the reference's
+  (kriging.py:523-557);
+* device fit vs oracle fit on the same sub-parts (fit fuzz bound);
+* size-independent properties: known planes bit-exact, predictions inside
+  the part's clamp range, bit-identical reruns, linear fields reproduced,
+  affine equivariance (models scale with the data, weights do not change).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import kriging_oracle as O
+
+pytestmark = [pytest.mark.gpu]
+
+TOL64 = 1e-6
+TOL32 = 1e-3
+FIT_FUZZ = 5e-5
+
+
+def _oracle_voxels(ks, b, e, factor, model, drift, zyx):
+    """Oracle predictions for selected voxels (z, y, x local to the part)."""
+    data, mask = O.subpart_grid(ks, b, e, factor)
+    dz, dy, dx = data.shape
+    kz = np.nonzero(~O.plane_flags(mask))[0]
+    known = data[~mask]
+    lo, hi = float(known.min()), float(known.max())
+    out = np.empty(len(zyx))
+    cache = {}
+    for n, (z, y, x) in enumerate(zyx):
+        planes = O.plane_window(int(z), kz, dz)
+        offs = [int(p) - int(z) for p in planes]
+        y0, y1 = O.window(int(y), 4, dy)
+        x0, x1 = O.window(int(x), 4, dx)
+        rel = np.array([(ox - x, oy - y, oz) for oz in offs for oy in range(y0, y1)
+                        for ox in range(x0, x1)], dtype=np.int64)
+        key = rel.tobytes()
+        if key not in cache:
+            cache[key] = O.stencil_weights(rel, model, drift)[0]
+        vals = np.concatenate([data[z + oz, y0:y1, x0:x1].ravel() for oz in offs])
+        out[n] = min(max(float(cache[key] @ vals), lo), hi)
+    return out
+
+
+@pytest.fixture(scope="module")
+def c4(cuda):
+    from paper_2303_09523_b200.phantoms import CONFIGS, known_slices
+    cfg = CONFIGS["C4"]
+    return cfg, known_slices(cfg)
+
+
+def test_c4_sampled_voxels_vs_oracle(cuda, c4):
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    cfg, ks = c4
+    f = cfg.factor
+    ranges = O.subpart_ranges(cfg.n_known, cfg.n_subparts)
+    kd = torch.from_numpy(ks).cuda()
+    # device fit + oracle fit on a few sub-parts
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, f, cfg.n_subparts)
+    out_fit, _ = zk.run(kd)
+    dev_models, _ = zk.finish()
+    parts = [0, 13, cfg.n_subparts - 1]
+    ref_models = {}
+    for s in parts:
+        b, e = ranges[s]
+        d, m = O.subpart_grid(ks, b, e, f)
+        ref_models[s] = O.fit_variogram(O.subpart_samples(d, m))
+        r, g = ref_models[s], dev_models[s]
+        assert abs(g.sill - r.sill) <= 1e-3 * r.sill, (s, g, r)
+    # device kriging with the oracle's models (others: device models)
+    models = [ref_models.get(s, dev_models[s]) for s in range(cfg.n_subparts)]
+    zf = ZPartKriging(cfg.n_known, cfg.height, cfg.width, f, cfg.n_subparts, fit=False)
+    out, _ = zf.run(kd, models=[VariogramModel("exponential", m.nugget, m.sill, m.range_len)
+                                for m in models])
+    zf.finish()
+    vol = out.cpu().numpy()
+    fitvol = out_fit.cpu().numpy()
+    rng = np.random.default_rng(0)
+    data_range = float(ks.max() - ks.min())
+    for s in parts:
+        b, e = ranges[s]
+        depth = (e - b) * f + 1
+        zl = rng.integers(0, depth, 400)
+        zl = zl[zl % f != 0]
+        # include border rows / columns explicitly
+        yl = np.concatenate([rng.integers(0, cfg.height, len(zl) - 6), [0, 1, cfg.height - 2,
+                                                                          cfg.height - 1, 0, 511]])
+        xl = np.concatenate([rng.integers(0, cfg.width, len(zl) - 6), [0, cfg.width - 1, 5,
+                                                                         cfg.width - 2, 1, 0]])
+        zyx = np.stack([zl, yl[:len(zl)], xl[:len(zl)]], 1)
+        exp = _oracle_voxels(ks, b, e, f, ref_models[s], "linear", zyx)
+        got = vol[b * f + zyx[:, 0], zyx[:, 1], zyx[:, 2]].astype(np.float64)
+        assert np.abs(got - exp).max() <= TOL64 * data_range
+        assert np.abs(np.rint(got) - np.rint(exp)).max() <= 1
+        gfit = fitvol[b * f + zyx[:, 0], zyx[:, 1], zyx[:, 2]].astype(np.float64)
+        assert np.abs(gfit - exp).max() <= FIT_FUZZ * data_range
+
+
+def test_c4_properties(cuda, c4):
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    cfg, ks = c4
+    f = cfg.factor
+    kd = torch.from_numpy(ks).cuda()
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, f, cfg.n_subparts)
+    a, _ = zk.run(kd)
+    _, lohi = zk.finish()
+    b2, _ = zk.run(kd)
+    zk.finish()
+    assert torch.equal(a, b2)                                # deterministic
+    vol = a.cpu().numpy()
+    assert np.array_equal(vol[::f], ks)                      # known planes bit-exact
+    for s, (b, e) in enumerate(O.subpart_ranges(cfg.n_known, cfg.n_subparts)):
+        part = vol[b * f:e * f + 1]
+        assert part.min() >= lohi[s, 0] and part.max() <= lohi[s, 1]
+        assert lohi[s, 0] == ks[b:e + 1].min() and lohi[s, 1] == ks[b:e + 1].max()
+
+
+def test_affine_equivariance_full_size(cuda, c4):
+    """x -> a x + c with the model scaled accordingly (nugget, sill * a^2,
+    same range): kriging weights are invariant to the sill scale and the
+    clamp range maps affinely, so predictions map affinely to rounding.
+    (The TRF fit itself is not scale invariant -- absolute gtol, x_scale=1 --
+    so the fitted path is checked against the oracle elsewhere.)"""
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    cfg, ks = c4
+    f = cfg.factor
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, f, cfg.n_subparts)
+    zk.run(torch.from_numpy(ks).cuda())
+    m1, _ = zk.finish()
+    a, c = 0.5, 1000.0
+    zf = ZPartKriging(cfg.n_known, cfg.height, cfg.width, f, cfg.n_subparts, fit=False)
+    o1, _ = zf.run(torch.from_numpy(ks).cuda(), models=m1)
+    zf.finish()
+    v1 = o1.cpu().numpy().astype(np.float64)
+    ks2 = (ks * a + c).astype(np.float32)                      # exact in f32 for 12-bit data
+    m2 = [VariogramModel("exponential", m.nugget * a * a, m.sill * a * a, m.range_len) for m in m1]
+    o2, _ = zf.run(torch.from_numpy(ks2).cuda(), models=m2)
+    zf.finish()
+    v2 = o2.cpu().numpy().astype(np.float64)
+    rng2 = float(ks2.max() - ks2.min())
+    # f32 rounding of outputs near 1000-3000 dominates: half an ulp at 2048 is 1.2e-4
+    assert np.abs((v1 * a + c) - v2).max() <= TOL64 * rng2 + 2.5e-4
+
+
+@pytest.mark.parametrize("name,accum", [("C2", "fp64"), ("C3", "fp32"), ("C5", "fp32")])
+def test_linear_field_reproduced_full_size(cuda, name, accum):
+    """Any field in the drift span {1, x, y, z} is reproduced exactly by
+    universal kriging with linear drift -- at full size."""
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.phantoms import CONFIGS
+    cfg = CONFIGS[name]
+    K, H, W, f = cfg.n_known, cfg.height, cfg.width, cfg.factor
+    z = (np.arange(K) * f).astype(np.float32)[:, None, None]
+    y = np.arange(H, dtype=np.float32)[None, :, None]
+    x = np.arange(W, dtype=np.float32)[None, None, :]
+    ks = (0.25 * x + 0.5 * y + 0.125 * z + 3.0).astype(np.float32)
+    zk = ZPartKriging(K, H, W, f, cfg.n_subparts, accum=accum)
+    out, _ = zk.run(torch.from_numpy(ks).cuda())
+    zk.finish()
+    T = out.shape[0]
+    yy = torch.arange(H, device="cuda", dtype=torch.float64)[None, :, None]
+    xx = torch.arange(W, device="cuda", dtype=torch.float64)[None, None, :]
+    err = 0.0
+    for z0 in range(0, T, 64):                       # chunked: C5 is 8.6 GB of output
+        zz = torch.arange(z0, min(T, z0 + 64), device="cuda", dtype=torch.float64)[:, None, None]
+        exact = 0.25 * xx + 0.5 * yy + 0.125 * zz + 3.0
+        err = max(err, (out[z0:z0 + 64].double() - exact).abs().max().item())
+    rng = float(ks.max() - ks.min())
+    assert err <= (TOL64 if accum == "fp64" else TOL32) * rng, err
