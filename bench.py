@@ -303,10 +303,11 @@ def run_gpu(args, cfg, ks):
     stages = {k2: v / args.steps for k2, v in stage_acc.items()}
     stages["sum"] = serial_ms
 
-    # end to end through the public API with host buffers
+    # end to end through the public API with host buffers (every rank: its
+    # own slab H2D, halo exchange, kriging path, its output D2H)
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = run_e2e(args, cfg, ks, zk, stream)
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, ks, stream, rank, world, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -334,22 +335,32 @@ def run_gpu(args, cfg, ks):
     return 0
 
 
-def run_e2e(args, cfg, ks, zk, stream):
+def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):
     """Same metric through the public API from pinned host buffers: H2D of
-    the known slices + kriging path + D2H of the reconstructed volume."""
+    the known slices + (halo exchange) + kriging path + D2H of the
+    reconstructed volume, every step.  Max over ranks."""
     import torch
+    import torch.distributed as dist
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.zshard import exchange_halo
     H, W = cfg.height, cfg.width
     K = cfg.n_known
+    has_halo = rank < world - 1
+    K_loc = K + int(has_halo)
     host_in = torch.from_numpy(ks).pin_memory()
-    from paper_2303_09523_b200 import ZPartKriging
-    zk1 = ZPartKriging(K, H, W, cfg.factor, cfg.n_subparts, accum=args.accum, redraw_pairs=True)
-    dev_in = torch.empty((K, H, W), dtype=torch.float32, device="cuda")
+    zk1 = ZPartKriging(K_loc, H, W, cfg.factor, cfg.n_subparts, accum=args.accum,
+                       redraw_pairs=True, part_len=K // cfg.n_subparts)
+    dev_in = torch.empty((K_loc, H, W), dtype=torch.float32, device=dev or "cuda")
     out, var = zk1.allocate(bool(args.variance))
     host_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
     host_var = torch.empty(var.shape, dtype=torch.float64).pin_memory() if var is not None else None
 
     def step():
-        dev_in.copy_(host_in, non_blocking=True)
+        dev_in[:K].copy_(host_in, non_blocking=True)
+        if world > 1:
+            halo = exchange_halo(dev_in[0], rank, world)
+            if halo is not None:
+                dev_in[K].copy_(halo)
         zk1.run(dev_in, out, var)
         host_out.copy_(out, non_blocking=True)
         if var is not None:
@@ -361,6 +372,8 @@ def run_e2e(args, cfg, ks, zk, stream):
     steps = max(2, min(args.steps, 5))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(steps):
@@ -369,10 +382,18 @@ def run_e2e(args, cfg, ks, zk, stream):
     torch.cuda.synchronize()
     zk1.finish()
     ms = e0.elapsed_time(e1) / steps
+    vox = float(zk1.interpolated_voxels)
+    if world > 1:
+        t = torch.tensor([ms, vox], device=dev, dtype=torch.float64)
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        tv = t[1:].clone()
+        dist.all_reduce(tv)
+        ms, vox = float(tm.item()), float(tv.item())
     d2h = out.numel() * 4 + (var.numel() * 8 if var is not None else 0)
-    return {"value": zk1.interpolated_voxels / (ms / 1e3), "unit": UNIT,
+    return {"value": vox / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": K * H * W * 4, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": steps}
+            "ms_per_step": ms, "steps": steps, "per_rank_bytes": True}
 
 
 def main(argv=None):
