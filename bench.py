@@ -44,6 +44,11 @@ def _peaks():
         return 6650.0, 1965.0, "fallback"
 
 
+# arithmetic the prediction stencil runs in (solves and fits are fp64 always)
+DTYPES = {"fp64": "f64", "fp32": "f32",
+          "fixed": "u8xs8->s32 (24-bit fixed-point values x 32-bit fixed-point weights, exact)"}
+
+
 def _profile_traffic(name: str):
     """dram bytes per launch of the prediction kernel from the committed ncu
     summary (profiles/*.json), or None."""
@@ -323,7 +328,7 @@ def run_gpu(args, cfg, ks):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64" if args.accum == "fp64" else "f32",
+            "dtype": DTYPES[args.accum],
             "data": "synthetic (seeded C4 HDR spine phantom)",
             "config": _config(cfg, args, world),
             "roofline": roof, "stage_ms": stages, "cpu_baseline": cpu, "e2e": e2e,
@@ -403,7 +408,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--accum", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--accum", default="fp64", choices=["fp64", "fp32", "fixed"])
     ap.add_argument("--variance", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

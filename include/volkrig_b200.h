@@ -53,7 +53,11 @@ typedef enum {
 
 enum { VK_KIND_EXPONENTIAL = 0, VK_KIND_GAUSSIAN = 1, VK_KIND_SPHERICAL = 2 };
 enum { VK_DRIFT_LINEAR = 0, VK_DRIFT_CONSTANT = 1 };
-enum { VK_ACCUM_FP64 = 0, VK_ACCUM_FP32 = 1 };
+/* prediction arithmetic: fp64 / fp32 DFMA-FFMA stencils, or FIXED: 24-bit
+ * fixed-point known values x 32-bit fixed-point weights on the int8 tensor
+ * cores with exact s32 accumulation (error <= ~2e-7 of the data range;
+ * plane-structured fast layout only, fp64 elsewhere) */
+enum { VK_ACCUM_FP64 = 0, VK_ACCUM_FP32 = 1, VK_ACCUM_FIXED = 2 };
 
 typedef struct vk_plan vk_plan;
 

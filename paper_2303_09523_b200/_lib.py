@@ -26,7 +26,7 @@ VK_E_FIT_FAILED = 9
 
 KIND_IDS = {"exponential": 0, "gaussian": 1, "spherical": 2}
 DRIFT_IDS = {"linear": 0, "constant": 1}
-ACCUM_IDS = {"fp64": 0, "fp32": 1}
+ACCUM_IDS = {"fp64": 0, "fp32": 1, "fixed": 2}
 FLAG_FORCE_GENERIC = 1
 FLAG_REDRAW_PAIRS = 2
 FLAG_OVERLAP = 4

@@ -28,6 +28,7 @@ UNITS = {
     "vk_variogram.cu": [],
     "vk_solve.cu": [],
     "vk_predict.cu": [],
+    "vk_predict_fixed.cu": [],
     "vk_geometry.cpp": [],
 }
 

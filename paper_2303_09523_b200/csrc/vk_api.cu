@@ -77,6 +77,10 @@ struct vk_plan {
   // workspace
   ChunkStat* d_stats = nullptr;
   double *d_partial = nullptr, *d_models = nullptr, *d_lohi = nullptr, *d_weights = nullptr, *d_var = nullptr;
+  double* d_kpm = nullptr;
+  uint32_t* d_fxb = nullptr;           // fixed path tables
+  float *d_fxc = nullptr, *d_fxq = nullptr;
+  int max_chunk = 0;                  // fast path: a run of this many gaps spans <= 4 parts
   int32_t *d_part_status = nullptr, *d_sys_status = nullptr;
   std::vector<PairTable> tables;
   PairTable* d_tables = nullptr;
@@ -153,6 +157,7 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   *out = nullptr;
   if (d->kind < 0 || d->kind > 2) return set_err(VK_E_INVALID_ARGUMENT, "kind");
   if (d->drift < 0 || d->drift > 1) return set_err(VK_E_INVALID_ARGUMENT, "drift");
+  if (d->accum < 0 || d->accum > 2) return set_err(VK_E_INVALID_ARGUMENT, "accum");
   if (d->n_bins < 1 || d->n_bins > MAX_BINS) return set_err(VK_E_INVALID_ARGUMENT, "n_bins must be in 1..32");
   if (d->max_pairs < 1 || d->max_pairs > (1ll << 30)) return set_err(VK_E_INVALID_ARGUMENT, "max_pairs");
   if (!d->known_z && d->n_known > 0) return set_err(VK_E_INVALID_ARGUMENT, "known_z");
@@ -261,6 +266,12 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   VK_TRY(p->alloc(&p->d_sys_status, (size_t)std::max(1, p->n_sys)));
   VK_TRY(p->alloc(&p->d_weights, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK) * WPAD));
   VK_TRY(p->alloc(&p->d_var, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK)));
+  if (g.fast) VK_TRY(p->alloc(&p->d_kpm, kpm_elems(S, std::max(1, p->NK))));
+  if (g.fast && d->accum == VK_ACCUM_FIXED) {
+    VK_TRY(p->alloc(&p->d_fxb, fxb_words(S, std::max(1, p->NK))));
+    VK_TRY(p->alloc(&p->d_fxc, fxc_floats(S, std::max(1, p->NK))));
+    VK_TRY(p->alloc(&p->d_fxq, (size_t)4));
+  }
   VK_TRY(cudaMallocHost((void**)&p->h_models, (size_t)S * 3 * sizeof(double)));
   if (d->fit_variogram) {
     VK_TRY(p->alloc(&p->d_partial, (size_t)S * p->nblk * d->n_bins));
@@ -306,6 +317,15 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   if (g.fast) {
     for (int s = 0; s <= S; ++s) p->gap_begin[s] = (s < S) ? g.parts[s].b : g.K - 1;
     for (int s = 0; s < S; ++s) p->gap_begin[s] = std::min(p->gap_begin[s], g.K - 1);
+    // shortest non-empty run of gaps owned by one part: a run of c gaps that
+    // touches 5 parts holds 3 of them whole, so c <= 3 * min_len + 1 keeps
+    // every unit within the kernel's 4 staged parts
+    int min_len = g.K;
+    for (int k = 0, run = 0; k < g.K - 1; ++k) {
+      ++run;
+      if (k == g.K - 2 || g.gap_part[k + 1] != g.gap_part[k]) { min_len = std::min(min_len, run); run = 0; }
+    }
+    p->max_chunk = 3 * std::max(1, min_len) + 1;
   }
   if ((d->flags & VK_FLAG_OVERLAP) && S > 1) {
     VK_TRY(cudaEventCreateWithFlags(&p->ev_kfork, cudaEventDisableTiming));
@@ -461,6 +481,14 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   pa.chunk = 0;
   pa.gap_part = p->d_gap_part;
   pa.gap_pattern = p->d_gap_pattern;
+  pa.part0 = 0;
+  pa.part1 = S;
+  pa.max_chunk = p->max_chunk;
+  pa.kpm = p->d_kpm;
+  pa.S = S;
+  pa.fxb = p->d_fxb;
+  pa.fxc = p->d_fxc;
+  pa.fxq = p->d_fxq;
   pa.num_sms = p->num_sms;
   const bool fast = g.fast && predict_fast_supported(g.G, d.accum);
   if (fast) VK_CUDA(prepare_predict_fast(pa, &p->fast_launch));
@@ -486,8 +514,10 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       p1.gap0 = p->gap_begin[s];
       p1.gap1 = p->gap_begin[s + 1];
       p1.chunk = p1.gap1 - p1.gap0;           // one unit = a tile over the part's gaps
+      p1.part0 = s;
+      p1.part1 = s + 1;
       VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, cs));
-      kernels += 2 + (s1.n_sys > 0);
+      kernels += 3 + (s1.n_sys > 0);
     }
     for (int c = 0; c < nch; ++c) {
       VK_CUDA(cudaEventRecord(p->ev_kjoin[c], p->chain[c]));
@@ -504,7 +534,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(mark(5));
     if (fast) {
       VK_CUDA(launch_predict_fast_prepared(p->fast_launch, pa, st));
-      ++kernels;
+      kernels += 2;                             // stencil table + streaming kernel
     } else {
       VK_CUDA(launch_copy_known(pa, st));
       VK_CUDA(launch_predict_generic(pa, st));

@@ -121,8 +121,17 @@ struct PredictArgs {
   int chunk;                   // gaps per unit (0: automatic)
   const int32_t* gap_part;     // [K-1]
   const int32_t* gap_pattern;  // [(K-1) * G]
+  int part0, part1;            // parts whose mirror-pair stencils this launch prepares
+  int S;                       // parts in the plan
+  void* fxb;                   // fixed path: [S][NK][32][8] u32 B fragments
+  void* fxc;                   // fixed path: [S][NK][8] float4 epilogue constants
+  void* fxq;                   // fixed path: float4 quantisation (L, 1/step, step, 0)
+  int max_chunk;               // gaps per unit so that a unit spans <= 4 parts (0: none)
+  void* kpm;                   // [S][NK][16][NSTP] Acc mirror-pair stencils (fast path)
   int num_sms;
 };
+// doubles the K+- table needs (fast path)
+inline size_t kpm_elems(int S, int NK) { return (size_t)S * (size_t)NK * 16 * 8; }
 // Launch state of the streaming kernel prepared once per known-plane buffer:
 // TMA descriptor, occupancy-derived grid size.
 struct FastLaunch {
@@ -136,5 +145,12 @@ cudaError_t launch_copy_known(const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_predict_generic(const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_predict_fast(const PredictArgs& a, cudaStream_t st);
 int predict_fast_supported(int G, int accum);
+// fp64 mirror-pair stencil table (a.kpm) for parts [a.part0, a.part1)
+cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st);
+// fixed-point tensor-core path (vk_predict_fixed.cu)
+cudaError_t occupancy_fixed(int G, int* occ);
+cudaError_t launch_predict_fixed(const void* tmap, int occ, const PredictArgs& a, cudaStream_t st);
+inline size_t fxb_words(int S, int NK) { return (size_t)S * (size_t)NK * 32 * 8; }
+inline size_t fxc_floats(int S, int NK) { return (size_t)S * (size_t)NK * 8 * 4; }
 
 }  // namespace vk

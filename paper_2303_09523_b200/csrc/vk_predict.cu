@@ -3,7 +3,7 @@
 // predict_fast   : the production layout -- every missing plane reads its two
 //                  bracketing known planes (k, k+1).  Persistent CTAs walk
 //                  (in-plane tile, run of gaps) units; known-plane tiles are
-//                  streamed into a 3-deep shared-memory ring by TMA
+//                  streamed into a 4-deep shared-memory ring by TMA
 //                  (cp.async.bulk.tensor, OOB zero fill supplies the volume
 //                  halo) so each known plane is read from HBM once per run.
 //                  The G missing planes of a gap come in z-mirror pairs
@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <type_traits>
 #include "vk_kernels.h"
+#include "vk_tma.cuh"
 
 namespace vk {
 
@@ -110,42 +111,11 @@ __global__ void __launch_bounds__(256) copy_known_kernel(PredictArgs a) {
 #endif
 constexpr int FT_WARPS = VK_FT_WARPS;
 constexpr int FT_THREADS = FT_WARPS * 32;
-constexpr int FT_TX = 128;                 // tile columns (32 lanes x 4)
 constexpr int FT_TY = VK_FT_TY;            // tile rows (warps x row steps)
-constexpr int FT_SX = FT_TX + 8;           // smem row: x0-4 .. x0+131
 constexpr int FT_SY = FT_TY + 3;           // smem rows: y0-1 .. y0+33
 constexpr int FT_BUF_FLOATS = ((FT_SX * FT_SY * 4 + 127) / 128) * 128 / 4;
-constexpr int FT_STAGES = 3;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
-                                            int z) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-      : "memory");
-}
+constexpr int FT_STAGES = 4;
+constexpr int FT_WPARTS = 4;             // parts whose stencils a unit stages
 
 template <typename Acc>
 struct AccVec;
@@ -163,9 +133,6 @@ __device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
                "f"(v.w)
                : "memory");
 }
-__device__ __forceinline__ void st_cs_d2(double* p, double a, double b) {
-  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
-}
 
 template <int COLS>
 __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
@@ -180,6 +147,64 @@ __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
 #define VK_FT_COLS 4
 #endif
 
+// Mirror-pair stencil table for the streaming kernel (one thread per
+// (part, kind, tap)).  Missing planes j and G-1-j are z-mirrors: their
+// stencils satisfy wA_j = wB_{G-1-j}, wB_j = wA_{G-1-j} (isotropic covariance;
+// drift span closed under z -> -z).  With a, b the mirror-averaged plane-A /
+// plane-B stencils of j, out_j = a*A + b*B = K+*(A+B) + K-*(A-B) and
+// out_{G-1-j} = K+*(A+B) - K-*(A-B) with K+- = (a +- b)/2: one symmetric and
+// one antisymmetric 16-tap stencil per pair instead of four.  Layout
+// [s][kind][tap][K+_0, K-_0, ..., K_mid, pad] so one 128-bit load fetches a
+// pair.  Taps outside a clamped border window are 0 in the solved weights.
+template <int G, typename Acc>
+__global__ void __launch_bounds__(256) fast_stencil_kernel(PredictArgs a) {
+  constexpr int NPAIR = G / 2;
+  constexpr bool MID = (G & 1) != 0;
+  constexpr int NST = 2 * NPAIR + (MID ? 1 : 0);
+  constexpr int NSTP = (NST + 1) & ~1;
+  const int per_part = a.NK * 16;
+  const int n = (a.part1 - a.part0) * per_part;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = a.part0 + i / per_part, r = i - (i / per_part) * per_part;
+    const int kind = r >> 4, t = r & 15;
+    Acc* dst = reinterpret_cast<Acc*>(a.kpm) + (((size_t)s * a.NK + kind) * 16 + t) * NSTP;
+    // patterns are identical for every gap on the fast path (each missing
+    // plane reads exactly its two bracketing known planes)
+    for (int pr = 0; pr < NPAIR + (MID ? 1 : 0); ++pr) {
+      const int pj = a.gap_pattern[pr], pm = a.gap_pattern[G - 1 - pr];
+      const double* wj = a.weights + (((int64_t)s * a.NP + pj) * a.NK + kind) * WPAD;
+      const double* wm = a.weights + (((int64_t)s * a.NP + pm) * a.NK + kind) * WPAD;
+      const double av = 0.5 * (wj[t] + wm[16 + t]);
+      const double bv = 0.5 * (wj[16 + t] + wm[t]);
+      if (pr < NPAIR) {
+        dst[2 * pr] = (Acc)(0.5 * (av + bv));
+        dst[2 * pr + 1] = (Acc)(0.5 * (av - bv));
+      } else {
+        dst[2 * NPAIR] = (Acc)(0.5 * (av + bv));
+      }
+    }
+    if (NSTP > NST) dst[NST] = (Acc)0;
+  }
+}
+
+template <typename Acc>
+struct Pair2;
+template <>
+struct Pair2<double> {
+  using T = double2;
+};
+template <>
+struct Pair2<float> {
+  using T = float2;
+};
+
+
+// Streaming kernel.  No CTA-wide barrier inside a unit: each warp waits only
+// for the TMA of the two planes its gap reads and, when done with plane k,
+// releases it; the last warp to release a ring slot refills it with plane
+// k + FT_STAGES.  Warps therefore drift apart by up to a few gaps, so the
+// FP64 pipe of an SM sub-partition sees a mix of DFMA-heavy and
+// load/convert/store phases instead of all warps in lock step.
 template <int G, typename Acc, int COLS = VK_FT_COLS>
 __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
     predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
@@ -188,26 +213,35 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
   constexpr bool MID = (G & 1) != 0;
   constexpr int NST = 2 * NPAIR + (MID ? 1 : 0);          // stencils per kind
   constexpr int NSTP = (NST + 1) & ~1;                     // padded: 16-byte aligned taps
+  using P2 = typename Pair2<Acc>::T;
   extern __shared__ __align__(128) float ring[];           // FT_STAGES x FT_BUF_FLOATS
   __shared__ __align__(8) uint64_t full[FT_STAGES];
-  // mirror-pair stencils per (y-kind, x-kind) present in the tile, tap-major
-  // so one 128-bit load fetches (K+_p, K-_p): [iy*nkx+ix][tap][K+_0, K-_0, ...,
-  // K_mid, pad]
-  __shared__ __align__(16) Acc s_k[4 * 4 * 16 * NSTP];
-  __shared__ double s_var[4 * 4 * G];
-  __shared__ int s_kind[2][4];                             // global axis kinds (y, x)
-  __shared__ float s_lohi[2];
+  __shared__ int released[FT_STAGES];                      // warps done with the slot's plane
+  // mirror-pair stencils of the unit's parts (<= FT_WPARTS) x row kinds of the
+  // tile (interior x kind), double-buffered by unit so staging the next
+  // unit's needs no barrier beyond the unit-start one
+  __shared__ __align__(16) Acc s_w[2][FT_WPARTS * 4 * 16 * NSTP];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = a.H, W = a.W;
   const int64_t P = a.P;
   if (tid == 0) {
-    for (int i = 0; i < FT_STAGES; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < FT_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      released[i] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const uint32_t tile_bytes = FT_SX * FT_SY * 4;
   uint32_t load_seq = 0;                                   // loads issued so far
   const int n_gaps = a.K - 1;
+  const Acc* kpm = reinterpret_cast<const Acc*>(a.kpm);
+  const int kint = a.kmap[AXIS_INTERIOR];                  // compact interior x-kind
+  // warp layout: WX column groups x WY rows per row step
+  constexpr int WX = (FT_TX / COLS) / 32;
+  constexpr int WY = FT_WARPS / WX;
+  const int wx = warp % WX, wy = warp / WX;
+  const int lc = lane + 32 * wx;                           // column group in the tile
 
   for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
     const int chunk_id = u / n_tiles, tile = u - chunk_id * n_tiles;
@@ -215,93 +249,58 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
     const int x0 = tx * FT_TX, y0 = ty * FT_TY;
     const int kb = a.gap0 + chunk_id * chunk, ke = min(a.gap1, kb + chunk);   // gaps [kb, ke)
     const int ty1 = min(H, y0 + FT_TY), tx1 = min(W, x0 + FT_TX);
-    // window kinds present in this tile: interior first, then the border ones
-    int nky = 1, nkx = 1;
-    int kyl[4] = {AXIS_INTERIOR, 0, 0, 0}, kxl[4] = {AXIS_INTERIOR, 0, 0, 0};
+    int nbc = 0, bcol[3] = {0, 0, 0};                      // border columns in this tile
+    int nky = 1, kyl[4] = {AXIS_INTERIOR, 0, 0, 0};        // row kinds: interior first
     {
+      const int cc[3] = {0, W - 2, W - 1};
+      for (int q = 0; q < 3; ++q)
+        if (cc[q] >= x0 && cc[q] < tx1) bcol[nbc++] = cc[q];
       const int rc[3] = {0, H - 2, H - 1};
       for (int q = 0; q < 3; ++q)
         if (rc[q] >= y0 && rc[q] < ty1) kyl[nky++] = axis_kind(rc[q], H);
-      const int cc[3] = {0, W - 2, W - 1};
-      for (int q = 0; q < 3; ++q)
-        if (cc[q] >= x0 && cc[q] < tx1) kxl[nkx++] = axis_kind(cc[q], W);
+    }
+    const int s_first = a.gap_part[kb];
+    const int npu = a.gap_part[ke - 1] - s_first + 1;       // <= FT_WPARTS (host caps chunk)
+    if (npu > FT_WPARTS) __trap();
+    Acc* sw = s_w[((u - blockIdx.x) / gridDim.x) & 1];
+    {
+      const int per_k = 16 * NSTP, n = npu * nky * per_k;
+      for (int i = tid; i < n; i += FT_THREADS) {
+        const int e = i % per_k, q = i / per_k;
+        const int iy = q % nky, pi = q / nky;
+        const int kind = a.kmap[NKIND1 + kyl[iy]] * a.nkx + kint;
+        sw[i] = kpm[((size_t)(s_first + pi) * a.NK + kind) * per_k + e];
+      }
     }
     const uint32_t seq0 = load_seq;
-    int cur_s = -1;                                        // part whose stencils are staged
-    __syncthreads();                                       // previous unit done with the ring
+    const int n_planes = ke - kb + 1;
+    __syncthreads();                                       // ring free, stencils staged
     if (tid == 0) {
-      for (int i = 0; i < 2; ++i) {
+      fence_proxy_async();
+      for (int i = 0; i < min(FT_STAGES, n_planes); ++i) {
         const uint32_t sq = seq0 + i;
         float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
         mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
         tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i);
       }
     }
-    load_seq += 2;
+    load_seq += n_planes;
+    const int gx = x0 + COLS * lc;
+    const bool col_ok = gx < W;
+    const bool xb0 = (gx == 0), xb1 = (gx + COLS > W - 2);  // group holds border columns
     for (int k = kb; k < ke; ++k) {
       const uint32_t sq_a = seq0 + (k - kb), sq_b = sq_a + 1;
-      __syncthreads();                                     // all threads done with gap k-1
-      if (tid == 0 && k + 2 <= ke) {
-        const uint32_t sq = sq_b + 1;
-        float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
-        mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
-        tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, k + 2);
-      }
-      if (k + 2 <= ke) load_seq += 1;
-      // ---- gap constants.  Missing planes j and G-1-j are z-mirrors: their
-      // stencils satisfy wA_j = wB_{G-1-j}, wB_j = wA_{G-1-j} (isotropic
-      // covariance; drift span closed under z -> -z).  With a, b the
-      // mirror-averaged plane-A / plane-B stencils of j, out_j = a*A + b*B =
-      // K+*(A+B) + K-*(A-B) and out_{G-1-j} = K+*(A+B) - K-*(A-B) with
-      // K+- = (a +- b)/2: one symmetric and one antisymmetric 16-tap stencil
-      // per pair instead of four.  Taps outside a clamped border window are 0.
       const int s = a.gap_part[k];
-      const bool reload = (s != cur_s);                    // CTA-uniform
-      cur_s = s;
-      const int n_items = reload ? nky * nkx * (NPAIR + (MID ? 1 : 0)) * 16 : 0;
-      for (int i = tid; i < n_items; i += FT_THREADS) {
-        const int t = i & 15, rest = i >> 4;
-        const int pr = rest % (NPAIR + (MID ? 1 : 0)), kk = rest / (NPAIR + (MID ? 1 : 0));
-        const int iy = kk / nkx, ix = kk - iy * nkx;
-        const int kind = a.kmap[NKIND1 + kyl[iy]] * a.nkx + a.kmap[kxl[ix]];
-        const int pj = a.gap_pattern[k * G + pr], pm = a.gap_pattern[k * G + (G - 1 - pr)];
-        const double* wj = a.weights + (((int64_t)s * a.NP + pj) * a.NK + kind) * WPAD;
-        const double* wm = a.weights + (((int64_t)s * a.NP + pm) * a.NK + kind) * WPAD;
-        const double av = 0.5 * (wj[t] + wm[16 + t]);
-        const double bv = 0.5 * (wj[16 + t] + wm[t]);
-        Acc* dst = s_k + ((size_t)kk * 16 + t) * NSTP;
-        if (pr < NPAIR) {
-          dst[2 * pr] = (Acc)(0.5 * (av + bv));
-          dst[2 * pr + 1] = (Acc)(0.5 * (av - bv));
-        } else {
-          dst[2 * NPAIR] = (Acc)(0.5 * (av + bv));
-        }
-      }
-      for (int i = tid; i < (reload ? nky * nkx * G : 0); i += FT_THREADS) {
-        const int j = i % G, kk = i / G;
-        const int iy = kk / nkx, ix = kk - iy * nkx;
-        const int kind = a.kmap[NKIND1 + kyl[iy]] * a.nkx + a.kmap[kxl[ix]];
-        s_var[i] = a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK + kind];
-      }
-      if (tid == 0 && reload) { s_lohi[0] = (float)a.lohi[2 * s]; s_lohi[1] = (float)a.lohi[2 * s + 1]; }
-      if (k == kb) mbar_wait(&full[sq_a % FT_STAGES], (sq_a / FT_STAGES) & 1);
-      mbar_wait(&full[sq_b % FT_STAGES], (sq_b / FT_STAGES) & 1);
-      if (reload) __syncthreads();                         // staged stencils visible
-      const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
-      const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
+      const Acc* wpart = kpm + (size_t)s * a.NK * 16 * NSTP;
       // the clamp commutes with the f32 rounding (lo, hi are f32 values and
       // rounding is monotone), so it is applied after the conversion
-      const float lo = s_lohi[0], hi = s_lohi[1];
+      const float lo = (float)a.lohi[2 * s], hi = (float)a.lohi[2 * s + 1];
       const int64_t zk = a.known_z[k];
       const bool copy_b = (k == n_gaps - 1);
-      // warp layout: WX column groups x WY rows per row step
-      constexpr int WX = (FT_TX / COLS) / 32;
-      constexpr int WY = FT_WARPS / WX;
-      const int wx = warp % WX, wy = warp / WX;
-      const int lc = lane + 32 * wx;                       // column group in the tile
-      const int gx = x0 + COLS * lc;
-      const bool col_ok = gx < W;
-      const bool xb0 = (gx == 0), xb1 = (gx + COLS > W - 2);  // group holds border columns
+      mbar_wait(&full[sq_a % FT_STAGES], (sq_a / FT_STAGES) & 1);
+      mbar_wait(&full[sq_b % FT_STAGES], (sq_b / FT_STAGES) & 1);
+      const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
+      const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
 #pragma unroll 1
       for (int rs = 0; rs < FT_TY / WY; ++rs) {
         const int r = wy + rs * WY;                        // tile row (warp-uniform)
@@ -311,7 +310,7 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
         const int kyr = axis_kind(gy, H);
         for (int q = 1; q < nky; ++q)
           if (kyl[q] == kyr) iy = q;
-        const Acc* wk = s_k + (size_t)(iy * nkx) * 16 * NSTP;  // x-kind: interior
+        const Acc* wk = sw + (size_t)((s - s_first) * nky + iy) * 16 * NSTP;
         Acc accS[NPAIR > 0 ? NPAIR : 1][COLS], accD[NPAIR > 0 ? NPAIR : 1][COLS], accC[COLS];
 #pragma unroll
         for (int c = 0; c < COLS; ++c) {
@@ -361,11 +360,11 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
             const Acc* wt = wk + t * NSTP;
 #pragma unroll
             for (int p = 0; p < NPAIR; ++p) {
-              const Acc wp = wt[2 * p], wm = wt[2 * p + 1];
+              const P2 w2 = reinterpret_cast<const P2*>(wt)[p];
 #pragma unroll
               for (int c = 0; c < COLS; ++c) {
-                accS[p][c] = fma(wp, S[c + ox + 1], accS[p][c]);
-                accD[p][c] = fma(wm, D[c + ox + 1], accD[p][c]);
+                accS[p][c] = fma(w2.x, S[c + ox + 1], accS[p][c]);
+                accD[p][c] = fma(w2.y, D[c + ox + 1], accD[p][c]);
               }
             }
             if (MID) {
@@ -384,7 +383,6 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
           if (copy_b)
             for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
         }
-        const double* vrow = s_var + (iy * nkx) * G;
 #pragma unroll
         for (int j = 0; j < G; ++j) {
           float o[COLS];
@@ -398,17 +396,21 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
           }
           float* dst = a.out + (zk + 1 + j) * P + pix;
           double* vdst = a.var ? a.var + (zk + 1 + j) * P + pix : nullptr;
+          const double vj =
+              a.var ? a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
+                             a.kmap[NKIND1 + kyr] * a.nkx + kint]
+                    : 0.0;
           if (!xb0 && !xb1) {
             st_cs_cols<COLS>(dst, o);
             if (vdst)
-              for (int c = 0; c < COLS; ++c) vdst[c] = vrow[j];
+              for (int c = 0; c < COLS; ++c) vdst[c] = vj;
           } else {
 #pragma unroll
             for (int c = 0; c < COLS; ++c) {
               const int xx = gx + c;
               if (xx >= 1 && xx <= W - 3) {
                 dst[c] = o[c];
-                if (vdst) vdst[c] = vrow[j];
+                if (vdst) vdst[c] = vj;
               }
             }
           }
@@ -416,21 +418,13 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
       }
       // ---- border columns x in {0, W-2, W-1}: one thread per (row, column),
       // all G planes with the column's window kind, same mirror-pair form
-      if (nkx > 1) {
-        const int rows_in = ty1 - y0, nbc = nkx - 1;
+      if (nbc > 0) {
+        const int rows_in = ty1 - y0;
         for (int idx = tid; idx < rows_in * nbc; idx += FT_THREADS) {
-          const int ic = 1 + idx % nbc, r = idx / nbc;
-          const int gy = y0 + r;
-          int xb = 0;
-          for (int q = 0, seen = 0; q < 3; ++q) {          // ic-th border column in the tile
-            const int cand = q == 0 ? 0 : (q == 1 ? W - 2 : W - 1);
-            if (cand >= x0 && cand < tx1 && ++seen == ic) xb = cand;
-          }
-          int iy = 0;
-          const int kyr = axis_kind(gy, H);
-          for (int q = 1; q < nky; ++q)
-            if (kyl[q] == kyr) iy = q;
-          const Acc* wk = s_k + (size_t)(iy * nkx + ic) * 16 * NSTP;
+          const int ic = idx % nbc, r = idx / nbc;
+          const int gy = y0 + r, xb = bcol[ic];
+          const int kind = a.kmap[NKIND1 + axis_kind(gy, H)] * a.nkx + a.kmap[axis_kind(xb, W)];
+          const Acc* wk = wpart + (size_t)kind * 16 * NSTP;
           Acc aS[NPAIR > 0 ? NPAIR : 1], aD[NPAIR > 0 ? NPAIR : 1], aC = (Acc)0;
           for (int p = 0; p < NPAIR; ++p) { aS[p] = (Acc)0; aD[p] = (Acc)0; }
           const int cx = xb - x0 + 4;
@@ -451,7 +445,6 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
             }
           }
           const int64_t pix = (int64_t)gy * W + xb;
-          const double* vv = s_var + (iy * nkx + ic) * G;
 #pragma unroll
           for (int j = 0; j < G; ++j) {
             Acc t;
@@ -459,7 +452,26 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
             else if (j < NPAIR) t = aS[j] + aD[j];
             else t = aS[G - 1 - j] - aD[G - 1 - j];
             a.out[(zk + 1 + j) * P + pix] = fminf(fmaxf((float)t, lo), hi);
-            if (a.var) a.var[(zk + 1 + j) * P + pix] = vv[j];
+            if (a.var)
+              a.var[(zk + 1 + j) * P + pix] =
+                  a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK + kind];
+          }
+        }
+      }
+      // ---- release plane k; the last warp out refills its slot
+      __syncwarp();
+      if (lane == 0) {
+        const int slot = sq_a % FT_STAGES;
+        __threadfence_block();
+        const int c = atomicAdd(&released[slot], 1);
+        if (c == FT_WARPS - 1) {
+          __threadfence_block();
+          released[slot] = 0;
+          const int kn = k + FT_STAGES;                    // plane of load sq_a + FT_STAGES
+          if (kn <= ke) {
+            fence_proxy_async();
+            mbar_expect_tx(&full[slot], tile_bytes);
+            tma_load_3d(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn);
           }
         }
       }
@@ -518,6 +530,20 @@ static cudaError_t occupancy_t(int* occ) {
   return e;
 }
 
+cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st) {
+  const int n_st = (a.part1 - a.part0) * a.NK * 16;
+  if (n_st <= 0) return cudaSuccess;
+  const int blocks = (n_st + 255) / 256;
+  switch (G) {
+#define VK_CASE(g) \
+  case g: fast_stencil_kernel<g, double><<<blocks, 256, 0, st>>>(a); break;
+    VK_CASE(1) VK_CASE(2) VK_CASE(3) VK_CASE(4) VK_CASE(5) VK_CASE(6) VK_CASE(7) VK_CASE(8)
+#undef VK_CASE
+    default: return cudaErrorNotSupported;
+  }
+  return cudaGetLastError();
+}
+
 template <int G, typename Acc>
 static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
   const size_t smem = fast_smem();
@@ -530,9 +556,12 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   int chunk = std::max(1, (int)((int64_t)n_tiles * n_gaps / ((int64_t)resident * 6)));
   chunk = std::min(std::max(chunk, std::min(4, n_gaps)), n_gaps);
   if (a.chunk > 0) chunk = std::min(a.chunk, n_gaps);
+  if (a.max_chunk > 0) chunk = std::min(chunk, a.max_chunk);
   const int n_chunks = (n_gaps + chunk - 1) / chunk;
   const int n_units = n_tiles * n_chunks;
   const int grid = std::min(n_units, resident);
+  const int n_st = (a.part1 - a.part0) * a.NK * 16;
+  if (n_st > 0) fast_stencil_kernel<G, Acc><<<(n_st + 255) / 256, 256, 0, st>>>(a);
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(fl.tmap);
   predict_fast_kernel<G, Acc><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
   return cudaGetLastError();
@@ -553,7 +582,8 @@ cudaError_t prepare_predict_fast(const PredictArgs& a, FastLaunch* fl) {
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   cudaError_t e = cudaErrorNotSupported;
   const bool f32 = a.accum == 1;
-  switch (a.G) {
+  if (a.accum == 2) e = occupancy_fixed(a.G, &fl->occ);
+  else switch (a.G) {
 #define VK_CASE(g) \
   case g: e = f32 ? occupancy_t<g, float>(&fl->occ) : occupancy_t<g, double>(&fl->occ); break;
     VK_CASE(1) VK_CASE(2) VK_CASE(3) VK_CASE(4) VK_CASE(5) VK_CASE(6) VK_CASE(7) VK_CASE(8)
@@ -568,6 +598,7 @@ cudaError_t prepare_predict_fast(const PredictArgs& a, FastLaunch* fl) {
 }
 
 cudaError_t launch_predict_fast_prepared(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
+  if (a.accum == 2) return launch_predict_fixed(fl.tmap, fl.occ, a, st);
   const bool f32 = a.accum == 1;
   switch (a.G) {
 #define VK_CASE(g) \
