@@ -84,13 +84,20 @@ typedef struct {
 #define VK_FLAG_REDRAW_PAIRS 2    /* redraw the pair tables on every execute
                                      (default: drawn once per plan, they depend
                                      only on geometry and seed)               */
-#define VK_FLAG_OVERLAP 4         /* per-part fit -> solve -> predict chains on
-                                     side streams, so parts whose fit converges
-                                     early start predicting while others still
-                                     fit (default: one launch per stage on the
-                                     caller's stream; measured slower on C4
-                                     because streaming CTAs slow the
-                                     latency-bound fits sharing their SMs)   */
+#define VK_FLAG_OVERLAP 4         /* accepted for compatibility: the per-part
+                                     chain schedule is now the default        */
+#define VK_FLAG_SERIAL 8          /* one launch per stage on the caller's
+                                     stream (per-stage timing).  Default with
+                                     S > 1 on the streaming path: per-part
+                                     fit -> solve -> predict chains on side
+                                     streams, launched breadth-first (all
+                                     fits, then solves, then predicts), so a
+                                     part whose variogram fit converges early
+                                     streams its planes while slower fits are
+                                     still iterating.  Set
+                                     CUDA_DEVICE_MAX_CONNECTIONS >= 32 before
+                                     the CUDA context is created for one
+                                     hardware queue per chain.                */
 
 /* Replaces: the window/stencil setup of fill_missing (kriging.py:485-515)
  * and the partition of SPEC.md:392-400.  Host-side, O(K + H + W). */

@@ -30,6 +30,7 @@ ACCUM_IDS = {"fp64": 0, "fp32": 1, "fixed": 2}
 FLAG_FORCE_GENERIC = 1
 FLAG_REDRAW_PAIRS = 2
 FLAG_OVERLAP = 4
+FLAG_SERIAL = 8
 N_STAGES = 6
 STAGES = ("stats", "pairs", "bins", "fit", "solve", "predict")
 

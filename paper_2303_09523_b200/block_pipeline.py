@@ -59,7 +59,7 @@ class ZPartKriging:
                  n_subparts: int, kind: str = "exponential", drift: str = "linear",
                  accum: str = "fp64", n_bins: int = 15, max_pairs: int = 100_000,
                  seed: int = 0, force_generic: bool = False, fit: bool = True,
-                 redraw_pairs: bool = False, part_len: int = 0, overlap: bool = False):
+                 redraw_pairs: bool = False, part_len: int = 0, overlap: bool = True):
         if factor < 1:
             raise ValueError("factor must be >= 1")
         self.ranges = subpart_ranges(n_known, n_subparts, part_len)   # validates

@@ -19,7 +19,7 @@ __device__ __forceinline__ double wsum(double v) {
 }
 
 #ifdef VK_FIT_PROFILE
-__device__ unsigned long long g_fit_prof[8];   // cycles: jac, svd, trsolve, select, resid, total, nfev, iters
+__device__ unsigned long long g_fit_prof[12];  // cycles: jac, svd, trsolve, select, resid, total, nfev, iters, svd-qr, svd-jacobi, sweeps
 #define VK_PT(v) const long long v = clock64()
 #define VK_PACC(slot, a, b) if (lane == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)((b) - (a)))
 #else
@@ -72,6 +72,7 @@ struct WarpTrf {
   // column), then a one-sided Jacobi SVD of the 3x3 R in registers.  Returns
   // s (descending), V, and uf = U^T f_aug directly (U = Q U_R).
   __device__ void svd_uf(double* a, double fl, double* s, double* V, double* uf) const {
+    VK_PT(t_q0);
     double R[9];
     for (int k = 0; k < 3; ++k) {
       const bool act = lane >= k;
@@ -104,8 +105,21 @@ struct WarpTrf {
     }
     for (int r = 0; r < 3; ++r)
       for (int c = 0; c < r; ++c) R[r * 3 + c] = 0.0;
-    // one-sided Jacobi on the columns of R (3x3, no cross-lane traffic)
-    for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0 : 0.0;
+    VK_PT(t_q1);
+    VK_PACC(8, t_q0, t_q1);
+    // one-sided Jacobi on the columns of R (3x3, no cross-lane traffic),
+    // warm-started from the caller's V (the previous iteration's right singular
+    // vectors: J moves little between TRF iterations, so R V is already nearly
+    // column-orthogonal and one or two sweeps finish it).  V enters orthogonal;
+    // the result is the SVD of R up to column order and signs, as from a cold
+    // start.
+    {
+      double RV[9];
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+          RV[r * 3 + c] = R[r * 3 + 0] * V[0 + c] + R[r * 3 + 1] * V[3 + c] + R[r * 3 + 2] * V[6 + c];
+      for (int i = 0; i < 9; ++i) R[i] = RV[i];
+    }
     for (int sweep = 0; sweep < 60; ++sweep) {
       bool rotated = false;
       for (int p = 0; p < 2; ++p)
@@ -120,12 +134,16 @@ struct WarpTrf {
           // working precision; the trust-region step uses s, V to ~1e-14)
           if (gamma == 0.0 || gamma * gamma <= 1e-30 * (alpha * beta)) continue;
           rotated = true;
-          // tan of the Jacobi angle without forming zeta = (beta-alpha)/(2 gamma):
-          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) = 2 gamma s / (|b-a| + sqrt((b-a)^2 + 4 gamma^2))
+          // the smaller Jacobi angle (|theta| <= pi/4) from its double angle:
+          // cos 2t = |b-a| / h, sin 2t = 2 gamma sign(b-a) / h, h = sqrt((b-a)^2 + 4 gamma^2);
+          // c = sqrt((1 + cos 2t) / 2), s = sin 2t / (2 c) -- two rsqrt, no
+          // division or sqrt on the dependent chain (x in [1/2, 1])
           const double bma = beta - alpha;
           const double sg = (bma >= 0.0) ? 1.0 : -1.0;
-          const double t = (2.0 * gamma * sg) / (fabs(bma) + sqrt(bma * bma + 4.0 * gamma * gamma));
-          const double c = rsqrt(1.0 + t * t), sn = c * t;
+          const double ih = rsqrt(bma * bma + 4.0 * gamma * gamma);
+          const double xh = 0.5 + 0.5 * (fabs(bma) * ih);
+          const double rx = rsqrt(xh);
+          const double c = xh * rx, sn = (gamma * sg) * ih * rx;
           for (int r = 0; r < 3; ++r) {
             const double rp = R[r * 3 + p], rq = R[r * 3 + q];
             R[r * 3 + p] = c * rp - sn * rq;
@@ -135,12 +153,19 @@ struct WarpTrf {
             V[r * 3 + q] = sn * vp + c * vq;
           }
         }
+#ifdef VK_FIT_PROFILE
+      if (lane == 0) atomicAdd(&g_fit_prof[10], 1ull);
+#endif
       if (!rotated) break;
     }
+    VK_PT(t_q2);
+    VK_PACC(9, t_q1, t_q2);
     double sv[3], uq[3];
     for (int j = 0; j < 3; ++j) {
-      sv[j] = sqrt(R[0 + j] * R[0 + j] + R[3 + j] * R[3 + j] + R[6 + j] * R[6 + j]);
-      uq[j] = sv[j] > 0.0 ? (R[0 + j] * qf[0] + R[3 + j] * qf[1] + R[6 + j] * qf[2]) / sv[j] : 0.0;
+      const double n2 = R[0 + j] * R[0 + j] + R[3 + j] * R[3 + j] + R[6 + j] * R[6 + j];
+      const double rn = n2 > 0.0 ? rsqrt(n2) : 0.0;
+      sv[j] = n2 * rn;
+      uq[j] = (R[0 + j] * qf[0] + R[3 + j] * qf[1] + R[6 + j] * qf[2]) * rn;
     }
     int order[3] = {0, 1, 2};
     for (int x = 0; x < 3; ++x)
@@ -290,6 +315,7 @@ struct WarpTrf {
       if (Delta == 0) Delta = 1.0;
     }
     double alpha = 0.0;
+    double V[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};   // right singular vectors, carried across iterations
     int status = -100;
     int iteration = 0;
     double x_new[3], f_new = 0.0, cost_new = 0.0, g_norm = 0.0;
@@ -313,7 +339,7 @@ struct WarpTrf {
         const int dr = lane - m;   // diagonal rows m..m+2
         for (int c = 0; c < 3; ++c) a[c] = (dr >= 0 && dr < 3 && dr == c) ? sqrt(diag_h[c]) : 0.0;
       }
-      double sv[3], V[9], uf[3];
+      double sv[3], uf[3];
       VK_PT(t_s0);
       svd_uf(a, row ? f : 0.0, sv, V, uf);
       VK_PT(t_s1);

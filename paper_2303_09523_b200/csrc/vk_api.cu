@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -81,6 +82,7 @@ struct vk_plan {
   uint32_t* d_fxb = nullptr;           // fixed path tables
   float *d_fxc = nullptr, *d_fxq = nullptr;
   int max_chunk = 0;                  // fast path: a run of this many gaps spans <= 4 parts
+  int fit_reserve = 160 * 1024;       // overlapped schedule: smem a fit CTA reserves on its SM
   int32_t *d_part_status = nullptr, *d_sys_status = nullptr;
   std::vector<PairTable> tables;
   PairTable* d_tables = nullptr;
@@ -327,7 +329,11 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
     }
     p->max_chunk = 3 * std::max(1, min_len) + 1;
   }
-  if ((d->flags & VK_FLAG_OVERLAP) && S > 1) {
+  if (const char* e = std::getenv("VK_FIT_RESERVE")) p->fit_reserve = std::atoi(e);   // tuning
+  // per-part chains are the default schedule whenever there is more than one
+  // part on the streaming path; VK_FLAG_SERIAL keeps one stream (per-stage
+  // timing, debugging)
+  if (!(d->flags & VK_FLAG_SERIAL) && S > 1 && g.fast) {
     VK_TRY(cudaEventCreateWithFlags(&p->ev_kfork, cudaEventDisableTiming));
     for (int i = 0; i < std::min(S, vk_plan::NCH); ++i) {
       VK_TRY(cudaStreamCreateWithFlags(&p->chain[i], cudaStreamNonBlocking));
@@ -499,25 +505,33 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(cudaEventRecord(p->ev_kfork, st));
     const int nch = std::min(S, vk_plan::NCH);
     for (int c = 0; c < nch; ++c) VK_CUDA(cudaStreamWaitEvent(p->chain[c], p->ev_kfork, 0));
+    // breadth-first launch order (all fits, then all solves, then all
+    // predicts): a chain's solve waits on its fit, and a waiting kernel at
+    // the head of a hardware work queue would block the fits queued behind it
     for (int s = 0; s < S; ++s) {
-      cudaStream_t cs = p->chain[s % nch];
       FitArgs f1 = fa;
       f1.part0 = s;
       f1.n_parts = 1;
-      f1.reserve_smem = 160 * 1024;           // one fit per SM, no streaming CTA beside it
-      VK_CUDA(launch_fit(f1, cs));
+      f1.reserve_smem = p->fit_reserve;
+      VK_CUDA(launch_fit(f1, p->chain[s % nch]));
+      ++kernels;
+    }
+    for (int s = 0; s < S; ++s) {
       SolveArgs s1 = sa;
       s1.sys0 = p->sys_begin[s];
       s1.n_sys = p->sys_begin[s + 1] - p->sys_begin[s];
-      VK_CUDA(launch_solve(s1, cs));
+      VK_CUDA(launch_solve(s1, p->chain[s % nch]));
+      kernels += (s1.n_sys > 0);
+    }
+    for (int s = 0; s < S; ++s) {
       PredictArgs p1 = pa;
       p1.gap0 = p->gap_begin[s];
       p1.gap1 = p->gap_begin[s + 1];
       p1.chunk = p1.gap1 - p1.gap0;           // one unit = a tile over the part's gaps
       p1.part0 = s;
       p1.part1 = s + 1;
-      VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, cs));
-      kernels += 3 + (s1.n_sys > 0);
+      VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, p->chain[s % nch]));
+      kernels += 2;
     }
     for (int c = 0; c < nch; ++c) {
       VK_CUDA(cudaEventRecord(p->ev_kjoin[c], p->chain[c]));

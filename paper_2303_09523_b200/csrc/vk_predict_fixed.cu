@@ -72,26 +72,6 @@ __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], ui
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// packed fp32x2 arithmetic (FFMA2 / FADD2), round-to-nearest like the scalar ops
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{\n.reg .b64 ra, rb, rc, rd;\n"
-      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
-      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-  float2 d;
-  asm("{\n.reg .b64 ra, rb, rd;\n"
-      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\n"
-      "add.rn.f32x2 rd, ra, rb;\nmov.b64 {%0, %1}, rd;\n}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-
 // volume-wide quantisation range from the per-part known ranges
 __device__ __forceinline__ void quant_range(const PredictArgs& a, double* L, double* R) {
   double lo = a.lohi[0], hi = a.lohi[1];
@@ -266,9 +246,8 @@ __global__ void __launch_bounds__(FX_THREADS, 2)
         const float4* csrc = reinterpret_cast<const float4*>(a.fxc);
         const int kin = a.kmap[NKIND1 + AXIS_INTERIOR] * a.nkx + kint;   // interior kind
         const int j0 = 2 * t, j1 = 2 * t + 1;              // C columns of this lane
-        int kcur = -1;
         uint32_t bf[8];
-        float2 chi, clo, cg, ch;
+        float chi0, chi1, clo0, clo1, cg, ch;              // constants of planes 2t, 2t+1
         double vj0 = 0.0, vj1 = 0.0;
         auto load_kind = [&](int kind) {
           const size_t sk = (size_t)s * a.NK + kind;
@@ -277,15 +256,24 @@ __global__ void __launch_bounds__(FX_THREADS, 2)
           bf[0] = b01.x; bf[1] = b01.y; bf[2] = b01.z; bf[3] = b01.w;
           bf[4] = b23.x; bf[5] = b23.y; bf[6] = b23.z; bf[7] = b23.w;
           const float4 e0 = csrc[sk * 8 + j0], e1 = csrc[sk * 8 + j1];
-          chi = make_float2(e0.x, e1.x);
-          clo = make_float2(e0.y, e1.y);
-          cg = make_float2(e0.z, e0.z);
-          ch = make_float2(e0.w, e0.w);
+          chi0 = e0.x; chi1 = e1.x;
+          clo0 = e0.y; clo1 = e1.y;
+          cg = e0.z;
+          ch = e0.w;
           if (VAR) {
             if (j0 < G) vj0 = a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j0]) * a.NK + kind];
             if (j1 < G) vj1 = a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j1]) * a.NK + kind];
           }
         };
+        load_kind(kin);
+        int kcur = kin;
+        // rows that need attention: border rows (own window kind), the row
+        // after the top border row (back to interior), rows past the volume
+        uint32_t special = 0;
+        for (int r = 0; r < FX_TY; ++r) {
+          const int y = y0 + r;
+          if (y >= H || y == 0 || y == 1 || y >= H - 2) special |= 1u << r;
+        }
         // byte-image columns of this lane's A registers: (x, plane A), (x+8, A),
         // (x, B), (x+8, B) with x = xs + g and tap column ox = t - 1
         const int cx = xs - x0 + g + t + 3;
@@ -294,76 +282,90 @@ __global__ void __launch_bounds__(FX_THREADS, 2)
         const int xv0 = xs + g, xv1 = xs + g + 8;          // voxels of C rows g, g + 8
         const bool okx0 = xv0 >= 1 && xv0 <= W - 3, okx1 = xv1 >= 1 && xv1 <= W - 3;
         const bool m0 = j0 < G && okx0, m1 = j1 < G && okx0, m2 = j0 < G && okx1, m3 = j1 < G && okx1;
-        // 32-bit element offsets from the gap's first missing plane
-        float* obase = a.out + (zk + 1) * P;
-        double* vbase = VAR ? a.var + (zk + 1) * P : nullptr;
-        uint32_t o0 = (uint32_t)(j0 * P + (int64_t)y0 * W + xv0);
-        uint32_t o1 = o0 + (uint32_t)P, o2 = o0 + 8u, o3 = o1 + 8u;
-        uint32_t wlo[3][4], whi[3][4];
-#pragma unroll
-        for (int sl = 0; sl < 3; ++sl)
-#pragma unroll
-          for (int m = 0; m < 4; ++m) whi[sl][m] = col[m][sl * FX_IMG_WORDS];
-#pragma unroll 1
-        for (int r4 = 0; r4 < FX_TY / 4; ++r4) {
-#pragma unroll
-          for (int sl = 0; sl < 3; ++sl)
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-              wlo[sl][m] = whi[sl][m];
-              whi[sl][m] = col[m][sl * FX_IMG_WORDS + r4 + 1];
-            }
-#pragma unroll
-          for (int sh = 0; sh < 4; ++sh) {
-            const int y = y0 + 4 * r4 + sh;
-            if (y >= H) break;                             // warp-uniform
-            const int kind_y = (y == 0 || y >= H - 2) ? a.kmap[NKIND1 + axis_kind(y, H)] * a.nkx + kint : kin;
-            if (kind_y != kcur) {                          // first row / border rows (warp-uniform)
+        // output pointers of (plane 2t, voxel xv0) and (plane 2t+1, voxel xv0);
+        // voxel xv1 = xv0 + 8 is an immediate offset
+        float* p0 = a.out + (zk + 1 + j0) * P + (int64_t)y0 * W + xv0;
+        float* p1 = p0 + P;
+        double* q0 = VAR ? a.var + (zk + 1 + j0) * P + (int64_t)y0 * W + xv0 : nullptr;
+        double* q1 = VAR ? q0 + P : nullptr;
+        bool done = false;
+        // one row: A fragments from the sliding byte words, 9 MMAs, epilogue
+        auto row = [&](const uint32_t (&wl)[3][4], const uint32_t (&wh)[3][4], const int r, const int sh) {
+          if (special & (1u << r)) {                       // warp-uniform
+            const int y = y0 + r;
+            if (y >= H) { done = true; return; }
+            const int kind_y = a.kmap[NKIND1 + axis_kind(y, H)] * a.nkx + kint;
+            if (kind_y != kcur) {
               kcur = kind_y;
               load_kind(kcur);
             }
-            uint32_t A[3][4];
+          }
+          uint32_t A[3][4];
+#pragma unroll
+          for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              A[sl][m] = sh == 0 ? wl[sl][m] : __byte_perm(wl[sl][m], wh[sl][m], 0x3210 + 0x1111 * sh);
+          int acc[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[q][c] = 0;
+          // group a + b = 2 .. 5 -> acc[a + b - 2]
+          mma_u8u8(acc[0], A[0], bf[4], bf[5]);            // (0, 2)
+          mma_u8u8(acc[0], A[1], bf[2], bf[3]);            // (1, 1)
+          mma_u8u8(acc[0], A[2], bf[0], bf[1]);            // (2, 0)
+          mma_u8s8(acc[1], A[0], bf[6], bf[7]);            // (0, 3)
+          mma_u8u8(acc[1], A[1], bf[4], bf[5]);            // (1, 2)
+          mma_u8u8(acc[1], A[2], bf[2], bf[3]);            // (2, 1)
+          mma_u8s8(acc[2], A[1], bf[6], bf[7]);            // (1, 3)
+          mma_u8u8(acc[2], A[2], bf[4], bf[5]);            // (2, 2)
+          mma_u8s8(acc[3], A[2], bf[6], bf[7]);            // (2, 3)
+          // C fragment: (c0, c1) -> voxel xv0, planes (2t, 2t+1); (c2, c3) -> xv1.
+          // T = 2^32 (256 P5 + P4) + 2^16 (256 P3 + P2); out = c0 + step 2^-P T
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ga = acc[3][2 * h] * 256 + acc[2][2 * h], gb = acc[3][2 * h + 1] * 256 + acc[2][2 * h + 1];
+            const int ha = acc[1][2 * h] * 256 + acc[0][2 * h], hb = acc[1][2 * h + 1] * 256 + acc[0][2 * h + 1];
+            const float vx = fminf(fmaxf(fmaf((float)ga, cg, fmaf((float)ha, ch, clo0)) + chi0, lo), hi);
+            const float vy = fminf(fmaxf(fmaf((float)gb, cg, fmaf((float)hb, ch, clo1)) + chi1, lo), hi);
+            const bool ma = h ? m2 : m0, mb = h ? m3 : m1;
+            if (ma) st_cs_f32(p0 + 8 * h, vx);
+            if (mb) st_cs_f32(p1 + 8 * h, vy);
+            if (VAR) {
+              if (ma) q0[8 * h] = vj0;
+              if (mb) q1[8 * h] = vj1;
+            }
+          }
+          p0 += W;
+          p1 += W;
+          if (VAR) { q0 += W; q1 += W; }
+        };
+        // words (rows 4i .. 4i+3) of the four columns in the three byte images;
+        // ping-pong between wa and wb so no register copies are needed
+        uint32_t wa[3][4], wb[3][4];
+#pragma unroll
+        for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            wa[sl][m] = col[m][sl * FX_IMG_WORDS];
+            wb[sl][m] = col[m][sl * FX_IMG_WORDS + 1];
+          }
+#pragma unroll 1
+        for (int r8 = 0; r8 < FX_TY / 8 && !done; ++r8) {
+#pragma unroll
+          for (int sh = 0; sh < 4 && !done; ++sh) row(wa, wb, 8 * r8 + sh, sh);
+#pragma unroll
+          for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) wa[sl][m] = col[m][sl * FX_IMG_WORDS + 2 * r8 + 2];
+#pragma unroll
+          for (int sh = 0; sh < 4 && !done; ++sh) row(wb, wa, 8 * r8 + 4 + sh, sh);
+          if (r8 + 1 < FX_TY / 8) {
 #pragma unroll
             for (int sl = 0; sl < 3; ++sl)
 #pragma unroll
-              for (int m = 0; m < 4; ++m)
-                A[sl][m] = sh == 0 ? wlo[sl][m] : __byte_perm(wlo[sl][m], whi[sl][m], 0x3210 + 0x1111 * sh);
-            int acc[4][4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-              for (int c = 0; c < 4; ++c) acc[q][c] = 0;
-            // group a + b = 2 .. 5 -> acc[a + b - 2]
-            mma_u8u8(acc[0], A[0], bf[4], bf[5]);          // (0, 2)
-            mma_u8u8(acc[0], A[1], bf[2], bf[3]);          // (1, 1)
-            mma_u8u8(acc[0], A[2], bf[0], bf[1]);          // (2, 0)
-            mma_u8s8(acc[1], A[0], bf[6], bf[7]);          // (0, 3)
-            mma_u8u8(acc[1], A[1], bf[4], bf[5]);          // (1, 2)
-            mma_u8u8(acc[1], A[2], bf[2], bf[3]);          // (2, 1)
-            mma_u8s8(acc[2], A[1], bf[6], bf[7]);          // (1, 3)
-            mma_u8u8(acc[2], A[2], bf[4], bf[5]);          // (2, 2)
-            mma_u8s8(acc[3], A[2], bf[6], bf[7]);          // (2, 3)
-            // C fragment: (c0, c1) -> voxel xv0, planes (2t, 2t+1); (c2, c3) -> xv1.
-            // T = 2^32 (256 P5 + P4) + 2^16 (256 P3 + P2); out = c0 + step 2^-P T
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int ga = acc[3][2 * h] * 256 + acc[2][2 * h], gb = acc[3][2 * h + 1] * 256 + acc[2][2 * h + 1];
-              const int ha = acc[1][2 * h] * 256 + acc[0][2 * h], hb = acc[1][2 * h + 1] * 256 + acc[0][2 * h + 1];
-              float2 v = ffma2(make_float2((float)ha, (float)hb), ch, clo);
-              v = ffma2(make_float2((float)ga, (float)gb), cg, v);
-              v = fadd2(v, chi);
-              v.x = fminf(fmaxf(v.x, lo), hi);
-              v.y = fminf(fmaxf(v.y, lo), hi);
-              const uint32_t oa = h ? o2 : o0, ob = h ? o3 : o1;
-              const bool ma = h ? m2 : m0, mb = h ? m3 : m1;
-              if (ma) st_cs_f32(obase + oa, v.x);
-              if (mb) st_cs_f32(obase + ob, v.y);
-              if (VAR) {
-                if (ma) vbase[oa] = vj0;
-                if (mb) vbase[ob] = vj1;
-              }
-            }
-            o0 += (uint32_t)W; o1 += (uint32_t)W; o2 += (uint32_t)W; o3 += (uint32_t)W;
+              for (int m = 0; m < 4; ++m) wb[sl][m] = col[m][sl * FX_IMG_WORDS + 2 * r8 + 3];
           }
         }
       }

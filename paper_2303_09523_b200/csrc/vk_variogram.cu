@@ -455,9 +455,9 @@ __global__ void __launch_bounds__(32) fit_scalar_kernel(FitArgs a) {
 
 #ifdef VK_FIT_PROFILE
 extern "C" int vk_debug_fit_profile(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, g_fit_prof, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out, g_fit_prof, sizeof(unsigned long long) * 12);
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_fit_prof, z, sizeof(z));
   }
   return 0;

@@ -90,7 +90,7 @@ class KrigingPlan:
     def __init__(self, height, width, depth, known_z, n_subparts=1,
                  kind="exponential", drift="linear", accum="fp64", fit=True,
                  n_bins=15, max_pairs=100_000, seed=0, force_generic=False,
-                 part_len=0, redraw_pairs=False, overlap=False):
+                 part_len=0, redraw_pairs=False, overlap=True):
         if callable(drift):
             raise DeviceUnsupported("a callable drift cannot cross the C ABI; "
                                     "use 'linear' or 'constant'")
@@ -115,7 +115,7 @@ class KrigingPlan:
             int(n_bins), int(max_pairs), int(seed), int(bool(fit)),
             (_lib.FLAG_FORCE_GENERIC if force_generic else 0)
             | (_lib.FLAG_REDRAW_PAIRS if redraw_pairs else 0)
-            | (_lib.FLAG_OVERLAP if overlap else 0), int(part_len))
+            | (0 if overlap else _lib.FLAG_SERIAL), int(part_len))
         handle = C.c_void_p()
         raise_for_status(self.lib.vk_plan_create(C.byref(desc), C.byref(handle)))
         self._h = handle

@@ -160,3 +160,26 @@ def test_fit_variogram_samples(cuda):
         exp = O.fit_variogram((c, v))
         assert abs(got.sill - exp.sill) <= 1e-4 * exp.sill, (got, exp)
         assert abs(got.range_len - exp.range_len) <= 1e-3 * exp.range_len, (got, exp)
+
+
+@pytest.mark.parametrize("accum", ["fp64", "fixed"])
+def test_chained_schedule_matches_serial(cuda, accum):
+    """The default per-part fit -> solve -> predict chains (side streams,
+    breadth-first launch) compute exactly what the serial schedule does."""
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("spine", 64, 128, 33, 4, n_subparts=8, seed=21)
+    ks = torch.from_numpy(known_slices(cfg)).cuda()
+    res = []
+    for overlap in (True, False):
+        zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts,
+                          accum=accum, overlap=overlap)
+        out, var = zk.run(ks, return_variance=True)
+        models, lohi = zk.finish()
+        res.append((out, var, np.array([[m.nugget, m.sill, m.range_len] for m in models]), lohi))
+        if overlap:
+            assert zk.plan.info["kernels_per_execute"] > 3 * cfg.n_subparts
+    (o1, v1, m1, l1), (o2, v2, m2, l2) = res
+    assert torch.equal(o1, o2) and torch.equal(v1, v2)
+    assert np.array_equal(m1, m2) and np.array_equal(l1, l2)

@@ -17,14 +17,15 @@ zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts
 lib = _lib.load()
 fn = lib.vk_debug_fit_profile
 fn.argtypes = [C.c_void_p, C.c_int]
-buf = np.zeros(8, np.uint64)
+buf = np.zeros(12, np.uint64)
 zk.run(ks)
 zk.finish()
 fn(buf.ctypes.data, 1)
 zk.run(ks)
 zk.finish()
 fn(buf.ctypes.data, 1)
-names = ["jac+grad", "svd_uf", "trust_region", "select_step", "resid", "total", "nfev", "iters"]
+names = ["jac+grad", "svd_uf", "trust_region", "select_step", "resid", "total", "nfev", "iters",
+         "svd: qr", "svd: jacobi", "jacobi sweeps"]
 S = cfg.n_subparts
 for n, v in zip(names, buf):
     print(f"{n:14s} {int(v) / S:12.0f} per part")
