@@ -156,18 +156,36 @@ __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
 // one antisymmetric 16-tap stencil per pair instead of four.  Layout
 // [s][kind][tap][K+_0, K-_0, ..., K_mid, pad] so one 128-bit load fetches a
 // pair.  Taps outside a clamped border window are 0 in the solved weights.
+// Per-tap layout of the mirror-pair stencils.  fp64 (DFMA, one stencil per
+// instruction): [K+_0, K-_0, K+_1, K-_1, ..., K_mid, pad].  fp32 (FFMA2, two
+// stencils per instruction against one broadcast S or D value): the symmetric
+// stencils together, then the antisymmetric ones, each run padded to a pair:
+// [K+_0, K+_1, ..., K+_{n-1}, K_mid, (pad) | K-_0, ..., K-_{n-1}, (pad)].
+template <int G, typename Acc>
+struct StLayout {
+  static constexpr int NPAIR = G / 2;
+  static constexpr bool MID = (G & 1) != 0;
+  static constexpr bool PAIRED = std::is_same<Acc, float>::value;
+  static constexpr int NPP = (NPAIR + (MID ? 1 : 0) + 1) & ~1;   // paired: symmetric run
+  static constexpr int NMP = (NPAIR + 1) & ~1;                   // paired: antisymmetric run
+  static constexpr int NSTP = PAIRED ? NPP + NMP : ((2 * NPAIR + (MID ? 1 : 0) + 1) & ~1);
+  static __host__ __device__ constexpr int plus(int p) { return PAIRED ? p : 2 * p; }
+  static __host__ __device__ constexpr int minus(int p) { return PAIRED ? NPP + p : 2 * p + 1; }
+  static __host__ __device__ constexpr int mid() { return PAIRED ? NPAIR : 2 * NPAIR; }
+};
+
 template <int G, typename Acc>
 __global__ void __launch_bounds__(256) fast_stencil_kernel(PredictArgs a) {
-  constexpr int NPAIR = G / 2;
-  constexpr bool MID = (G & 1) != 0;
-  constexpr int NST = 2 * NPAIR + (MID ? 1 : 0);
-  constexpr int NSTP = (NST + 1) & ~1;
+  using L = StLayout<G, Acc>;
+  constexpr int NPAIR = L::NPAIR, NSTP = L::NSTP;
+  constexpr bool MID = L::MID;
   const int per_part = a.NK * 16;
   const int n = (a.part1 - a.part0) * per_part;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int s = a.part0 + i / per_part, r = i - (i / per_part) * per_part;
     const int kind = r >> 4, t = r & 15;
     Acc* dst = reinterpret_cast<Acc*>(a.kpm) + (((size_t)s * a.NK + kind) * 16 + t) * NSTP;
+    for (int q = 0; q < NSTP; ++q) dst[q] = (Acc)0;
     // patterns are identical for every gap on the fast path (each missing
     // plane reads exactly its two bracketing known planes)
     for (int pr = 0; pr < NPAIR + (MID ? 1 : 0); ++pr) {
@@ -177,14 +195,26 @@ __global__ void __launch_bounds__(256) fast_stencil_kernel(PredictArgs a) {
       const double av = 0.5 * (wj[t] + wm[16 + t]);
       const double bv = 0.5 * (wj[16 + t] + wm[t]);
       if (pr < NPAIR) {
-        dst[2 * pr] = (Acc)(0.5 * (av + bv));
-        dst[2 * pr + 1] = (Acc)(0.5 * (av - bv));
+        dst[L::plus(pr)] = (Acc)(0.5 * (av + bv));
+        dst[L::minus(pr)] = (Acc)(0.5 * (av - bv));
       } else {
-        dst[2 * NPAIR] = (Acc)(0.5 * (av + bv));
+        dst[L::mid()] = (Acc)(0.5 * (av + bv));
       }
     }
-    if (NSTP > NST) dst[NST] = (Acc)0;
   }
+}
+
+// packed fp32x2 FMA (FFMA2) on 64-bit register pairs; a pair built from one
+// value twice becomes the instruction's broadcast operand
+__device__ __forceinline__ uint64_t f2pack(float x, float y) {
+  return (uint64_t)__float_as_uint(x) | ((uint64_t)__float_as_uint(y) << 32);
+}
+__device__ __forceinline__ float f2lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
 }
 
 template <typename Acc>
@@ -205,14 +235,14 @@ struct Pair2<float> {
 // k + FT_STAGES.  Warps therefore drift apart by up to a few gaps, so the
 // FP64 pipe of an SM sub-partition sees a mix of DFMA-heavy and
 // load/convert/store phases instead of all warps in lock step.
-template <int G, typename Acc, int COLS = VK_FT_COLS>
+template <int G, typename Acc, bool VAR, int COLS = VK_FT_COLS>
 __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
     predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
                         int n_tiles, int chunk, int n_units) {
-  constexpr int NPAIR = G / 2;
-  constexpr bool MID = (G & 1) != 0;
-  constexpr int NST = 2 * NPAIR + (MID ? 1 : 0);          // stencils per kind
-  constexpr int NSTP = (NST + 1) & ~1;                     // padded: 16-byte aligned taps
+  using L = StLayout<G, Acc>;
+  constexpr int NPAIR = L::NPAIR;
+  constexpr bool MID = L::MID;
+  constexpr int NSTP = L::NSTP;                            // padded: 16-byte aligned taps
   using P2 = typename Pair2<Acc>::T;
   extern __shared__ __align__(128) float ring[];           // FT_STAGES x FT_BUF_FLOATS
   __shared__ __align__(8) uint64_t full[FT_STAGES];
@@ -311,12 +341,19 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
         for (int q = 1; q < nky; ++q)
           if (kyl[q] == kyr) iy = q;
         const Acc* wk = sw + (size_t)((s - s_first) * nky + iy) * 16 * NSTP;
+        constexpr bool PAIRED = L::PAIRED;
+        constexpr int QP = PAIRED ? L::NPP / 2 : 1, QM = (PAIRED && L::NMP > 0) ? L::NMP / 2 : 1;
         Acc accS[NPAIR > 0 ? NPAIR : 1][COLS], accD[NPAIR > 0 ? NPAIR : 1][COLS], accC[COLS];
+        uint64_t aP[QP][COLS], aM[QM][COLS];               // fp32: stencil pairs (FFMA2)
 #pragma unroll
         for (int c = 0; c < COLS; ++c) {
           accC[c] = (Acc)0;
 #pragma unroll
           for (int p = 0; p < NPAIR; ++p) { accS[p][c] = (Acc)0; accD[p][c] = (Acc)0; }
+#pragma unroll
+          for (int q = 0; q < QP; ++q) aP[q][c] = 0;
+#pragma unroll
+          for (int q = 0; q < QM; ++q) aM[q][c] = 0;
         }
         float selfA[COLS], selfB[COLS];
 #pragma unroll
@@ -358,19 +395,37 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
           for (int ox = -1; ox <= 2; ++ox) {
             const int t = (oy + 1) * 4 + (ox + 1);
             const Acc* wt = wk + t * NSTP;
+            if constexpr (PAIRED) {
+              // two stencils per FFMA2 against the broadcast S (or D) value
 #pragma unroll
-            for (int p = 0; p < NPAIR; ++p) {
-              const P2 w2 = reinterpret_cast<const P2*>(wt)[p];
+              for (int q = 0; q < L::NPP / 2; ++q) {
+                const uint64_t w2 = reinterpret_cast<const uint64_t*>(wt)[q];
 #pragma unroll
-              for (int c = 0; c < COLS; ++c) {
-                accS[p][c] = fma(w2.x, S[c + ox + 1], accS[p][c]);
-                accD[p][c] = fma(w2.y, D[c + ox + 1], accD[p][c]);
+                for (int c = 0; c < COLS; ++c)
+                  aP[q][c] = f2fma(w2, f2pack(S[c + ox + 1], S[c + ox + 1]), aP[q][c]);
               }
-            }
-            if (MID) {
-              const Acc wc = wt[2 * NPAIR];
 #pragma unroll
-              for (int c = 0; c < COLS; ++c) accC[c] = fma(wc, S[c + ox + 1], accC[c]);
+              for (int q = 0; q < L::NMP / 2; ++q) {
+                const uint64_t w2 = reinterpret_cast<const uint64_t*>(wt + L::NPP)[q];
+#pragma unroll
+                for (int c = 0; c < COLS; ++c)
+                  aM[q][c] = f2fma(w2, f2pack(D[c + ox + 1], D[c + ox + 1]), aM[q][c]);
+              }
+            } else {
+#pragma unroll
+              for (int p = 0; p < NPAIR; ++p) {
+                const P2 w2 = reinterpret_cast<const P2*>(wt)[p];
+#pragma unroll
+                for (int c = 0; c < COLS; ++c) {
+                  accS[p][c] = fma(w2.x, S[c + ox + 1], accS[p][c]);
+                  accD[p][c] = fma(w2.y, D[c + ox + 1], accD[p][c]);
+                }
+              }
+              if (MID) {
+                const Acc wc = wt[2 * NPAIR];
+#pragma unroll
+                for (int c = 0; c < COLS; ++c) accC[c] = fma(wc, S[c + ox + 1], accC[c]);
+              }
             }
           }
         }
@@ -378,7 +433,7 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
         // known planes pass through bit-exactly (kriging.py:481)
         st_cs_cols<COLS>(a.out + zk * P + pix, selfA);
         if (copy_b) st_cs_cols<COLS>(a.out + (zk + G + 1) * P + pix, selfB);
-        if (a.var) {
+        if (VAR) {
           for (int c = 0; c < COLS; ++c) a.var[zk * P + pix + c] = 0.0;
           if (copy_b)
             for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
@@ -389,20 +444,28 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
 #pragma unroll
           for (int c = 0; c < COLS; ++c) {
             Acc t;
-            if (MID && j == NPAIR) t = accC[c];
-            else if (j < NPAIR) t = accS[j][c] + accD[j][c];
-            else t = accS[G - 1 - j][c] - accD[G - 1 - j][c];
+            if constexpr (PAIRED) {
+              auto pv = [&](int i) { return (i & 1) ? f2hi(aP[i >> 1][c]) : f2lo(aP[i >> 1][c]); };
+              auto mv = [&](int i) { return (i & 1) ? f2hi(aM[i >> 1][c]) : f2lo(aM[i >> 1][c]); };
+              if (MID && j == NPAIR) t = pv(NPAIR);
+              else if (j < NPAIR) t = pv(j) + mv(j);
+              else t = pv(G - 1 - j) - mv(G - 1 - j);
+            } else {
+              if (MID && j == NPAIR) t = accC[c];
+              else if (j < NPAIR) t = accS[j][c] + accD[j][c];
+              else t = accS[G - 1 - j][c] - accD[G - 1 - j][c];
+            }
             o[c] = fminf(fmaxf((float)t, lo), hi);
           }
           float* dst = a.out + (zk + 1 + j) * P + pix;
-          double* vdst = a.var ? a.var + (zk + 1 + j) * P + pix : nullptr;
+          double* vdst = VAR ? a.var + (zk + 1 + j) * P + pix : nullptr;
           const double vj =
-              a.var ? a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
+              VAR ? a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
                              a.kmap[NKIND1 + kyr] * a.nkx + kint]
                     : 0.0;
           if (!xb0 && !xb1) {
             st_cs_cols<COLS>(dst, o);
-            if (vdst)
+            if (VAR)
               for (int c = 0; c < COLS; ++c) vdst[c] = vj;
           } else {
 #pragma unroll
@@ -410,7 +473,7 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
               const int xx = gx + c;
               if (xx >= 1 && xx <= W - 3) {
                 dst[c] = o[c];
-                if (vdst) vdst[c] = vj;
+                if (VAR) vdst[c] = vj;
               }
             }
           }
@@ -438,10 +501,10 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
               const Acc Sv = x + y, Dv = x - y;
 #pragma unroll
               for (int p = 0; p < NPAIR; ++p) {
-                aS[p] = fma(wk[t * NSTP + 2 * p], Sv, aS[p]);
-                aD[p] = fma(wk[t * NSTP + 2 * p + 1], Dv, aD[p]);
+                aS[p] = fma(wk[t * NSTP + L::plus(p)], Sv, aS[p]);
+                aD[p] = fma(wk[t * NSTP + L::minus(p)], Dv, aD[p]);
               }
-              if (MID) aC = fma(wk[t * NSTP + 2 * NPAIR], Sv, aC);
+              if (MID) aC = fma(wk[t * NSTP + L::mid()], Sv, aC);
             }
           }
           const int64_t pix = (int64_t)gy * W + xb;
@@ -452,7 +515,7 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
             else if (j < NPAIR) t = aS[j] + aD[j];
             else t = aS[G - 1 - j] - aD[G - 1 - j];
             a.out[(zk + 1 + j) * P + pix] = fminf(fmaxf((float)t, lo), hi);
-            if (a.var)
+            if (VAR)
               a.var[(zk + 1 + j) * P + pix] =
                   a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK + kind];
           }
@@ -523,9 +586,13 @@ static size_t fast_smem() { return (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(fl
 template <int G, typename Acc>
 static cudaError_t occupancy_t(int* occ) {
   const size_t smem = fast_smem();
-  auto kern = predict_fast_kernel<G, Acc>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, FT_THREADS, smem);
+  cudaError_t e = cudaFuncSetAttribute(predict_fast_kernel<G, Acc, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(predict_fast_kernel<G, Acc, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, predict_fast_kernel<G, Acc, false>, FT_THREADS, smem);
   *occ = std::max(1, *occ);
   return e;
 }
@@ -563,7 +630,10 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   const int n_st = (a.part1 - a.part0) * a.NK * 16;
   if (n_st > 0) fast_stencil_kernel<G, Acc><<<(n_st + 255) / 256, 256, 0, st>>>(a);
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(fl.tmap);
-  predict_fast_kernel<G, Acc><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
+  if (a.var)
+    predict_fast_kernel<G, Acc, true><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
+  else
+    predict_fast_kernel<G, Acc, false><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
   return cudaGetLastError();
 }
 
