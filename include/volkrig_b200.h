@@ -178,6 +178,22 @@ int vk_grid_scan(const float* data, const uint8_t* mask, int64_t planes,
 int vk_gather_planes(const float* src, const int32_t* known_z, int32_t K,
                      int64_t plane_elems, float* dst, void* stream);
 
+/* Generic per-voxel fill for masks that are not whole known / missing
+ * planes: the reference's fallback _predict_generic (kriging.py:408-431,
+ * window schedule kriging.py:37-40, _gather_window kriging.py:345-357,
+ * weight cache kriging.py:364-381).  data f32 [depth][height][width] (NaN at
+ * missing voxels), mask u8 same shape (1 = missing), model = (nugget, sill,
+ * range_len), lo/hi = known-value clamp range (kriging.py:475-479).  Writes
+ * out (known voxels copied bit-exactly) and, if var != NULL, the kriging
+ * variance (0 at known voxels).  info[3] (host, may be NULL): first voxel
+ * without neighbours (raster index, -1 if none), distinct window patterns
+ * solved, missing voxels.  Synchronous on `stream`.  Status
+ * VK_E_NO_KNOWN_NEIGHBORS, VK_E_SINGULAR_SYSTEM, or VK_E_UNSUPPORTED when a
+ * window holds more than 1024 known voxels. */
+int vk_fill_generic(const float* data, const uint8_t* mask, int32_t depth, int32_t height,
+                    int32_t width, int32_t kind, int32_t drift, const double* model, double lo,
+                    double hi, float* out, double* var, int64_t* info, void* stream);
+
 const char* vk_status_string(int status);
 /* Message of the last failing call on this thread (for exceptions). */
 const char* vk_last_error(void);

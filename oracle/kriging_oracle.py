@@ -309,7 +309,9 @@ def plane_flags(mask: np.ndarray):
 
 def fill_missing(data, mask, model: Model, drift="linear",
                  return_variance=False):
-    """Plane-structured ``fill_missing`` -- kriging.py:458-496, 499-557.
+    """``fill_missing`` -- kriging.py:458-496: the plane-structured stencil
+    path (kriging.py:499-557) or, for any other mask, the per-voxel window
+    path (``fill_generic``, kriging.py:408-431).
 
     ``data`` float32 [dz, dy, dx] with NaN planes, ``mask`` bool.  Returns
     (out float32, var float64 or None).
@@ -329,8 +331,8 @@ def fill_missing(data, mask, model: Model, drift="linear",
     out = data.copy()
     var = np.zeros(data.shape) if return_variance else None
     flags = plane_flags(mask)
-    if flags is None:
-        raise NotImplementedError("oracle covers the plane-structured path")
+    if flags is None:                                       # kriging.py:488-490
+        return fill_generic(data, mask, model, drift, lo, hi, out, var)
 
     dz, dy, dx = data.shape
     known_z = np.nonzero(~flags)[0]
@@ -381,6 +383,62 @@ def fill_missing(data, mask, model: Model, drift="linear",
                 out[z, y, x] = min(max(pred, lo), hi)
                 if var is not None:
                     var[z, y, x] = v
+    return out, var
+
+
+# --------------------------------------------------------------------------
+# generic per-voxel path                               kriging.py:37-40, 345-431
+# --------------------------------------------------------------------------
+
+WINDOW_SCHEDULE = ((4, 4), (4, 8), (4, 16), (8, 16), (16, 16))   # kriging.py:39
+
+
+def gather_window(mask, x, y, z, inplane, z_extent):
+    """Known voxels of the clamped window around (x, y, z) in np.nonzero
+    (z, y, x) order, as (x, y, z) coords -- kriging.py:345-357."""
+    dz, dy, dx = mask.shape
+    x0, x1 = window(x, inplane, dx)
+    y0, y1 = window(y, inplane, dy)
+    z0, z1 = window(z, z_extent, dz)
+    kz, ky, kx = np.nonzero(~mask[z0:z1, y0:y1, x0:x1])
+    if len(kz) == 0:
+        return None
+    return np.column_stack([kx + x0, ky + y0, kz + z0])
+
+
+def choose_window(mask, x, y, z):
+    """The schedule walk of ``_predict_generic`` -- kriging.py:414-424: the
+    first window whose known voxels bracket z, or at z extent 16 the first
+    window with any known voxel.  Returns (schedule index, coords) or None."""
+    for i, (inplane, z_extent) in enumerate(WINDOW_SCHEDULE):
+        coords = gather_window(mask, x, y, z, inplane, z_extent)
+        if coords is None:
+            continue
+        cz = coords[:, 2]
+        if ((cz < z).any() and (cz > z).any()) or z_extent == 16:
+            return i, coords
+    return None
+
+
+def fill_generic(data, mask, model: Model, drift, lo, hi, out, var):
+    """Per-voxel path over np.argwhere(mask) raster order, weights cached by
+    the int16 relative-offset signature -- kriging.py:408-431, 364-381."""
+    cache: dict[bytes, tuple] = {}
+    for z, y, x in np.argwhere(mask):
+        got = choose_window(mask, int(x), int(y), int(z))
+        if got is None:
+            raise NoKnownNeighbors(f"no known voxel near {(int(x), int(y), int(z))}")
+        coords = got[1]
+        rel = coords - np.array([x, y, z])
+        key = rel.astype(np.int16).tobytes()
+        if key not in cache:
+            cache[key] = stencil_weights(rel, model, drift)
+        w, v = cache[key]
+        vals = data[coords[:, 2], coords[:, 1], coords[:, 0]].astype(np.float64)
+        pred = float(w @ vals)
+        out[z, y, x] = min(max(pred, lo), hi)
+        if var is not None:
+            var[z, y, x] = v
     return out, var
 
 

@@ -29,6 +29,7 @@ UNITS = {
     "vk_solve.cu": [],
     "vk_predict.cu": [],
     "vk_predict_fixed.cu": [],
+    "vk_generic.cu": [],
     "vk_geometry.cpp": [],
 }
 

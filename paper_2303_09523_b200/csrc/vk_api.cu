@@ -561,6 +561,29 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   return VK_OK;
 }
 
+int vk_fill_generic(const float* data, const uint8_t* mask, int32_t depth, int32_t height, int32_t width,
+                    int32_t kind, int32_t drift, const double* model, double lo, double hi, float* out,
+                    double* var, int64_t* info, void* stream) {
+  if (!data || !mask || !model || !out) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  if (depth < 1 || height < 1 || width < 1) return set_err(VK_E_INVALID_ARGUMENT, "dims");
+  if (kind < 0 || kind > 2) return set_err(VK_E_INVALID_ARGUMENT, "kind");
+  if (drift < 0 || drift > 1) return set_err(VK_E_INVALID_ARGUMENT, "drift");
+  const GenericResult r = fill_generic(data, mask, depth, height, width, model, kind, drift, lo, hi, out, var,
+                                       (cudaStream_t)stream);
+  if (info) {
+    info[0] = r.failed;
+    info[1] = r.n_systems;
+    info[2] = r.n_missing;
+  }
+  switch (r.status) {
+    case 0: return VK_OK;
+    case 2: return set_err(VK_E_NO_KNOWN_NEIGHBORS, r.msg);
+    case 3: return set_err(VK_E_SINGULAR_SYSTEM, r.msg);
+    case 6: return set_err(VK_E_UNSUPPORTED, r.msg);
+    default: return set_err(VK_E_CUDA, r.msg);
+  }
+}
+
 int vk_plan_set_timing(vk_plan* p, int ring) {
   if (!p || ring < 0) return set_err(VK_E_INVALID_ARGUMENT, "bad plan / ring");
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <string>
 #include "vk_common.h"
 
 namespace vk {
@@ -150,6 +151,16 @@ cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st);
 // fixed-point tensor-core path (vk_predict_fixed.cu)
 cudaError_t occupancy_fixed(int G, int* occ);
 cudaError_t launch_predict_fixed(const void* tmap, int occ, const PredictArgs& a, cudaStream_t st);
+// generic per-voxel fill (vk_generic.cu); synchronous on `st`
+struct GenericResult {
+  int status = 0;          // 0 ok, 2 no neighbours, 3 singular, 6 unsupported, 7 CUDA
+  std::string msg;
+  int64_t failed = -1;     // first voxel (raster index) without neighbours
+  int n_systems = 0;       // distinct window patterns solved
+  int64_t n_missing = 0;
+};
+GenericResult fill_generic(const float* data, const uint8_t* mask, int T, int H, int W, const double* model,
+                           int kind, int drift, double lo, double hi, float* out, double* var, cudaStream_t st);
 inline size_t fxb_words(int S, int NK) { return (size_t)S * (size_t)NK * 32 * 8; }
 inline size_t fxc_floats(int S, int NK) { return (size_t)S * (size_t)NK * 8 * 4; }
 

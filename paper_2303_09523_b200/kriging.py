@@ -273,15 +273,40 @@ def _scan_grid(data_d, mask_d):
     return counts.cpu().numpy()
 
 
+def _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev):
+    """Non-plane masks on the device: ``vk_fill_generic`` (window schedule,
+    distinct-pattern solves, per-voxel prediction; kriging.py:408-431)."""
+    torch = _torch()
+    lib = _lib.load()
+    T, H, W = data_d.shape
+    known = data_d[mask_d == 0]
+    lo, hi = float(known.min().item()), float(known.max().item())   # kriging.py:475-479
+    out_d = torch.empty_like(data_d)
+    var_d = (torch.empty(data_d.shape, dtype=torch.float64, device=data_d.device)
+             if return_variance else None)
+    m = np.ascontiguousarray(model.as_array(), dtype=np.float64)
+    info = np.zeros(3, np.int64)
+    raise_for_status(lib.vk_fill_generic(
+        data_d.data_ptr(), mask_d.data_ptr(), T, H, W, _lib.KIND_IDS[model.kind],
+        _lib.DRIFT_IDS[drift], m.ctypes.data, lo, hi, out_d.data_ptr(),
+        var_d.data_ptr() if var_d is not None else None, info.ctypes.data,
+        _stream_handle(None)))
+    if on_dev:
+        out_grid = VolumeGrid(out_d, torch.zeros_like(grid.missing_mask), grid.origin_offset)
+        return (out_grid, var_d) if return_variance else out_grid
+    out_grid = VolumeGrid(out_d.cpu().numpy(), np.zeros_like(grid.missing_mask), grid.origin_offset)
+    return (out_grid, var_d.cpu().numpy()) if return_variance else out_grid
+
+
 def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
                  return_variance: bool = False, *, accum: str = "fp64"):
     """Fill every missing voxel by kriging from known voxels only.
 
     Known voxels pass through bit-exactly; predictions never read other
     predictions.  Host (numpy) grids come back as numpy, CUDA grids as CUDA
-    tensors.  Only the plane-structured layout (the production case,
-    kriging.py:485-487) runs on the device in this release; other masks raise
-    ``DeviceUnsupported``.
+    tensors.  Plane-structured masks (the production case, kriging.py:485-487)
+    take the streaming stencil kernels; any other mask takes the device
+    per-voxel window path (kriging.py:488-490, 408-431).
     """
     torch = _torch()
     if callable(drift):
@@ -308,15 +333,14 @@ def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
             return out, zeros
         return out
     P = H * W
-    known_z = np.nonzero(n_missing == 0)[0].astype(np.int32)
-    if len(known_z) == 0:
+    if int((P - n_missing).sum()) == 0:                      # kriging.py:475-477
         raise NoKnownNeighbors("grid has no known voxels at all")
-    if not np.all((n_missing == 0) | (n_missing == P)):
-        raise DeviceUnsupported(
-            "only plane-structured masks (whole known / missing planes) run on "
-            "the device; the per-voxel window path is not implemented yet")
+    known_z = np.nonzero(n_missing == 0)[0].astype(np.int32)
     if drift not in _lib.DRIFT_IDS:
         raise ValueError(f"unknown drift {drift!r}")
+    if not np.all((n_missing == 0) | (n_missing == P)):
+        # arbitrary mask: the per-voxel window path (kriging.py:488-490, 408-431)
+        return _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev)
     plan = cached_plan(height=H, width=W, depth=T, known_z=known_z.tolist(), n_subparts=1,
                        kind=model.kind, drift=drift, accum=accum, fit=False)
     lib = _lib.load()

@@ -141,3 +141,51 @@ def test_oracle_equals_live_reference():
         a = K.fit_variogram((c, v))
         b = O.fit_variogram((c, v))
         assert (a.nugget, a.sill, a.range_len) == (b.nugget, b.sill, b.range_len)
+
+
+# --------------------------------------------------------------------------
+# generic per-voxel path (non-plane masks), tests/golden/make_golden_generic.py
+# --------------------------------------------------------------------------
+
+def _generic_golden():
+    d = np.load(os.path.join(HERE, "golden", "reference_generic.npz"))
+    with open(os.path.join(HERE, "golden", "reference_generic.json")) as f:
+        meta = json.load(f)
+    return d, meta
+
+
+def test_oracle_generic_path_matches_reference_goldens():
+    d, meta = _generic_golden()
+    assert len(meta["cases"]) >= 7
+    for c in meta["cases"]:
+        n = c["name"]
+        kind, nug, sill, rng = c["model"]
+        out, var = O.fill_missing(d[f"{n}/data"], d[f"{n}/mask"], O.Model(kind, nug, sill, rng),
+                                  c["drift"], True)
+        assert O.plane_flags(d[f"{n}/mask"]) is None
+        np.testing.assert_array_equal(out, d[f"{n}/out"], err_msg=n)
+        np.testing.assert_allclose(var, d[f"{n}/var"], rtol=1e-12, atol=1e-12 * sill, err_msg=n)
+
+
+def test_oracle_generic_no_neighbors():
+    _, meta = _generic_golden()
+    nn = meta["no_neighbors"]
+    data = np.full(nn["shape"], np.nan, np.float32)
+    data[0, 0, nn["known_x"]] = 5.0
+    with pytest.raises(O.NoKnownNeighbors, match=r"\(8, 0, 0\)"):
+        O.fill_missing(data, np.isnan(data), O.Model("exponential", 0.0, 1.0, 3.0))
+
+
+def test_oracle_generic_window_schedule():
+    """kriging.py:39, 414-424: bracketing decides the z extent; at z extent
+    16 the first window with any known voxel is taken."""
+    mask = np.ones((20, 9, 9), bool)
+    mask[3] = False                                   # known plane below z=10 only
+    i, coords = O.choose_window(mask, 4, 4, 10)
+    assert O.WINDOW_SCHEDULE[i] == (4, 16) and set(coords[:, 2]) == {3}
+    mask[12] = False                                  # above only at z extent 8 (planes 7..14)
+    i, coords = O.choose_window(mask, 4, 4, 10)
+    assert O.WINDOW_SCHEDULE[i] == (4, 16) and set(coords[:, 2]) == {3, 12}
+    mask[8] = False                                   # bracketed at z extent 8
+    i, coords = O.choose_window(mask, 4, 4, 10)
+    assert O.WINDOW_SCHEDULE[i] == (4, 8) and set(coords[:, 2]) == {8, 12}
