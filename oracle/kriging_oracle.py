@@ -519,3 +519,52 @@ def reconstruct_zparts(slices, factor, n_parts, kind="exponential",
 def interpolated_voxels(n_known: int, factor: int, h: int, w: int) -> int:
     return (n_known - 1) * (factor - 1) * h * w
 
+
+# --------------------------------------------------------------------------
+# block pipeline (absent from the reference's code)
+# --------------------------------------------------------------------------
+
+def block_boxes(height, width, halo_width=2, tiles=(2, 2)):
+    """In-plane tiles: (core, box) with the halo on internal sides only --
+    SPEC.md:388-395, 422-424."""
+    ty_n, tx_n = tiles
+    ys = [(i * (height // ty_n), (i + 1) * (height // ty_n) if i < ty_n - 1 else height)
+          for i in range(ty_n)]
+    xs = [(i * (width // tx_n), (i + 1) * (width // tx_n) if i < tx_n - 1 else width)
+          for i in range(tx_n)]
+    out = []
+    for iy, (y0, y1) in enumerate(ys):
+        for ix, (x0, x1) in enumerate(xs):
+            by0 = y0 - halo_width if iy > 0 else y0
+            by1 = y1 + halo_width if iy < ty_n - 1 else y1
+            bx0 = x0 - halo_width if ix > 0 else x0
+            bx1 = x1 + halo_width if ix < tx_n - 1 else x1
+            out.append(((y0, y1, x0, x1), (max(0, by0), min(height, by1), max(0, bx0), min(width, bx1))))
+    return out
+
+
+def reconstruct_blocks(slices, factor, k=2, halo_width=2, tiles=(2, 2), models=None):
+    """partition -> per-block fit + fill -> merge: every
+    in-plane tile runs the Z sub-part pipeline with k chunks; the merged
+    volume keeps each tile's core.  ``models`` ([tiles*k] Model, (tile,
+    chunk) order) skips the fits."""
+    slices = np.ascontiguousarray(slices, dtype=np.float32)
+    K, H, W = slices.shape
+    T = K + (K - 1) * (factor - 1)
+    out = np.empty((T, H, W), np.float32)
+    all_models = []
+    for ti, ((y0, y1, x0, x1), (by0, by1, bx0, bx1)) in enumerate(block_boxes(H, W, halo_width, tiles)):
+        sub = slices[:, by0:by1, bx0:bx1]
+        if models is None:
+            vol, _, ms = reconstruct_zparts(sub, factor, k)
+        else:
+            ms = models[ti * k:(ti + 1) * k]
+            vol = np.empty((T, by1 - by0, bx1 - bx0), np.float32)
+            for c, (b, e) in enumerate(subpart_ranges(K, k)):
+                d, m = subpart_grid(sub, b, e, factor)
+                o, _ = fill_missing(d, m, ms[c])
+                vol[b * factor:b * factor + o.shape[0]] = o
+        out[:, y0:y1, x0:x1] = vol[:, y0 - by0:y1 - by0, x0 - bx0:x1 - bx0]
+        all_models.extend(ms)
+    return out, all_models
+

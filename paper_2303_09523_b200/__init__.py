@@ -10,11 +10,13 @@ from .errors import (DegenerateLags, DeviceError, DeviceUnsupported,
 from .model import SliceStack, VolumeGrid, missing_planes_per_gap
 from .kriging import (KrigingPlan, VariogramModel, fill_missing, fit_variogram)
 from .block_pipeline import ZPartKriging, reconstruct_zparts, subpart_ranges
+from .blocks import BlockDescriptor, BlockKriging, partition, reconstruct_blocks
 
 __all__ = [
     "DegenerateLags", "DeviceError", "DeviceUnsupported", "InsufficientSamples",
     "NoKnownNeighbors", "SingularSystem", "TooFewSlices", "VolkrigError",
     "SliceStack", "VolumeGrid", "missing_planes_per_gap", "KrigingPlan",
     "VariogramModel", "fill_missing", "fit_variogram", "ZPartKriging",
-    "reconstruct_zparts", "subpart_ranges",
+    "reconstruct_zparts", "subpart_ranges", "BlockDescriptor", "BlockKriging", "partition",
+    "reconstruct_blocks",
 ]
