@@ -194,6 +194,16 @@ int vk_fill_generic(const float* data, const uint8_t* mask, int32_t depth, int32
                     int32_t width, int32_t kind, int32_t drift, const double* model, double lo,
                     double hi, float* out, double* var, int64_t* info, void* stream);
 
+/* Binary volume format (io.py:146-200, VOLKRIG\0 v1): CRC-32 of device
+ * bytes continuing from `crc_in` exactly as zlib.crc32(data, crc_in) (so a
+ * host header, a device payload and a device mask chain into the file's
+ * single CRC), and the mask bit packing of np.packbits / np.unpackbits
+ * (big-endian bits, zero-padded last byte).  vk_crc32 is synchronous on
+ * `stream`; the packers are asynchronous. */
+int vk_crc32(const void* data, int64_t n_bytes, uint32_t crc_in, uint32_t* crc_out, void* stream);
+int vk_packbits(const uint8_t* mask, int64_t n, uint8_t* bits, void* stream);
+int vk_unpackbits(const uint8_t* bits, int64_t n, uint8_t* mask, void* stream);
+
 const char* vk_status_string(int status);
 /* Message of the last failing call on this thread (for exceptions). */
 const char* vk_last_error(void);

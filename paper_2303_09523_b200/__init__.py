@@ -11,6 +11,7 @@ from .model import SliceStack, VolumeGrid, missing_planes_per_gap
 from .kriging import (KrigingPlan, VariogramModel, fill_missing, fit_variogram)
 from .block_pipeline import ZPartKriging, reconstruct_zparts, subpart_ranges
 from .blocks import BlockDescriptor, BlockKriging, partition, reconstruct_blocks
+from .volume_io import load_volume, save_volume
 
 __all__ = [
     "DegenerateLags", "DeviceError", "DeviceUnsupported", "InsufficientSamples",
@@ -18,5 +19,5 @@ __all__ = [
     "SliceStack", "VolumeGrid", "missing_planes_per_gap", "KrigingPlan",
     "VariogramModel", "fill_missing", "fit_variogram", "ZPartKriging",
     "reconstruct_zparts", "subpart_ranges", "BlockDescriptor", "BlockKriging", "partition",
-    "reconstruct_blocks",
+    "reconstruct_blocks", "load_volume", "save_volume",
 ]

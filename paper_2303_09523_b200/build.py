@@ -30,6 +30,7 @@ UNITS = {
     "vk_predict.cu": [],
     "vk_predict_fixed.cu": [],
     "vk_generic.cu": [],
+    "vk_volio.cu": [],
     "vk_geometry.cpp": [],
 }
 

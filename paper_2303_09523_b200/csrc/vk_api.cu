@@ -584,6 +584,24 @@ int vk_fill_generic(const float* data, const uint8_t* mask, int32_t depth, int32
   }
 }
 
+int vk_crc32(const void* data, int64_t n_bytes, uint32_t crc_in, uint32_t* crc_out, void* stream) {
+  if ((!data && n_bytes > 0) || !crc_out || n_bytes < 0) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  VK_CUDA(crc32_device(data, n_bytes, crc_in, crc_out, (cudaStream_t)stream));
+  return VK_OK;
+}
+
+int vk_packbits(const uint8_t* mask, int64_t n, uint8_t* bits, void* stream) {
+  if ((!mask || !bits) && n > 0) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  VK_CUDA(packbits_device(mask, n, bits, (cudaStream_t)stream));
+  return VK_OK;
+}
+
+int vk_unpackbits(const uint8_t* bits, int64_t n, uint8_t* mask, void* stream) {
+  if ((!mask || !bits) && n > 0) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  VK_CUDA(unpackbits_device(bits, n, mask, (cudaStream_t)stream));
+  return VK_OK;
+}
+
 int vk_plan_set_timing(vk_plan* p, int ring) {
   if (!p || ring < 0) return set_err(VK_E_INVALID_ARGUMENT, "bad plan / ring");
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);

@@ -161,6 +161,10 @@ struct GenericResult {
 };
 GenericResult fill_generic(const float* data, const uint8_t* mask, int T, int H, int W, const double* model,
                            int kind, int drift, double lo, double hi, float* out, double* var, cudaStream_t st);
+// binary volume format helpers (vk_volio.cu)
+cudaError_t crc32_device(const void* data, int64_t n, uint32_t crc_in, uint32_t* crc_out, cudaStream_t st);
+cudaError_t packbits_device(const uint8_t* mask, int64_t n, uint8_t* bits, cudaStream_t st);
+cudaError_t unpackbits_device(const uint8_t* bits, int64_t n, uint8_t* mask, cudaStream_t st);
 inline size_t fxb_words(int S, int NK) { return (size_t)S * (size_t)NK * 32 * 8; }
 inline size_t fxc_floats(int S, int NK) { return (size_t)S * (size_t)NK * 8 * 4; }
 
