@@ -363,9 +363,12 @@ def run_gpu(args, cfg, ks):
 
 
 def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):
-    """Same metric through the public API from pinned host buffers: H2D of
-    the known slices + (halo exchange) + kriging path + D2H of the
-    reconstructed volume, every step.  Max over ranks."""
+    """Same metric through the public API from pinned host buffers: every
+    step uploads its known slices, (exchanges the halo,) runs the kriging
+    path and downloads the whole reconstructed volume.  Steps are
+    double-buffered across three streams -- upload of step i+1 and download
+    of step i-1 overlap step i's compute (PCIe is full duplex) -- and every
+    step still moves all of its bytes.  Device time, max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2303_09523_b200 import ZPartKriging
@@ -377,34 +380,55 @@ def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):
     host_in = torch.from_numpy(ks).pin_memory()
     zk1 = ZPartKriging(K_loc, H, W, cfg.factor, cfg.n_subparts, accum=args.accum,
                        redraw_pairs=True, part_len=K // cfg.n_subparts)
-    dev_in = torch.empty((K_loc, H, W), dtype=torch.float32, device=dev or "cuda")
-    out, var = zk1.allocate(bool(args.variance))
-    host_out = torch.empty(out.shape, dtype=torch.float32).pin_memory()
-    host_var = torch.empty(var.shape, dtype=torch.float64).pin_memory() if var is not None else None
+    dev_in = [torch.empty((K_loc, H, W), dtype=torch.float32, device=dev or "cuda") for _ in range(2)]
+    bufs = [zk1.allocate(bool(args.variance)) for _ in range(2)]
+    host_out = [torch.empty(bufs[0][0].shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+    host_var = ([torch.empty(bufs[0][1].shape, dtype=torch.float64).pin_memory() for _ in range(2)]
+                if args.variance else [None, None])
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_done + ev_out:
+        e.record(stream)
 
-    def step():
-        dev_in[:K].copy_(host_in, non_blocking=True)
+    def step(i):
+        b = i % 2
+        with torch.cuda.stream(s_in):                  # upload (input buffer free after step i-2)
+            s_in.wait_event(ev_done[b])
+            dev_in[b][:K].copy_(host_in, non_blocking=True)
+            ev_in[b].record(s_in)
+        stream.wait_event(ev_in[b])
+        stream.wait_event(ev_out[b])                   # output buffer downloaded (step i-2)
         if world > 1:
-            halo = exchange_halo(dev_in[0], rank, world)
+            halo = exchange_halo(dev_in[b][0], rank, world)
             if halo is not None:
-                dev_in[K].copy_(halo)
-        zk1.run(dev_in, out, var)
-        host_out.copy_(out, non_blocking=True)
-        if var is not None:
-            host_var.copy_(var, non_blocking=True)
+                dev_in[b][K].copy_(halo)
+        out, var = bufs[b]
+        zk1.run(dev_in[b], out, var)
+        ev_done[b].record(stream)
+        with torch.cuda.stream(s_out):                 # download
+            s_out.wait_event(ev_done[b])
+            host_out[b].copy_(out, non_blocking=True)
+            if var is not None:
+                host_var[b].copy_(var, non_blocking=True)
+            ev_out[b].record(s_out)
 
-    for _ in range(2):
-        step()
+    for i in range(2):
+        step(i)
+    torch.cuda.synchronize()
     zk1.finish()
-    steps = max(2, min(args.steps, 5))
+    steps = max(2, min(args.steps, 6))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
-    for _ in range(steps):
-        step()
+    for i in range(steps):
+        step(i)
+    for e in ev_out:                                   # region ends when the last download lands
+        stream.wait_event(e)
     e1.record(stream)
     torch.cuda.synchronize()
     zk1.finish()
@@ -417,10 +441,12 @@ def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):
         tv = t[1:].clone()
         dist.all_reduce(tv)
         ms, vox = float(tm.item()), float(tv.item())
+    out, var = bufs[0]
     d2h = out.numel() * 4 + (var.numel() * 8 if var is not None else 0)
     return {"value": vox / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": K * H * W * 4, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": steps, "per_rank_bytes": True}
+            "ms_per_step": ms, "steps": steps, "per_rank_bytes": True,
+            "pipelining": "double-buffered: upload i+1 / compute i / download i-1 on 3 streams"}
 
 
 def main(argv=None):
