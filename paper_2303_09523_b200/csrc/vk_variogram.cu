@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(PT_BLOCK) pair_bin_kernel(const PairJob* jobs)
 
 __global__ void __launch_bounds__(256) bins_kernel(BinsArgs a) {
   extern __shared__ double acc[];          // [n_bins][blockDim]
-  const int s = blockIdx.y, blk = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  // parts in reverse: the statistics pass streams the planes in order just
+  // before, so the last parts' planes are still in L2 when their random
+  // gathers start
+  const int s = a.S - 1 - (int)blockIdx.y, blk = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const PairTable t = a.tables[a.part_class[s]];
   const int64_t npairs = (int64_t)t.scal[2];
   const int64_t per = (npairs + a.nblk - 1) / a.nblk;
