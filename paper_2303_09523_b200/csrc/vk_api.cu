@@ -96,8 +96,9 @@ struct vk_plan {
   // per-part chains (fit -> solve -> predict): one stream per part (up to
   // NCH), so every part's latency-bound fit starts at once
   static constexpr int NCH = 64;
-  cudaStream_t chain[NCH] = {};
-  cudaEvent_t ev_kfork = nullptr, ev_kjoin[NCH] = {};
+  cudaStream_t chain[NCH] = {};        // fit -> solve (high priority)
+  cudaStream_t pchain[NCH] = {};       // predict (low priority), after its part's solve
+  cudaEvent_t ev_kfork = nullptr, ev_kjoin[NCH] = {}, ev_solved[NCH] = {}, ev_pjoin[NCH] = {};
   std::vector<int> sys_begin;         // [S + 1] system range of each part
   std::vector<int> gap_begin;         // [S + 1] gap range of each part (fast path)
   FastLaunch fast_launch;             // cached TMA descriptor + occupancy
@@ -125,7 +126,10 @@ struct vk_plan {
     if (ev_kfork) cudaEventDestroy(ev_kfork);
     for (int i = 0; i < NCH; ++i) {
       if (ev_kjoin[i]) cudaEventDestroy(ev_kjoin[i]);
+      if (ev_solved[i]) cudaEventDestroy(ev_solved[i]);
+      if (ev_pjoin[i]) cudaEventDestroy(ev_pjoin[i]);
       if (chain[i]) cudaStreamDestroy(chain[i]);
+      if (pchain[i]) cudaStreamDestroy(pchain[i]);
     }
     for (void* p : allocs) cudaFree(p);
     if (h_models) cudaFreeHost(h_models);
@@ -335,8 +339,16 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   // timing, debugging)
   if (!(d->flags & VK_FLAG_SERIAL) && S > 1 && g.fast) {
     VK_TRY(cudaEventCreateWithFlags(&p->ev_kfork, cudaEventDisableTiming));
+    // fits and solves are latency chains: their streams get the highest
+    // priority so a part's solve CTAs are placed ahead of the streaming CTAs
+    // of parts already predicting; predicts run at the lowest priority
+    int prio_lo = 0, prio_hi = 0;
+    VK_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     for (int i = 0; i < std::min(S, vk_plan::NCH); ++i) {
-      VK_TRY(cudaStreamCreateWithFlags(&p->chain[i], cudaStreamNonBlocking));
+      VK_TRY(cudaStreamCreateWithPriority(&p->chain[i], cudaStreamNonBlocking, prio_hi));
+      VK_TRY(cudaStreamCreateWithPriority(&p->pchain[i], cudaStreamNonBlocking, prio_lo));
+      VK_TRY(cudaEventCreateWithFlags(&p->ev_solved[i], cudaEventDisableTiming));
+      VK_TRY(cudaEventCreateWithFlags(&p->ev_pjoin[i], cudaEventDisableTiming));
       VK_TRY(cudaEventCreateWithFlags(&p->ev_kjoin[i], cudaEventDisableTiming));
     }
   }
@@ -505,6 +517,14 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(cudaEventRecord(p->ev_kfork, st));
     const int nch = std::min(S, vk_plan::NCH);
     for (int c = 0; c < nch; ++c) VK_CUDA(cudaStreamWaitEvent(p->chain[c], p->ev_kfork, 0));
+    // VK_CHAIN_TRACE (debug): per-part fit / solve / predict completion times
+    static const bool trace = std::getenv("VK_CHAIN_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    if (trace) {
+      tev.resize(1 + 3 * S);
+      for (auto& e : tev) cudaEventCreate(&e);
+      cudaEventRecord(tev[0], st);
+    }
     // breadth-first launch order (all fits, then all solves, then all
     // predicts): a chain's solve waits on its fit, and a waiting kernel at
     // the head of a hardware work queue would block the fits queued behind it
@@ -515,6 +535,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       f1.reserve_smem = p->fit_reserve;
       VK_CUDA(launch_fit(f1, p->chain[s % nch]));
       ++kernels;
+      if (trace) cudaEventRecord(tev[1 + 3 * s], p->chain[s % nch]);
     }
     for (int s = 0; s < S; ++s) {
       SolveArgs s1 = sa;
@@ -522,6 +543,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       s1.n_sys = p->sys_begin[s + 1] - p->sys_begin[s];
       VK_CUDA(launch_solve(s1, p->chain[s % nch]));
       kernels += (s1.n_sys > 0);
+      if (trace) cudaEventRecord(tev[2 + 3 * s], p->chain[s % nch]);
     }
     for (int s = 0; s < S; ++s) {
       PredictArgs p1 = pa;
@@ -530,12 +552,31 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       p1.chunk = p1.gap1 - p1.gap0;           // one unit = a tile over the part's gaps
       p1.part0 = s;
       p1.part1 = s + 1;
-      VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, p->chain[s % nch]));
+      // the part's solve finished on its high-priority chain (a part reuses
+      // a chain slot only when S > NCH, in launch order, so the event
+      // recorded last on the slot covers this part)
+      VK_CUDA(cudaEventRecord(p->ev_solved[s % nch], p->chain[s % nch]));
+      VK_CUDA(cudaStreamWaitEvent(p->pchain[s % nch], p->ev_solved[s % nch], 0));
+      VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, p->pchain[s % nch]));
       kernels += 2;
+      if (trace) cudaEventRecord(tev[3 + 3 * s], p->pchain[s % nch]);
     }
     for (int c = 0; c < nch; ++c) {
       VK_CUDA(cudaEventRecord(p->ev_kjoin[c], p->chain[c]));
       VK_CUDA(cudaStreamWaitEvent(st, p->ev_kjoin[c], 0));
+      VK_CUDA(cudaEventRecord(p->ev_pjoin[c], p->pchain[c]));
+      VK_CUDA(cudaStreamWaitEvent(st, p->ev_pjoin[c], 0));
+    }
+    if (trace) {
+      cudaStreamSynchronize(st);
+      for (int s2 = 0; s2 < S; ++s2) {
+        float f = 0, v = 0, q = 0;
+        cudaEventElapsedTime(&f, tev[0], tev[1 + 3 * s2]);
+        cudaEventElapsedTime(&v, tev[0], tev[2 + 3 * s2]);
+        cudaEventElapsedTime(&q, tev[0], tev[3 + 3 * s2]);
+        std::fprintf(stderr, "chain %2d fit %.3f solve %.3f predict %.3f ms\n", s2, f, v, q);
+      }
+      for (auto& e : tev) cudaEventDestroy(e);
     }
     VK_CUDA(mark(4));
     VK_CUDA(mark(5));
