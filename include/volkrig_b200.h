@@ -194,6 +194,20 @@ int vk_fill_generic(const float* data, const uint8_t* mask, int32_t depth, int32
                     int32_t width, int32_t kind, int32_t drift, const double* model, double lo,
                     double hi, float* out, double* var, int64_t* info, void* stream);
 
+/* Batched extended kriging systems for arbitrary neighbour sets -- the
+ * reference's build_system + solve_ked (kriging.py:159-245) for each entry of
+ * a weight cache (kriging.py:364-381): rel = device int16 [total][3]
+ * target-relative (x, y, z) offsets of every system's neighbours, offsets =
+ * host int64 [n_systems + 1] (system i owns rel rows offsets[i] ..
+ * offsets[i+1]-1, 1..1024 rows), model = host (nugget, sill, range_len).
+ * Drift columns are kept by the reference's rank test; LU with partial
+ * pivoting, residual check 1e-8, one ridge retry.  Writes weights (device
+ * f64 [total]) and variance (device f64 [n_systems]); status (host int32
+ * [n_systems], may be NULL): 0 ok, 1 singular.  Synchronous on `stream`. */
+int vk_solve_systems(const int16_t* rel, const int64_t* offsets, int32_t n_systems, int32_t kind,
+                     int32_t drift, const double* model, double* weights, double* variance,
+                     int32_t* status, void* stream);
+
 /* Binary volume format (io.py:146-200, VOLKRIG\0 v1): CRC-32 of device
  * bytes continuing from `crc_in` exactly as zlib.crc32(data, crc_in) (so a
  * host header, a device payload and a device mask chain into the file's

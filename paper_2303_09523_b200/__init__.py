@@ -8,7 +8,8 @@ from .errors import (DegenerateLags, DeviceError, DeviceUnsupported,
                      InsufficientSamples, NoKnownNeighbors, SingularSystem,
                      TooFewSlices, VolkrigError)
 from .model import SliceStack, VolumeGrid, missing_planes_per_gap
-from .kriging import (KrigingPlan, VariogramModel, fill_missing, fit_variogram)
+from .kriging import (KrigingPlan, VariogramModel, fill_missing, fit_variogram,
+                      interpolate_voxel, solve_systems)
 from .block_pipeline import ZPartKriging, reconstruct_zparts, subpart_ranges
 from .blocks import BlockDescriptor, BlockKriging, partition, reconstruct_blocks
 from .volume_io import load_volume, save_volume
@@ -17,7 +18,8 @@ __all__ = [
     "DegenerateLags", "DeviceError", "DeviceUnsupported", "InsufficientSamples",
     "NoKnownNeighbors", "SingularSystem", "TooFewSlices", "VolkrigError",
     "SliceStack", "VolumeGrid", "missing_planes_per_gap", "KrigingPlan",
-    "VariogramModel", "fill_missing", "fit_variogram", "ZPartKriging",
+    "VariogramModel", "fill_missing", "fit_variogram", "interpolate_voxel", "solve_systems",
+    "ZPartKriging",
     "reconstruct_zparts", "subpart_ranges", "BlockDescriptor", "BlockKriging", "partition",
     "reconstruct_blocks", "load_volume", "save_volume",
 ]

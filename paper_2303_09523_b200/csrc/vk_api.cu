@@ -625,6 +625,35 @@ int vk_fill_generic(const float* data, const uint8_t* mask, int32_t depth, int32
   }
 }
 
+int vk_solve_systems(const int16_t* rel, const int64_t* offsets, int32_t n_systems, int32_t kind, int32_t drift,
+                     const double* model, double* weights, double* variance, int32_t* status, void* stream) {
+  if (!rel || !offsets || !model || !weights || !variance || n_systems < 1)
+    return set_err(VK_E_INVALID_ARGUMENT, "null argument or no systems");
+  if (kind < 0 || kind > 2) return set_err(VK_E_INVALID_ARGUMENT, "kind");
+  if (drift < 0 || drift > 1) return set_err(VK_E_INVALID_ARGUMENT, "drift");
+  std::vector<int64_t> off(offsets, offsets + n_systems + 1);
+  for (int i = 0; i < n_systems; ++i) {
+    const int64_t n = off[i + 1] - off[i];
+    if (n <= 0) return set_err(VK_E_NO_KNOWN_NEIGHBORS, "cannot build a system with zero neighbors");
+    if (n > 1024) return set_err(VK_E_UNSUPPORTED, "a system with more than 1024 neighbours");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* d_status = nullptr;
+  VK_CUDA(cudaMallocAsync((void**)&d_status, n_systems * sizeof(int32_t), st));
+  cudaError_t e = solve_systems_device(rel, off, kind, drift, model, weights, variance, d_status, st);
+  std::vector<int32_t> hs(n_systems, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), d_status, n_systems * 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_status, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_err(VK_E_CUDA, std::string("vk_solve_systems: ") + cudaGetErrorString(e));
+  bool bad = false;
+  for (int i = 0; i < n_systems; ++i) {
+    if (status) status[i] = hs[i] == PS_OK ? 0 : 1;
+    bad |= hs[i] != PS_OK;
+  }
+  return bad ? set_err(VK_E_SINGULAR_SYSTEM, "extended kriging matrix is singular") : VK_OK;
+}
+
 int vk_crc32(const void* data, int64_t n_bytes, uint32_t crc_in, uint32_t* crc_out, void* stream) {
   if ((!data && n_bytes > 0) || !crc_out || n_bytes < 0) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
   VK_CUDA(crc32_device(data, n_bytes, crc_in, crc_out, (cudaStream_t)stream));

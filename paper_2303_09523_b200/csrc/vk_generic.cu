@@ -429,6 +429,45 @@ struct KeyHash {
 
 }  // namespace
 
+cudaError_t solve_systems_device(const int16_t* rel_dev, const std::vector<int64_t>& rel_off, int kind, int drift,
+                                 const double* model, double* w_dev, double* var_dev, int32_t* status_dev,
+                                 cudaStream_t st) {
+  const int nu = (int)rel_off.size() - 1;
+  if (nu <= 0) return cudaSuccess;
+  std::vector<int32_t> n_of(nu);
+  std::vector<int64_t> mat_off(nu + 1, 0);
+  int64_t biggest = 0;
+  for (int u = 0; u < nu; ++u) {
+    n_of[u] = (int32_t)(rel_off[u + 1] - rel_off[u]);
+    const int64_t NN = n_of[u] + 4;
+    mat_off[u + 1] = mat_off[u] + NN * NN;
+    biggest = std::max(biggest, NN * NN);
+  }
+  DevBuf<int32_t> d_n;
+  DevBuf<int64_t> d_rel_off, d_mat_off;
+  DevBuf<double> scratch;
+  const int64_t max_scratch = (int64_t)256 << 20;   // doubles per batch (2 GB)
+  cudaError_t e = d_n.alloc(nu);
+  if (e == cudaSuccess) e = d_rel_off.alloc(nu + 1);
+  if (e == cudaSuccess) e = d_mat_off.alloc(nu + 1);
+  if (e == cudaSuccess) e = scratch.alloc((size_t)std::min(mat_off[nu], std::max(max_scratch, biggest)));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_n.p, n_of.data(), nu * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_rel_off.p, rel_off.data(), (nu + 1) * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_mat_off.p, mat_off.data(), (nu + 1) * 8, cudaMemcpyHostToDevice, st);
+  SolveCtx ctx{kind, drift, Model{model[0], model[1], model[2]}};
+  for (int u0 = 0; e == cudaSuccess && u0 < nu;) {
+    int u1 = u0 + 1;
+    while (u1 < nu && mat_off[u1 + 1] - mat_off[u0] <= max_scratch && u1 - u0 < 65535) ++u1;
+    generic_solve_kernel<<<u1 - u0, 256, 0, st>>>(ctx, rel_dev, d_rel_off.p, d_n.p, d_mat_off.p, u0, scratch.p,
+                                                  w_dev, var_dev, status_dev);
+    e = cudaGetLastError();
+    u0 = u1;
+  }
+  // the buffers above are freed when this returns: finish the work first
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e;
+}
+
 GenericResult fill_generic(const float* data, const uint8_t* mask, int T, int H, int W, const double* model,
                            int kind, int drift, double lo, double hi, float* out, double* var,
                            cudaStream_t st) {
@@ -504,51 +543,33 @@ GenericResult fill_generic(const float* data, const uint8_t* mask, int T, int H,
     uid[i] = it->second;
   }
   const int nu = (int)rep.size();
-  std::vector<int64_t> rel_off(nu + 1, 0), mat_off(nu + 1, 0);
-  for (int u = 0; u < nu; ++u) {
-    rel_off[u + 1] = rel_off[u] + n_of[u];
-    const int64_t NN = n_of[u] + 4;
-    mat_off[u + 1] = mat_off[u] + NN * NN;
-  }
-  DevBuf<int32_t> d_uid, d_n, d_status;
-  DevBuf<int64_t> d_rep, d_rel_off, d_mat_off;
+  std::vector<int64_t> rel_off(nu + 1, 0);
+  for (int u = 0; u < nu; ++u) rel_off[u + 1] = rel_off[u] + n_of[u];
+  DevBuf<int32_t> d_uid, d_status;
+  DevBuf<int64_t> d_rep, d_rel_off;
   DevBuf<int16_t> d_rel;
   DevBuf<double> d_w, d_var;
   DevBuf<int> d_mis;
   GEN_TRY(d_uid.alloc(n_miss));
-  GEN_TRY(d_n.alloc(nu));
   GEN_TRY(d_status.alloc(nu));
   GEN_TRY(d_rep.alloc(nu));
   GEN_TRY(d_rel_off.alloc(nu + 1));
-  GEN_TRY(d_mat_off.alloc(nu + 1));
   GEN_TRY(d_rel.alloc(3 * rel_off[nu]));
   GEN_TRY(d_w.alloc(rel_off[nu]));
   GEN_TRY(d_var.alloc(nu));
   GEN_TRY(d_mis.alloc(1));
   GEN_TRY(cudaMemcpyAsync(d_uid.p, uid.data(), n_miss * 4, cudaMemcpyHostToDevice, st));
-  GEN_TRY(cudaMemcpyAsync(d_n.p, n_of.data(), nu * 4, cudaMemcpyHostToDevice, st));
   GEN_TRY(cudaMemcpyAsync(d_rep.p, rep.data(), nu * 8, cudaMemcpyHostToDevice, st));
   GEN_TRY(cudaMemcpyAsync(d_rel_off.p, rel_off.data(), (nu + 1) * 8, cudaMemcpyHostToDevice, st));
-  GEN_TRY(cudaMemcpyAsync(d_mat_off.p, mat_off.data(), (nu + 1) * 8, cudaMemcpyHostToDevice, st));
   GEN_TRY(cudaMemsetAsync(d_mis.p, 0, sizeof(int), st));
   verify_kernel<<<nb, 128, 0, st>>>(mask, T, H, W, miss.p, n_miss, sel.p, d_uid.p, d_rep.p, d_mis.p);
   rel_kernel<<<(nu + 127) / 128, 128, 0, st>>>(mask, T, H, W, miss.p, sel.p, d_rep.p, d_rel_off.p, 0, nu,
                                               d_rel.p);
   GEN_TRY(cudaGetLastError());
-  // ---- solve the distinct systems in batches bounded by the scratch size
-  SolveCtx ctx{kind, drift, Model{model[0], model[1], model[2]}};
-  const int64_t max_scratch = (int64_t)256 << 20;   // doubles per batch (2 GB)
-  int64_t biggest = 0;
-  for (int u = 0; u < nu; ++u) biggest = std::max(biggest, mat_off[u + 1] - mat_off[u]);
-  DevBuf<double> scratch;
-  GEN_TRY(scratch.alloc((size_t)std::min(mat_off[nu], std::max(max_scratch, biggest))));
-  for (int u0 = 0; u0 < nu;) {
-    int u1 = u0 + 1;
-    while (u1 < nu && mat_off[u1 + 1] - mat_off[u0] <= max_scratch && u1 - u0 < 65535) ++u1;
-    generic_solve_kernel<<<u1 - u0, 256, 0, st>>>(ctx, d_rel.p, d_rel_off.p, d_n.p, d_mat_off.p, u0, scratch.p,
-                                                  d_w.p, d_var.p, d_status.p);
-    GEN_TRY(cudaGetLastError());
-    u0 = u1;
+  // ---- solve the distinct systems (batched, bounded scratch)
+  {
+    cudaError_t e = solve_systems_device(d_rel.p, rel_off, kind, drift, model, d_w.p, d_var.p, d_status.p, st);
+    if (e != cudaSuccess) return cuda_fail(e, "solve_systems_device");
   }
   std::vector<int32_t> status(nu);
   int mismatch = 0;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <string>
+#include <vector>
 #include "vk_common.h"
 
 namespace vk {
@@ -159,6 +160,12 @@ struct GenericResult {
   int n_systems = 0;       // distinct window patterns solved
   int64_t n_missing = 0;
 };
+// batched extended-system solves for arbitrary neighbour sets (vk_generic.cu):
+// rel_dev int16 [total][3] target-relative offsets, rel_off host [n + 1];
+// writes weights [total], variances [n], PartStatus [n] (device); synchronous
+cudaError_t solve_systems_device(const int16_t* rel_dev, const std::vector<int64_t>& rel_off, int kind, int drift,
+                                 const double* model, double* w_dev, double* var_dev, int32_t* status_dev,
+                                 cudaStream_t st);
 GenericResult fill_generic(const float* data, const uint8_t* mask, int T, int H, int W, const double* model,
                            int kind, int drift, double lo, double hi, float* out, double* var, cudaStream_t st);
 // binary volume format helpers (vk_volio.cu)

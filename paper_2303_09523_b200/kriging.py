@@ -273,6 +273,66 @@ def _scan_grid(data_d, mask_d):
     return counts.cpu().numpy()
 
 
+def solve_systems(rels, model: VariogramModel, drift="linear"):
+    """``build_system`` + ``solve_ked`` (kriging.py:159-245) for a batch of
+    neighbour sets, on the device (``vk_solve_systems``).  ``rels`` is a list
+    of (n_i, 3) integer target-relative (x, y, z) offsets; returns (list of
+    weight arrays, variance array).  Raises ``SingularSystem`` like the
+    reference when a system stays singular after the ridge retry."""
+    torch = _torch()
+    if callable(drift):
+        raise DeviceUnsupported("a callable drift cannot cross the C ABI")
+    if drift not in _lib.DRIFT_IDS:
+        raise ValueError(f"unknown drift {drift!r}")
+    arrs = [np.asarray(r, dtype=np.int64).reshape(-1, 3) for r in rels]
+    if any(a.size and np.abs(a).max() > 32767 for a in arrs):
+        raise ValueError("relative offsets must fit int16")
+    off = np.zeros(len(arrs) + 1, np.int64)
+    off[1:] = np.cumsum([len(a) for a in arrs])
+    rel_d = torch.from_numpy(np.concatenate(arrs).astype(np.int16) if arrs else
+                             np.zeros((0, 3), np.int16)).cuda()
+    w_d = torch.empty(int(off[-1]), dtype=torch.float64, device="cuda")
+    v_d = torch.empty(len(arrs), dtype=torch.float64, device="cuda")
+    m = np.ascontiguousarray(model.as_array(), dtype=np.float64)
+    raise_for_status(_lib.load().vk_solve_systems(
+        rel_d.data_ptr(), off.ctypes.data, len(arrs), _lib.KIND_IDS[model.kind],
+        _lib.DRIFT_IDS[drift], m.ctypes.data, w_d.data_ptr(), v_d.data_ptr(), None,
+        _stream_handle(None)))
+    w = w_d.cpu().numpy()
+    return [w[off[i]:off[i + 1]] for i in range(len(arrs))], v_d.cpu().numpy()
+
+
+def interpolate_voxel(grid: VolumeGrid, target, model: VariogramModel, drift="linear",
+                      inplane: int = 4, z_extent: int = 4,
+                      clamp_range: tuple[float, float] | None = None) -> float:
+    """kriging.py:384-405: one voxel from the known voxels of its
+    (inplane, z_extent) window, clamped to the grid's known range.  The
+    window gather is index arithmetic on the mask; the system is solved on
+    the device (``solve_systems``)."""
+    x, y, z = (int(v) for v in target)
+    data = grid.data.cpu().numpy() if grid.on_device else grid.data
+    mask = grid.missing_mask.cpu().numpy() if grid.on_device else grid.missing_mask
+    if not mask[z, y, x]:
+        return float(data[z, y, x])
+    dz, dy, dx = data.shape
+
+    def win(c, extent, size):                      # kriging.py:334-342
+        return max(0, c - (extent // 2 - 1)), min(size, c + extent // 2 + 1)
+    x0, x1 = win(x, inplane, dx)
+    y0, y1 = win(y, inplane, dy)
+    z0, z1 = win(z, z_extent, dz)
+    kz, ky, kx = np.nonzero(~mask[z0:z1, y0:y1, x0:x1])   # kriging.py:345-357
+    if len(kz) == 0:
+        raise NoKnownNeighbors(f"no known voxel near {(x, y, z)}")
+    coords = np.column_stack([kx + x0, ky + y0, kz + z0])
+    (w,), _ = solve_systems([coords - np.array([x, y, z])], model, drift)
+    pred = float(w @ data[coords[:, 2], coords[:, 1], coords[:, 0]].astype(np.float64))
+    if clamp_range is None:
+        known = data[~mask]
+        clamp_range = (float(known.min()), float(known.max()))
+    return float(np.clip(pred, clamp_range[0], clamp_range[1]))
+
+
 def _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev):
     """Non-plane masks on the device: ``vk_fill_generic`` (window schedule,
     distinct-pattern solves, per-voxel prediction; kriging.py:408-431)."""

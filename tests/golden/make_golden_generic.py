@@ -76,6 +76,28 @@ def main():
         blob[f"{name}/var"] = v
         meta["cases"].append({"name": name, "model": [kind, nug, sill, rng_], "drift": drift,
                               "shape": list(d.shape), "n_missing": int(m.sum())})
+    # interpolate_voxel (kriging.py:384-405) on the first case's grid: a few
+    # targets x windows, own RNG so the cases above do not move
+    name0, d0, m0, (kind0, nug0, sill0, rng0), drift0 = cases()[0]
+    data0 = d0.copy()
+    data0[m0] = np.nan
+    g0 = VolumeGrid(data0, m0)
+    rv = np.random.default_rng(384)
+    vox = []
+    miss = np.argwhere(m0)
+    for t in rv.choice(len(miss), 12, replace=False):
+        z, y, x = (int(v) for v in miss[t])
+        for inplane, z_extent in ((4, 4), (4, 8), (8, 16)):
+            try:
+                val = K.interpolate_voxel(g0, (x, y, z), K.VariogramModel(kind0, nug0, sill0, rng0), drift0,
+                                          inplane, z_extent)
+            except NoKnownNeighbors:
+                val = None
+            vox.append({"target": [x, y, z], "inplane": inplane, "z_extent": z_extent, "value": val})
+    known = np.argwhere(~m0)[0]
+    vox.append({"target": [int(known[2]), int(known[1]), int(known[0])], "inplane": 4, "z_extent": 4,
+                "value": float(data0[tuple(known)])})
+    meta["interpolate_voxel"] = {"case": name0, "voxels": vox}
     # NoKnownNeighbors: nothing known within the widest window of x = 39
     data = np.full((1, 1, 40), np.nan, np.float32)
     data[0, 0, 0] = 5.0

@@ -100,3 +100,40 @@ def test_generic_planes_with_holes_vs_oracle(cuda):
     ref, _ = O.fill_missing(data, mask, O.Model("exponential", 1.0, 9e5, 12.0))
     rng = float(base[~mask].max() - base[~mask].min())
     assert np.abs(got.data.astype(np.float64) - ref).max() <= TOL64 * rng
+
+
+def test_solve_systems_vs_reference_solve_ked(cuda):
+    """vk_solve_systems on the 672 stencil systems the live reference solved
+    with build_system + solve_ked (tests/golden/make_golden.py), batched by
+    model and drift."""
+    from paper_2303_09523_b200 import VariogramModel, solve_systems
+    gold = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
+    with open(os.path.join(HERE, "golden", "reference_golden.json")) as f:
+        meta = json.load(f)
+    groups = {}
+    for s in meta["systems"]:
+        groups.setdefault((tuple(s["model"]), s["drift"]), []).append(s)
+    worst_w = worst_v = 0.0
+    for (model, drift), sys_ in groups.items():
+        kind, nug, sill, rng = model
+        ws, vs = solve_systems([gold[f"sys_{s['id']}_rel"] for s in sys_],
+                               VariogramModel(kind, nug, sill, rng), drift)
+        for s, w, v in zip(sys_, ws, vs):
+            ref = gold[f"sys_{s['id']}_w"]
+            worst_w = max(worst_w, float(np.abs(w - ref).max() / max(1.0, np.abs(ref).max())))
+            worst_v = max(worst_v, abs(v - s["variance"]) / max(abs(s["variance"]), 1e-12 * sill))
+    assert worst_w <= 1e-7, worst_w
+    assert worst_v <= 1e-7, worst_v
+
+
+def test_interpolate_voxel_vs_reference(cuda):
+    from paper_2303_09523_b200 import VolumeGrid, interpolate_voxel
+    d, meta = _golden()
+    iv = meta["interpolate_voxel"]
+    c = next(c for c in meta["cases"] if c["name"] == iv["case"])
+    data, mask = d[f"{iv['case']}/data"], d[f"{iv['case']}/mask"]
+    grid = VolumeGrid(data, mask)
+    rng = float(np.nanmax(data) - np.nanmin(data))
+    for v in iv["voxels"]:
+        got = interpolate_voxel(grid, v["target"], _model(c), c["drift"], v["inplane"], v["z_extent"])
+        assert abs(got - v["value"]) <= 1e-9 * rng, (v, got)
