@@ -198,7 +198,7 @@ def run_reference(args, cfg, ks):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded C4 HDR spine phantom)",
+        "data": _data_desc(cfg),
         "config": _config(cfg, args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
@@ -208,13 +208,26 @@ def run_reference(args, cfg, ks):
     return 0
 
 
+def _data_desc(cfg):
+    return f"synthetic (seeded {cfg.name} phantom, {cfg.quantise} values; no clinical MRI available)"
+
+
+def _l2_desc(cfg):
+    T = cfg.n_known + (cfg.n_known - 1) * (cfg.factor - 1)
+    vin = cfg.n_known * cfg.height * cfg.width * 4 / 1e6
+    vout = T * cfg.height * cfg.width * 4 / 1e6
+    if vin + vout > 126:
+        return (f"no flush: per-GPU inputs {vin:.0f} MB and outputs {vout:.0f} MB exceed the 126 MB L2")
+    return f"inputs {vin:.0f} MB + outputs {vout:.0f} MB fit the 126 MB L2 (small config, no flush)"
+
+
 def _config(cfg, args, world):
     return {"workload": f"{cfg.name} {cfg.height}x{cfg.width}, K={cfg.n_known} known slices/GPU, "
                         f"factor {cfg.factor}, {cfg.n_subparts} Z sub-parts/GPU",
             "kind": "exponential", "drift": "linear", "accum": args.accum,
             "return_variance": bool(args.variance), "max_pairs": 100000, "seed": 0,
             "parallelism": f"zparts x {world} GPU (weak, 1-slice NCCL halo)",
-            "l2": "no flush: per-GPU inputs 268 MB and outputs 2.1 GB exceed the 126 MB L2",
+            "l2": _l2_desc(cfg),
             "pair_draws": "redrawn every step"}
 
 
@@ -350,7 +363,7 @@ def run_gpu(args, cfg, ks):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": DTYPES[args.accum],
-            "data": "synthetic (seeded C4 HDR spine phantom)",
+            "data": _data_desc(cfg),
             "config": _config(cfg, args, world),
             "schedule": "serial" if args.serial else "per-part fit->solve->predict chains",
             "roofline": roof, "stage_ms_serial": stages, "cpu_baseline": cpu, "e2e": e2e,

@@ -114,7 +114,13 @@ constexpr int FT_THREADS = FT_WARPS * 32;
 constexpr int FT_TY = VK_FT_TY;            // tile rows (warps x row steps)
 constexpr int FT_SY = FT_TY + 3;           // smem rows: y0-1 .. y0+33
 constexpr int FT_BUF_FLOATS = ((FT_SX * FT_SY * 4 + 127) / 128) * 128 / 4;
-constexpr int FT_STAGES = 4;
+// Occupancy by gap size: with G <= 4 missing planes the accumulators fit 80
+// registers, so three CTAs share an SM (3-deep ring); larger G keeps 128
+// registers, two CTAs and a 4-deep ring (C5 fp32: 58.9 -> 60.6 % of the HBM
+// roofline; C4 (G = 7) spills at 80 registers and stays at two CTAs).
+constexpr int FT_STAGES_MAX = 4;
+__host__ __device__ constexpr int ft_stages(int G) { return G <= 4 ? 3 : 4; }
+__host__ __device__ constexpr int ft_minb(int G) { return G <= 4 ? 3 : VK_FT_MINB; }
 constexpr int FT_WPARTS = 4;             // parts whose stencils a unit stages
 
 template <typename Acc>
@@ -236,7 +242,7 @@ struct Pair2<float> {
 // FP64 pipe of an SM sub-partition sees a mix of DFMA-heavy and
 // load/convert/store phases instead of all warps in lock step.
 template <int G, typename Acc, bool VAR, int COLS = VK_FT_COLS>
-__global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
+__global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
     predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
                         int n_tiles, int chunk, int n_units) {
   using L = StLayout<G, Acc>;
@@ -244,6 +250,7 @@ __global__ void __launch_bounds__(FT_THREADS, VK_FT_MINB)
   constexpr bool MID = L::MID;
   constexpr int NSTP = L::NSTP;                            // padded: 16-byte aligned taps
   using P2 = typename Pair2<Acc>::T;
+  constexpr int FT_STAGES = ft_stages(G);
   extern __shared__ __align__(128) float ring[];           // FT_STAGES x FT_BUF_FLOATS
   __shared__ __align__(8) uint64_t full[FT_STAGES];
   __shared__ int released[FT_STAGES];                      // warps done with the slot's plane
@@ -581,11 +588,11 @@ int predict_fast_supported(int G, int accum) {
   return G >= 1 && G <= 8;
 }
 
-static size_t fast_smem() { return (size_t)FT_STAGES * FT_BUF_FLOATS * sizeof(float); }
+static size_t fast_smem(int G) { return (size_t)ft_stages(G) * FT_BUF_FLOATS * sizeof(float); }
 
 template <int G, typename Acc>
 static cudaError_t occupancy_t(int* occ) {
-  const size_t smem = fast_smem();
+  const size_t smem = fast_smem(G);
   cudaError_t e = cudaFuncSetAttribute(predict_fast_kernel<G, Acc, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
@@ -613,7 +620,7 @@ cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st) {
 
 template <int G, typename Acc>
 static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
-  const size_t smem = fast_smem();
+  const size_t smem = fast_smem(G);
   const int ntx = (a.W + FT_TX - 1) / FT_TX, nty = (a.H + FT_TY - 1) / FT_TY;
   const int n_tiles = ntx * nty, n_gaps = a.gap1 - a.gap0;
   if (n_gaps <= 0) return cudaSuccess;
