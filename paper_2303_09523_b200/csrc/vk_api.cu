@@ -311,7 +311,11 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
       }
       VK_TRY(p->put(&p->d_jobs, p->jobs));
     }
-    VK_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    {
+      int lo_prio = 0, hi_prio = 0;
+      VK_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+      VK_TRY(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi_prio));
+    }
     VK_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     VK_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   }
@@ -399,35 +403,46 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   // the pair draw depends only on geometry and seed: fork it onto the side
   // stream so it overlaps the plane statistics
   const bool draw = d.fit_variogram && (!p->pairs_ready || (d.flags & VK_FLAG_REDRAW_PAIRS));
-  if (draw) {
+  // chained schedule: the binned semivariogram needs the pair tables and the
+  // data, not the statistics, so it follows the draw on the side stream
+  // (highest priority: the draw's small grids are placed first and the
+  // statistics pass fills the remaining SMs)
+  const bool side_bins = d.fit_variogram && p->chain[0] != nullptr;
+  BinsArgs ba;
+  ba.known = known;
+  ba.values = nullptr;
+  ba.part_base = p->d_part_base;
+  ba.part_class = p->d_part_class;
+  ba.tables = p->d_tables;
+  ba.max_pairs = d.max_pairs;
+  ba.n_bins = d.n_bins;
+  ba.nblk = p->nblk;
+  ba.S = S;
+  ba.partial = p->d_partial;
+  if (draw || side_bins) {
     VK_CUDA(cudaEventRecord(p->ev_fork, st));
     VK_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
-    VK_CUDA(launch_pair_tables(p->d_jobs, p->jobs.data(), (int)p->jobs.size(), p->side));
-    kernels += 5;
-    p->pairs_ready = true;
+    if (draw) {
+      VK_CUDA(launch_pair_tables(p->d_jobs, p->jobs.data(), (int)p->jobs.size(), p->side));
+      kernels += 5;
+      p->pairs_ready = true;
+    }
+    if (side_bins) {
+      VK_CUDA(launch_bins(ba, p->side));
+      ++kernels;
+    }
     VK_CUDA(cudaEventRecord(p->ev_join, p->side));
   }
   VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st));
   ++kernels;
   VK_CUDA(mark(1));
-  if (draw) VK_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));   // "pairs" = residual wait
-  if (d.fit_variogram) {
+  if (draw || side_bins) VK_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));   // "pairs" = residual wait
+  if (d.fit_variogram && !side_bins) {
     VK_CUDA(mark(2));
-    BinsArgs ba;
-    ba.known = known;
-    ba.values = nullptr;
-    ba.part_base = p->d_part_base;
-    ba.part_class = p->d_part_class;
-    ba.tables = p->d_tables;
-    ba.max_pairs = d.max_pairs;
-    ba.n_bins = d.n_bins;
-    ba.nblk = p->nblk;
-    ba.S = S;
-    ba.partial = p->d_partial;
     VK_CUDA(launch_bins(ba, st));
     ++kernels;
   }
-  if (!d.fit_variogram) VK_CUDA(mark(2));
+  if (!d.fit_variogram || side_bins) VK_CUDA(mark(2));
   VK_CUDA(mark(3));
   FitArgs fa;
   fa.S = S;
