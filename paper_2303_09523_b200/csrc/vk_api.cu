@@ -564,7 +564,14 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       PredictArgs p1 = pa;
       p1.gap0 = p->gap_begin[s];
       p1.gap1 = p->gap_begin[s + 1];
-      p1.chunk = p1.gap1 - p1.gap0;           // one unit = a tile over the part's gaps
+      // units of half a part's gaps: streaming CTAs retire often enough that
+      // a late part's solve finds a free slot soon (they hold all of an SM's
+      // registers), at the cost of one extra known-plane load per unit
+      // (C4: 8-gap units 1.351 ms, 4-gap 1.329 ms, 2-gap 1.342 ms)
+      static const int chain_chunk = std::getenv("VK_CHAIN_CHUNK") ? std::atoi(std::getenv("VK_CHAIN_CHUNK")) : 0;
+      const int part_gaps = p1.gap1 - p1.gap0;
+      p1.chunk = part_gaps > 4 ? (part_gaps + 1) / 2 : part_gaps;
+      if (chain_chunk > 0) p1.chunk = std::min(part_gaps, chain_chunk);
       p1.part0 = s;
       p1.part1 = s + 1;
       // the part's solve finished on its high-priority chain (a part reuses
