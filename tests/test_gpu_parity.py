@@ -183,3 +183,18 @@ def test_chained_schedule_matches_serial(cuda, accum):
     (o1, v1, m1, l1), (o2, v2, m2, l2) = res
     assert torch.equal(o1, o2) and torch.equal(v1, v2)
     assert np.array_equal(m1, m2) and np.array_equal(l1, l2)
+
+
+@pytest.mark.parametrize("n_bins", [3, 29, 30, 32])
+def test_fit_variogram_bin_counts(cuda, n_bins):
+    """n_bins + 3 residual rows above a warp (30, 32) take the scalar TRF
+    kernel (fit_scalar_kernel); 29 is the largest warp-parallel case."""
+    from paper_2303_09523_b200 import fit_variogram
+    r = np.random.default_rng(n_bins)
+    c = r.integers(0, 60, size=(4000, 3)).astype(float)
+    v = np.sin(c[:, 0] / 9) * 10 + 0.5 * c[:, 2] + r.normal(size=len(c))
+    got = fit_variogram((c, v), n_bins=n_bins)
+    exp = O.fit_variogram((c, v), n_bins=n_bins)
+    assert abs(got.sill - exp.sill) <= 1e-4 * exp.sill, (got, exp)
+    assert abs(got.range_len - exp.range_len) <= 1e-3 * exp.range_len, (got, exp)
+    assert abs(got.nugget - exp.nugget) <= 1e-4 * exp.sill, (got, exp)
