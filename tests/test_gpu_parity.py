@@ -198,3 +198,31 @@ def test_fit_variogram_bin_counts(cuda, n_bins):
     assert abs(got.sill - exp.sill) <= 1e-4 * exp.sill, (got, exp)
     assert abs(got.range_len - exp.range_len) <= 1e-3 * exp.range_len, (got, exp)
     assert abs(got.nugget - exp.nugget) <= 1e-4 * exp.sill, (got, exp)
+
+
+@pytest.mark.parametrize("kind,drift", [("gaussian", "linear"), ("spherical", "linear"),
+                                        ("exponential", "constant"), ("gaussian", "constant")])
+def test_zpart_pipeline_kinds_and_drifts(cuda, kind, drift):
+    """Per-part fit + fill for every variogram kind and both drifts against
+    the oracle's Z-part pipeline: strict with the oracle's models, fit fuzz
+    end to end."""
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("brain", 48, 64, 9, 4, n_subparts=2, seed=31)
+    ks = known_slices(cfg)
+    kd = torch.from_numpy(ks).cuda()
+    ref, _, rmodels = O.reconstruct_zparts(ks, cfg.factor, cfg.n_subparts, kind=kind, drift=drift)
+    rng = _rng(ks)
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts, kind=kind,
+                      drift=drift)
+    out, _ = zk.run(kd)
+    models, _ = zk.finish()
+    assert np.abs(out.cpu().numpy().astype(np.float64) - ref).max() <= FIT_FUZZ * rng
+    for m, r in zip(models, rmodels):
+        assert abs(m.sill - r.sill) <= 1e-3 * r.sill, (m, r)
+    zf = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts, kind=kind,
+                      drift=drift, fit=False)
+    of, _ = zf.run(kd, models=[VariogramModel(kind, m.nugget, m.sill, m.range_len) for m in rmodels])
+    zf.finish()
+    assert np.abs(of.cpu().numpy().astype(np.float64) - ref).max() <= TOL64 * rng
