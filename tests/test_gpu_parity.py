@@ -226,3 +226,26 @@ def test_zpart_pipeline_kinds_and_drifts(cuda, kind, drift):
     of, _ = zf.run(kd, models=[VariogramModel(kind, m.nugget, m.sill, m.range_len) for m in rmodels])
     zf.finish()
     assert np.abs(of.cpu().numpy().astype(np.float64) - ref).max() <= TOL64 * rng
+
+
+@pytest.mark.parametrize("f", [2, 4, 8])
+@pytest.mark.parametrize("accum", ["fp64", "fp32"])
+def test_streaming_variance_all_fast_gaps(cuda, f, accum):
+    """The streaming kernel's variance instantiation (VAR = true) for every
+    fast-path gap size G = f - 1, against the oracle's kriging variance."""
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("spine", 37, 136, 6, f, n_subparts=2, seed=40 + f)
+    ks = known_slices(cfg)
+    ref, rvar, rmodels = O.reconstruct_zparts(ks, cfg.factor, cfg.n_subparts, return_variance=True)
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts, accum=accum,
+                      fit=False)
+    assert zk.plan.info["fast_path"] == 1
+    out, var = zk.run(torch.from_numpy(ks).cuda(), return_variance=True,
+                      models=[VariogramModel("exponential", m.nugget, m.sill, m.range_len)
+                              for m in rmodels])
+    zk.finish()
+    tol = TOL64 if accum == "fp64" else TOL32
+    assert np.abs(out.cpu().numpy().astype(np.float64) - ref).max() <= tol * _rng(ks)
+    assert np.allclose(var.cpu().numpy(), rvar, rtol=1e-7, atol=1e-9 * max(m.sill for m in rmodels))
