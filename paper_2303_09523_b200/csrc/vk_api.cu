@@ -79,6 +79,7 @@ struct vk_plan {
   ChunkStat* d_stats = nullptr;
   double *d_partial = nullptr, *d_models = nullptr, *d_lohi = nullptr, *d_weights = nullptr, *d_var = nullptr;
   double* d_kpm = nullptr;
+  int* d_inexact = nullptr;           // stats pass: any known value not an integer below 2^23
   uint32_t* d_fxb = nullptr;           // fixed path tables
   float *d_fxc = nullptr, *d_fxq = nullptr;
   int max_chunk = 0;                  // fast path: a run of this many gaps spans <= 4 parts
@@ -273,6 +274,7 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   VK_TRY(p->alloc(&p->d_weights, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK) * WPAD));
   VK_TRY(p->alloc(&p->d_var, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK)));
   if (g.fast) VK_TRY(p->alloc(&p->d_kpm, kpm_elems(S, std::max(1, p->NK))));
+  VK_TRY(p->alloc(&p->d_inexact, (size_t)1));
   if (g.fast && d->accum == VK_ACCUM_FIXED) {
     VK_TRY(p->alloc(&p->d_fxb, fxb_words(S, std::max(1, p->NK))));
     VK_TRY(p->alloc(&p->d_fxc, fxc_floats(S, std::max(1, p->NK))));
@@ -433,7 +435,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     }
     VK_CUDA(cudaEventRecord(p->ev_join, p->side));
   }
-  VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st));
+  VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st, p->d_inexact));
   ++kernels;
   VK_CUDA(mark(1));
   if (draw || side_bins) VK_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));   // "pairs" = residual wait
@@ -518,6 +520,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   pa.part1 = S;
   pa.max_chunk = p->max_chunk;
   pa.kpm = p->d_kpm;
+  pa.sd_inexact = p->d_inexact;
   pa.S = S;
   pa.fxb = p->d_fxb;
   pa.fxc = p->d_fxc;

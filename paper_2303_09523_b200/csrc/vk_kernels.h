@@ -37,8 +37,8 @@ struct SampleGeom {
   int32_t W;
 };
 
-cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out,
-                               int nchunk, cudaStream_t st);
+cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out, int nchunk,
+                               cudaStream_t st, int* inexact = nullptr);
 // One pair class to draw (numpy-identical PCG64 + Lemire; triu when all
 // pairs fit), with its table and the sample geometry for the lags.
 struct PairJob {
@@ -130,6 +130,8 @@ struct PredictArgs {
   void* fxq;                   // fixed path: float4 quantisation (L, 1/step, step, 0)
   int max_chunk;               // gaps per unit so that a unit spans <= 4 parts (0: none)
   void* kpm;                   // [S][NK][16][NSTP] Acc mirror-pair stencils (fast path)
+  const int* sd_inexact;       // device flag from the stats pass: 0 -> every known value is an
+                               // integer below 2^23, so A +- B is exact in fp32
   int num_sms;
 };
 // doubles the K+- table needs (fast path)

@@ -338,6 +338,9 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
       mbar_wait(&full[sq_b % FT_STAGES], (sq_b / FT_STAGES) & 1);
       const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
       const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
+      const bool sd_exact = a.sd_inexact != nullptr && *a.sd_inexact == 0;
+      auto row_steps = [&](auto exact_c) {
+      constexpr bool EXACT = decltype(exact_c)::value;
 #pragma unroll 1
       for (int rs = 0; rs < FT_TY / WY; ++rs) {
         const int r = wy + rs * WY;                        // tile row (warp-uniform)
@@ -394,9 +397,16 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
           Acc S[COLS + 3], D[COLS + 3];                    // exact in fp64
 #pragma unroll
           for (int i = 0; i < COLS + 3; ++i) {
-            const Acc x = AccVec<Acc>::cvt(fa[i]), y = AccVec<Acc>::cvt(fb[i]);
-            S[i] = x + y;
-            D[i] = x - y;
+            if constexpr (EXACT) {
+              // integer data below 2^23: fa +- fb is exact in fp32, so the two
+              // DADDs leave the FP64 pipe (same S, D bits)
+              S[i] = (Acc)(fa[i] + fb[i]);
+              D[i] = (Acc)(fa[i] - fb[i]);
+            } else {
+              const Acc x = AccVec<Acc>::cvt(fa[i]), y = AccVec<Acc>::cvt(fb[i]);
+              S[i] = x + y;
+              D[i] = x - y;
+            }
           }
 #pragma unroll
           for (int ox = -1; ox <= 2; ++ox) {
@@ -485,6 +495,13 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
             }
           }
         }
+      }
+      };
+      if constexpr (std::is_same<Acc, double>::value) {
+        if (sd_exact) row_steps(std::true_type{});
+        else row_steps(std::false_type{});
+      } else {
+        row_steps(std::false_type{});
       }
       // ---- border columns x in {0, W-2, W-1}: one thread per (row, column),
       // all G planes with the column's window kind, same mirror-pair form

@@ -41,7 +41,8 @@ __device__ __forceinline__ double warp_max(double v) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ data, int64_t P,
-                                                          int nchunk, ChunkStat* __restrict__ out) {
+                                                          int nchunk, ChunkStat* __restrict__ out,
+                                                          int* __restrict__ inexact) {
   const int k = blockIdx.y, c = blockIdx.x;
   const int64_t beg = (int64_t)c * STATS_CHUNK;
   const int64_t end = min(P, beg + (int64_t)STATS_CHUNK);
@@ -56,6 +57,7 @@ __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ 
     mn = fmin(mn, v);
     mx = fmax(mx, v);
   };
+  bool notint = false;
   const bool vec = sizeof(T) == 4 && ((P & 3) == 0) && ((end - beg) & 3) == 0;
   if (vec) {
     // 128-bit loads, 4 in flight per thread
@@ -72,11 +74,22 @@ __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ 
       for (int u = 0; u < 4; ++u) {
         if (i + (int64_t)u * blockDim.x >= n4) continue;
         take(v[u].x); take(v[u].y); take(v[u].z); take(v[u].w);
+        // integer-valued with |v| < 2^23: A +- B of two such values is exact
+        // in fp32 (the streaming kernel's fp64 path then forms S, D in fp32)
+        notint |= (v[u].x != rintf(v[u].x)) | (fabsf(v[u].x) >= 8388608.0f) |
+                  (v[u].y != rintf(v[u].y)) | (fabsf(v[u].y) >= 8388608.0f) |
+                  (v[u].z != rintf(v[u].z)) | (fabsf(v[u].z) >= 8388608.0f) |
+                  (v[u].w != rintf(v[u].w)) | (fabsf(v[u].w) >= 8388608.0f);
       }
     }
   } else {
-    for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) take((double)p[i]);
+    for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+      const double dv = (double)p[i];
+      take(dv);
+      notint |= (dv != rint(dv)) | (fabs(dv) >= 8388608.0);
+    }
   }
+  if (inexact && __syncthreads_or(notint) && threadIdx.x == 0) atomicOr(inexact, 1);
   __shared__ double sh[5][8];
   s1 = warp_sum(s1); s2 = warp_sum(s2); bad = warp_sum(bad);
   mn = warp_min(mn); mx = warp_max(mx);
@@ -468,16 +481,20 @@ extern "C" int vk_debug_fit_profile(unsigned long long* out, int reset) {
 #endif
 
 cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out, int nchunk,
-                               cudaStream_t st) {
+                               cudaStream_t st, int* inexact) {
   dim3 grid(nchunk, K);
-  plane_stats_kernel<float><<<grid, 256, 0, st>>>(known, P, nchunk, out);
+  if (inexact) {
+    cudaError_t e = cudaMemsetAsync(inexact, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
+  plane_stats_kernel<float><<<grid, 256, 0, st>>>(known, P, nchunk, out, inexact);
   return cudaGetLastError();
 }
 
 cudaError_t launch_plane_stats_f64(const double* values, int64_t m, ChunkStat* out, int nchunk,
                                    cudaStream_t st) {
   dim3 grid(nchunk, 1);
-  plane_stats_kernel<double><<<grid, 256, 0, st>>>(values, m, nchunk, out);
+  plane_stats_kernel<double><<<grid, 256, 0, st>>>(values, m, nchunk, out, nullptr);
   return cudaGetLastError();
 }
 

@@ -249,3 +249,31 @@ def test_streaming_variance_all_fast_gaps(cuda, f, accum):
     tol = TOL64 if accum == "fp64" else TOL32
     assert np.abs(out.cpu().numpy().astype(np.float64) - ref).max() <= tol * _rng(ks)
     assert np.allclose(var.cpu().numpy(), rvar, rtol=1e-7, atol=1e-9 * max(m.sill for m in rmodels))
+
+
+def test_integer_data_fast_sd_path_is_bit_identical(cuda):
+    """Integer-valued known planes take the fp32 S/D form in the fp64
+    streaming kernel (A +- B exact in fp32); one non-integer voxel switches the
+    whole volume to the general form.  Voxels whose windows do not reach the
+    changed voxel must come out bit-identical from both."""
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("spine", 64, 128, 9, 8, n_subparts=1, seed=77)
+    ks = known_slices(cfg)
+    assert np.array_equal(ks, np.rint(ks))
+    ks2 = ks.copy()
+    ks2[8, 60, 120] += 0.5                         # last known plane, far corner
+    lo, hi = ks.min(), ks.max()
+    assert lo < ks2[8, 60, 120] < hi
+    m = [VariogramModel("exponential", 1.0, 900.0, 12.0)]
+    outs = []
+    for data in (ks, ks2):
+        zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, 1, fit=False)
+        o, _ = zk.run(torch.from_numpy(data).cuda(), models=m)
+        zk.finish()
+        outs.append(o.cpu().numpy())
+    a, b = outs
+    # gaps 0..6 never read plane 8; rows/cols away from (60, 120) in gap 7
+    assert np.array_equal(a[:7 * cfg.factor + 1], b[:7 * cfg.factor + 1])
+    assert np.array_equal(a[:, :50], b[:, :50])
