@@ -118,7 +118,6 @@ constexpr int FT_BUF_FLOATS = ((FT_SX * FT_SY * 4 + 127) / 128) * 128 / 4;
 // registers, so three CTAs share an SM (3-deep ring); larger G keeps 128
 // registers, two CTAs and a 4-deep ring (C5 fp32: 58.9 -> 60.6 % of the HBM
 // roofline; C4 (G = 7) spills at 80 registers and stays at two CTAs).
-constexpr int FT_STAGES_MAX = 4;
 __host__ __device__ constexpr int ft_stages(int G) { return G <= 4 ? 3 : 4; }
 __host__ __device__ constexpr int ft_minb(int G) { return G <= 4 ? 3 : VK_FT_MINB; }
 constexpr int FT_WPARTS = 4;             // parts whose stencils a unit stages
