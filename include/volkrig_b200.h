@@ -218,6 +218,21 @@ int vk_crc32(const void* data, int64_t n_bytes, uint32_t crc_in, uint32_t* crc_o
 int vk_packbits(const uint8_t* mask, int64_t n, uint8_t* bits, void* stream);
 int vk_unpackbits(const uint8_t* bits, int64_t n, uint8_t* mask, void* stream);
 
+/* Slice stack decode and normalisation -- _decode_slice + normalize_stack
+ * (io.py:108-125, model.py:189-202).  `raw` holds n device samples of one
+ * type: VK_SAMPLE_U8 (PIL "L"/"P"/"1" after convert("L"), / 255),
+ * VK_SAMPLE_U16 ("I;16", / 65535), VK_SAMPLE_I32 ("I", f32(v) / 65535) or
+ * VK_SAMPLE_F32 (already decoded).  vk_decode_samples writes the decoded f32
+ * values; vk_normalize_stack decodes, reduces the global min/max and writes
+ * (v - lo) / f32(hi - lo) in f32 (all zeros when hi == lo), bit-identical to
+ * numpy.  `minmax` is a device int[2] scratch (ordered-integer keys of lo and
+ * hi on return); it may be NULL (the library then allocates stream-ordered
+ * scratch).  `out` may alias `raw` for VK_SAMPLE_F32 only.  Asynchronous. */
+enum { VK_SAMPLE_U8 = 0, VK_SAMPLE_U16 = 1, VK_SAMPLE_I32 = 2, VK_SAMPLE_F32 = 3 };
+int vk_decode_samples(const void* raw, int32_t sample_type, int64_t n, float* out, void* stream);
+int vk_normalize_stack(const void* raw, int32_t sample_type, int64_t n, float* out, int32_t* minmax,
+                       void* stream);
+
 const char* vk_status_string(int status);
 /* Message of the last failing call on this thread (for exceptions). */
 const char* vk_last_error(void);

@@ -13,6 +13,7 @@ from .kriging import (KrigingPlan, VariogramModel, fill_missing, fit_variogram,
 from .block_pipeline import ZPartKriging, reconstruct_zparts, subpart_ranges
 from .blocks import BlockDescriptor, BlockKriging, partition, reconstruct_blocks
 from .volume_io import load_volume, save_volume
+from .stack_io import StackManifest, load_stack, normalize_stack, parse_manifest, write_manifest
 
 __all__ = [
     "DegenerateLags", "DeviceError", "DeviceUnsupported", "InsufficientSamples",
@@ -21,5 +22,6 @@ __all__ = [
     "VariogramModel", "fill_missing", "fit_variogram", "interpolate_voxel", "solve_systems",
     "ZPartKriging",
     "reconstruct_zparts", "subpart_ranges", "BlockDescriptor", "BlockKriging", "partition",
-    "reconstruct_blocks", "load_volume", "save_volume",
+    "reconstruct_blocks", "load_volume", "save_volume", "StackManifest", "load_stack",
+    "normalize_stack", "parse_manifest", "write_manifest",
 ]

@@ -85,6 +85,8 @@ SIGNATURES = {
     "vk_crc32": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint32, C.POINTER(C.c_uint32), C.c_void_p]),
     "vk_packbits": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "vk_unpackbits": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vk_decode_samples": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p]),
+    "vk_normalize_stack": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vk_status_string": (C.c_char_p, [C.c_int]),
     "vk_last_error": (C.c_char_p, []),
     "vk_abi_version": (C.c_int, []),

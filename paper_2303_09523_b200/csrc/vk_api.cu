@@ -697,6 +697,30 @@ int vk_unpackbits(const uint8_t* bits, int64_t n, uint8_t* mask, void* stream) {
   return VK_OK;
 }
 
+int vk_decode_samples(const void* raw, int32_t sample_type, int64_t n, float* out, void* stream) {
+  if (sample_type < VK_SAMPLE_U8 || sample_type > VK_SAMPLE_F32 || n < 0)
+    return set_err(VK_E_INVALID_ARGUMENT, "bad sample type / count");
+  if ((!raw || !out) && n > 0) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  VK_CUDA(decode_samples_device(raw, sample_type, n, out, (cudaStream_t)stream));
+  return VK_OK;
+}
+
+int vk_normalize_stack(const void* raw, int32_t sample_type, int64_t n, float* out, int32_t* minmax,
+                       void* stream) {
+  if (sample_type < VK_SAMPLE_U8 || sample_type > VK_SAMPLE_F32 || n < 0)
+    return set_err(VK_E_INVALID_ARGUMENT, "bad sample type / count");
+  if ((!raw || !out) && n > 0) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  if (out == raw && sample_type != VK_SAMPLE_F32 && n > 0)
+    return set_err(VK_E_INVALID_ARGUMENT, "in-place normalisation needs f32 samples");
+  cudaStream_t st = (cudaStream_t)stream;
+  int* keys = minmax;
+  if (!keys) VK_CUDA(cudaMallocAsync((void**)&keys, 2 * sizeof(int), st));
+  const cudaError_t e = normalize_stack_device(raw, sample_type, n, out, keys, st);
+  if (!minmax) cudaFreeAsync(keys, st);
+  VK_CUDA(e);
+  return VK_OK;
+}
+
 int vk_plan_set_timing(vk_plan* p, int ring) {
   if (!p || ring < 0) return set_err(VK_E_INVALID_ARGUMENT, "bad plan / ring");
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);

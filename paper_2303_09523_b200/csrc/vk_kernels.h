@@ -174,6 +174,9 @@ GenericResult fill_generic(const float* data, const uint8_t* mask, int T, int H,
 cudaError_t crc32_device(const void* data, int64_t n, uint32_t crc_in, uint32_t* crc_out, cudaStream_t st);
 cudaError_t packbits_device(const uint8_t* mask, int64_t n, uint8_t* bits, cudaStream_t st);
 cudaError_t unpackbits_device(const uint8_t* bits, int64_t n, uint8_t* mask, cudaStream_t st);
+cudaError_t decode_samples_device(const void* raw, int sample_type, int64_t n, float* out, cudaStream_t st);
+cudaError_t normalize_stack_device(const void* raw, int sample_type, int64_t n, float* out, int* keys,
+                                   cudaStream_t st);
 inline size_t fxb_words(int S, int NK) { return (size_t)S * (size_t)NK * 32 * 8; }
 inline size_t fxc_floats(int S, int NK) { return (size_t)S * (size_t)NK * 8 * 4; }
 

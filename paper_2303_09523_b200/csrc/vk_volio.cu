@@ -3,6 +3,13 @@
 // and final xor 0xFFFFFFFF) and the missing-mask bit packing of
 // np.packbits / np.unpackbits (big-endian bit order, zero-padded last byte).
 //
+// Slice decode + normalisation of load_stack (io.py:108-143, model.py:189-202)
+// on the device: raw PNG samples (u8 "L", u16 "I;16", i32 "I") or already
+// decoded f32 are converted exactly as numpy does it (f32(sample) / 255 or
+// / 65535, IEEE division in f32), the global min/max are reduced as ordered
+// integer keys, and out = (v - lo) / f32(double(hi) - double(lo)) in f32, or
+// 0 for a constant stack.  Two passes over the raw samples, no host sync.
+//
 // CRC over n bytes at HBM speed: one thread per 16 KB chunk computes the raw
 // CRC of its chunk (register starting at 0) with slicing-by-16 tables in
 // shared memory; chunk CRCs are merged pairwise, bottom-up, by
@@ -11,8 +18,10 @@
 // zlib publishes as crc32_combine).  Continuing from a previous CRC c:
 //   crc32(data, c) = ~(raw(data) ^ shift(~c, |data|)).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 #include <vector>
+#include "../../include/volkrig_b200.h"
 #include "vk_kernels.h"
 
 namespace vk {
@@ -136,7 +145,229 @@ __global__ void unpackbits_kernel(const uint8_t* __restrict__ bits, int64_t n, u
     mask[i] = (bits[i >> 3] >> (7 - (i & 7))) & 1;
 }
 
+// monotone float <-> signed int key (total order of non-NaN floats)
+__device__ __forceinline__ int f2key(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float key2f(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+
+// Sample traits: raw type, samples per 16-byte vector, decode, and an integer
+// order key.  Decoding is monotone in the raw value (int -> f32 and a
+// correctly rounded division by a positive constant both are), so the min/max
+// pass reduces raw integers and decodes only the two extremes.
+template <int T> struct Samp;
+template <> struct Samp<VK_SAMPLE_U8> {
+  using raw_t = uint8_t;
+  static __device__ __forceinline__ float decode(raw_t v) { return __fdiv_rn((float)v, 255.0f); }
+  static __device__ __forceinline__ int key(raw_t v) { return v; }
+  static __device__ __forceinline__ float value(int k) { return __fdiv_rn((float)k, 255.0f); }
+};
+template <> struct Samp<VK_SAMPLE_U16> {
+  using raw_t = uint16_t;
+  static __device__ __forceinline__ float decode(raw_t v) { return __fdiv_rn((float)v, 65535.0f); }
+  static __device__ __forceinline__ int key(raw_t v) { return v; }
+  static __device__ __forceinline__ float value(int k) { return __fdiv_rn((float)k, 65535.0f); }
+};
+template <> struct Samp<VK_SAMPLE_I32> {
+  using raw_t = int32_t;
+  static __device__ __forceinline__ float decode(raw_t v) { return __fdiv_rn(__int2float_rn(v), 65535.0f); }
+  static __device__ __forceinline__ int key(raw_t v) { return v; }
+  static __device__ __forceinline__ float value(int k) { return __fdiv_rn(__int2float_rn(k), 65535.0f); }
+};
+template <> struct Samp<VK_SAMPLE_F32> {
+  using raw_t = float;
+  static __device__ __forceinline__ float decode(raw_t v) { return v; }
+  static __device__ __forceinline__ int key(raw_t v) { return f2key(v); }
+  static __device__ __forceinline__ float value(int k) { return key2f(k); }
+};
+
+constexpr int EW_THREADS = 256;
+constexpr int EW_UNROLL = 4;    // 16-byte vectors in flight per thread
+
+template <int T>
+union Vec16 {
+  uint4 q;
+  typename Samp<T>::raw_t s[16 / sizeof(typename Samp<T>::raw_t)];
+};
+
+__global__ void init_keys_kernel(int* keys) {
+  if (threadIdx.x == 0) {
+    keys[0] = 0x7fffffff;
+    keys[1] = (int)0x80000000;
+  }
+}
+
+// Pass 1: min/max order keys.  nvec 16-byte vectors (0 when the buffer is
+// not 16-byte aligned), then the scalar tail [nvec * V, n).
+template <int T>
+__global__ void __launch_bounds__(EW_THREADS) minmax_kernel(const void* __restrict__ raw, int64_t n, int64_t nvec,
+                                                            int* __restrict__ keys) {
+  using S = Samp<T>;
+  using raw_t = typename S::raw_t;
+  constexpr int V = 16 / sizeof(raw_t);
+  int lo = 0x7fffffff, hi = (int)0x80000000;
+  const uint4* vec = reinterpret_cast<const uint4*>(raw);
+  const int64_t step = (int64_t)gridDim.x * EW_THREADS * EW_UNROLL;
+  for (int64_t base = (int64_t)blockIdx.x * EW_THREADS * EW_UNROLL + threadIdx.x; base < nvec; base += step) {
+    Vec16<T> v[EW_UNROLL];
+#pragma unroll
+    for (int u = 0; u < EW_UNROLL; ++u) {
+      const int64_t i = base + (int64_t)u * EW_THREADS;
+      v[u].q = __ldcs(vec + (i < nvec ? i : base));   // out-of-range lanes re-read `base`: harmless for min/max
+    }
+#pragma unroll
+    for (int u = 0; u < EW_UNROLL; ++u)
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const raw_t x = v[u].s[j];
+        if (T == VK_SAMPLE_F32 && !(x == x)) continue;
+        lo = min(lo, S::key(x));
+        hi = max(hi, S::key(x));
+      }
+  }
+  const raw_t* r = reinterpret_cast<const raw_t*>(raw);
+  for (int64_t i = nvec * V + (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * EW_THREADS) {
+    const raw_t x = r[i];
+    if (T == VK_SAMPLE_F32 && !(x == x)) continue;
+    lo = min(lo, S::key(x));
+    hi = max(hi, S::key(x));
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ int s[2][EW_THREADS / 32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s[0][w] = lo;
+    s[1][w] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < EW_THREADS / 32; ++k) {
+      lo = min(lo, s[0][k]);
+      hi = max(hi, s[1][k]);
+    }
+    if (lo <= hi) {                           // decoded keys of this block's extremes
+      atomicMin(keys, f2key(S::value(lo)));
+      atomicMax(keys + 1, f2key(S::value(hi)));
+    }
+  }
+}
+
+// Pass 2 (RESCALE) or plain decode: out = decode(raw) or
+// (decode(raw) - lo) / f32(double(hi) - double(lo)), 0 for a flat stack.
+// Each thread loads EW_UNROLL vectors before storing any, so out may alias
+// raw (f32 in place: every element is read and written by one thread).
+template <int T, bool RESCALE>
+__global__ void __launch_bounds__(EW_THREADS) map_kernel(const void* raw, int64_t n, int64_t nvec,
+                                                         const int* __restrict__ keys, float* out) {
+  using S = Samp<T>;
+  using raw_t = typename S::raw_t;
+  constexpr int V = 16 / sizeof(raw_t);
+  float lo = 0.0f, range = 1.0f;
+  bool flat = false;
+  if (RESCALE) {
+    lo = key2f(keys[0]);
+    const float hi = key2f(keys[1]);
+    flat = !(hi > lo);
+    range = (float)((double)hi - (double)lo);   // a Python float, cast to f32 by numpy
+  }
+  auto f = [&](raw_t x) {
+    const float d = S::decode(x);
+    return RESCALE ? (flat ? 0.0f : __fdiv_rn(__fsub_rn(d, lo), range)) : d;
+  };
+  const uint4* vec = reinterpret_cast<const uint4*>(raw);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  const int64_t step = (int64_t)gridDim.x * EW_THREADS * EW_UNROLL;
+  for (int64_t base = (int64_t)blockIdx.x * EW_THREADS * EW_UNROLL + threadIdx.x; base < nvec; base += step) {
+    Vec16<T> v[EW_UNROLL];
+#pragma unroll
+    for (int u = 0; u < EW_UNROLL; ++u) {
+      const int64_t i = base + (int64_t)u * EW_THREADS;
+      if (i < nvec) v[u].q = __ldcs(vec + i);
+    }
+#pragma unroll
+    for (int u = 0; u < EW_UNROLL; ++u) {
+      const int64_t i = base + (int64_t)u * EW_THREADS;
+      if (i >= nvec) break;
+#pragma unroll
+      for (int j = 0; j < V; j += 4)
+        __stcs(o4 + i * (V / 4) + j / 4,
+               make_float4(f(v[u].s[j]), f(v[u].s[j + 1]), f(v[u].s[j + 2]), f(v[u].s[j + 3])));
+    }
+  }
+  const raw_t* r = reinterpret_cast<const raw_t*>(raw);
+  for (int64_t i = nvec * V + (int64_t)blockIdx.x * EW_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * EW_THREADS)
+    out[i] = f(r[i]);
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// grid: enough CTAs for every vector once, capped at 8 resident CTAs per SM
+int map_grid(int64_t nvec, int64_t n) {
+  const int64_t per = (int64_t)EW_THREADS * EW_UNROLL;
+  const int64_t need = nvec > 0 ? (nvec + per - 1) / per : (n + EW_THREADS - 1) / EW_THREADS;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sm_count() * 8));
+}
+
+template <int T>
+int64_t n_vectors(const void* raw, const float* out, int64_t n) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(raw) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  return aligned ? n / (16 / (int64_t)sizeof(typename Samp<T>::raw_t)) : 0;
+}
+
+template <int T>
+void launch_decode(const void* raw, int64_t n, float* out, cudaStream_t st) {
+  const int64_t nv = n_vectors<T>(raw, out, n);
+  map_kernel<T, false><<<map_grid(nv, n), EW_THREADS, 0, st>>>(raw, n, nv, nullptr, out);
+}
+
+template <int T>
+void launch_normalize(const void* raw, int64_t n, float* out, int* keys, cudaStream_t st) {
+  const int64_t nv = n_vectors<T>(raw, out, n);
+  const int g = map_grid(nv, n);
+  minmax_kernel<T><<<g, EW_THREADS, 0, st>>>(raw, n, nv, keys);
+  map_kernel<T, true><<<g, EW_THREADS, 0, st>>>(raw, n, nv, keys, out);
+}
+
 }  // namespace
+
+cudaError_t decode_samples_device(const void* raw, int sample_type, int64_t n, float* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  switch (sample_type) {
+    case VK_SAMPLE_U8: launch_decode<VK_SAMPLE_U8>(raw, n, out, st); break;
+    case VK_SAMPLE_U16: launch_decode<VK_SAMPLE_U16>(raw, n, out, st); break;
+    case VK_SAMPLE_I32: launch_decode<VK_SAMPLE_I32>(raw, n, out, st); break;
+    case VK_SAMPLE_F32: launch_decode<VK_SAMPLE_F32>(raw, n, out, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t normalize_stack_device(const void* raw, int sample_type, int64_t n, float* out, int* keys,
+                                   cudaStream_t st) {
+  init_keys_kernel<<<1, 32, 0, st>>>(keys);
+  if (n <= 0) return cudaGetLastError();
+  switch (sample_type) {
+    case VK_SAMPLE_U8: launch_normalize<VK_SAMPLE_U8>(raw, n, out, keys, st); break;
+    case VK_SAMPLE_U16: launch_normalize<VK_SAMPLE_U16>(raw, n, out, keys, st); break;
+    case VK_SAMPLE_I32: launch_normalize<VK_SAMPLE_I32>(raw, n, out, keys, st); break;
+    case VK_SAMPLE_F32: launch_normalize<VK_SAMPLE_F32>(raw, n, out, keys, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t crc32_device(const void* data, int64_t n, uint32_t crc_in, uint32_t* crc_out, cudaStream_t st) {
   static const Tables host_tables = make_tables();

@@ -29,9 +29,22 @@ def missing_planes_per_gap(slice_gap_mm: float, pixel_spacing_mm: float) -> int:
     return max(0, int(np.floor(slice_gap_mm / pixel_spacing_mm + 0.5)) - 1)
 
 
+def check_stack_meta(shape, pixel_spacing, slice_gap_mm, axis_label) -> None:
+    """The shape/spacing/axis checks of SliceStack.__post_init__ (model.py:37-44),
+    in order; callable before any sample is on the device."""
+    if len(shape) != 3 or shape[0] < 2:
+        raise EmptyStack("a stack needs at least 2 slices of equal size")
+    if slice_gap_mm <= 0 or min(pixel_spacing) <= 0:
+        raise NonPositiveSpacing("spacing and gap must be > 0")
+    if axis_label not in AXIS_LABELS:
+        raise ValueError(f"axis_label must be one of {AXIS_LABELS}")
+
+
 @dataclass
 class SliceStack:
-    """Registered 2D slices along one axis -- model.py:23-68."""
+    """Registered 2D slices along one axis -- model.py:23-68.  ``slices`` is a
+    float32 ``[n, h, w]`` numpy array or CUDA tensor (``load_stack`` returns
+    the device form)."""
 
     slices: np.ndarray
     pixel_spacing: tuple[float, float]
@@ -39,19 +52,35 @@ class SliceStack:
     axis_label: str = "axial"
 
     def __post_init__(self):
-        self.slices = np.ascontiguousarray(self.slices, dtype=np.float32)
-        if self.slices.ndim != 3 or self.slices.shape[0] < 2:
-            raise EmptyStack("a stack needs at least 2 slices of equal size")
-        if self.slice_gap_mm <= 0 or min(self.pixel_spacing) <= 0:
-            raise NonPositiveSpacing("spacing and gap must be > 0")
-        if self.axis_label not in AXIS_LABELS:
-            raise ValueError(f"axis_label must be one of {AXIS_LABELS}")
-        if not np.isfinite(self.slices).all():
+        if _is_torch(self.slices):
+            import torch
+            self.slices = self.slices.to(torch.float32).contiguous()
+        else:
+            self.slices = np.ascontiguousarray(self.slices, dtype=np.float32)
+        check_stack_meta(tuple(self.slices.shape), self.pixel_spacing, self.slice_gap_mm, self.axis_label)
+        if _is_torch(self.slices):
+            import torch
+            finite = bool(torch.isfinite(self.slices).all())
+        else:
+            finite = bool(np.isfinite(self.slices).all())
+        if not finite:
             raise ValueError("slice values must be finite")
+
+    @property
+    def on_device(self) -> bool:
+        return _is_torch(self.slices)
 
     @property
     def n(self) -> int:
         return self.slices.shape[0]
+
+    @property
+    def height(self) -> int:
+        return self.slices.shape[1]
+
+    @property
+    def width(self) -> int:
+        return self.slices.shape[2]
 
     @property
     def missing_per_gap(self) -> int:
