@@ -116,6 +116,17 @@ void vk_plan_destroy(vk_plan* plan);
 int vk_plan_execute(vk_plan* plan, const float* known, const double* models,
                     float* out, double* var, void* stream);
 
+/* Copies a reconstructed volume to host memory, as the reference's
+ * fill_missing returns it (kriging.py:481-496): the interpolated planes come
+ * from the device volume `out_dev` (one strided device-to-host copy on a
+ * regular layout), the known planes from the caller's host input
+ * `known_host` ([n_known][H][W], the device holds bit-identical copies of
+ * them), copied host to host on a plan-owned stream concurrently with the
+ * download.  Stream-ordered on `stream`; pinned `out_host` / `known_host`
+ * make it asynchronous.  Device-to-host bytes: the interpolated planes only. */
+int vk_plan_download(vk_plan* plan, const float* out_dev, const float* known_host, float* out_host,
+                     void* stream);
+
 /* Synchronises the stream, maps device-side statuses to a vk_status.
  * failed_part: first failing sub-part or -1.  models_out: host f64 [S][3]
  * fitted (or supplied) models, may be NULL.  lohi_out: host f64 [S][2] clamp

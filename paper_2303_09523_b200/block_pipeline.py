@@ -100,6 +100,11 @@ class ZPartKriging:
         self.plan.execute(known, out, var, models=models, stream=stream)
         return out, var
 
+    def download(self, out, known_host, out_host=None, stream=None):
+        """Volume to host memory, known planes taken from the host input
+        (``KrigingPlan.download``)."""
+        return self.plan.download(out, known_host, out_host, stream)
+
     def finish(self, stream=None):
         models, lohi = self.plan.finish(stream)
         return [VariogramModel(self.kind, *map(float, m)) for m in models], lohi
@@ -112,13 +117,19 @@ def reconstruct_zparts(slices, factor: int, n_subparts: int, kind: str = "expone
     -> (volume, variance or None, models).  numpy in, numpy out."""
     torch = _torch()
     host = isinstance(slices, np.ndarray)
-    known = (torch.from_numpy(np.ascontiguousarray(slices, dtype=np.float32)).cuda()
-             if host else slices.to(torch.float32).contiguous())
+    if host:
+        known_host = torch.from_numpy(np.ascontiguousarray(slices, dtype=np.float32))
+        known = known_host.cuda()
+    else:
+        known = slices.to(torch.float32).contiguous()
     K, H, W = known.shape
     zk = ZPartKriging(K, H, W, factor, n_subparts, kind=kind, drift=drift, accum=accum,
                       seed=seed)
     out, var = zk.run(known, return_variance=return_variance)
-    models, _ = zk.finish()
     if host:
-        return out.cpu().numpy(), (var.cpu().numpy() if var is not None else None), models
+        # interpolated planes from the device, known planes from the input
+        vol = zk.download(out, known_host)
+        models, _ = zk.finish()
+        return vol.numpy(), (var.cpu().numpy() if var is not None else None), models
+    models, _ = zk.finish()
     return out, var, models

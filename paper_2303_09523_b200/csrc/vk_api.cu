@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <string>
 #include <vector>
+#include <thread>
+#include <memory>
 
 #include "../../include/volkrig_b200.h"
 #include "pcg64.h"
@@ -93,6 +95,8 @@ struct vk_plan {
   double* h_models = nullptr;        // pinned staging [S][3]
   int kernels = 0;
   cudaStream_t side = nullptr;        // pair draw runs here, concurrent with stats
+  cudaStream_t io = nullptr;          // vk_plan_download: host-side known planes
+  cudaEvent_t ev_io_fork = nullptr, ev_io_join = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // per-part chains (fit -> solve -> predict): one stream per part (up to
   // NCH), so every part's latency-bound fit starts at once
@@ -100,6 +104,10 @@ struct vk_plan {
   cudaStream_t chain[NCH] = {};        // fit -> solve (high priority)
   cudaStream_t pchain[NCH] = {};       // predict (low priority), after its part's solve
   cudaEvent_t ev_kfork = nullptr, ev_kjoin[NCH] = {}, ev_solved[NCH] = {}, ev_pjoin[NCH] = {};
+  // head parts (chained schedule): statistics and bins of the first parts go
+  // first, so their chains start before the rest of the volume is reduced
+  cudaEvent_t ev_hstats = nullptr, ev_hbins = nullptr;
+  int head_parts = 0;
   std::vector<int> sys_begin;         // [S + 1] system range of each part
   std::vector<int> gap_begin;         // [S + 1] gap range of each part (fast path)
   FastLaunch fast_launch;             // cached TMA descriptor + occupancy
@@ -124,7 +132,12 @@ struct vk_plan {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
+    if (io) cudaStreamDestroy(io);
+    if (ev_io_fork) cudaEventDestroy(ev_io_fork);
+    if (ev_io_join) cudaEventDestroy(ev_io_join);
     if (ev_kfork) cudaEventDestroy(ev_kfork);
+    if (ev_hstats) cudaEventDestroy(ev_hstats);
+    if (ev_hbins) cudaEventDestroy(ev_hbins);
     for (int i = 0; i < NCH; ++i) {
       if (ev_kjoin[i]) cudaEventDestroy(ev_kjoin[i]);
       if (ev_solved[i]) cudaEventDestroy(ev_solved[i]);
@@ -274,11 +287,11 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   VK_TRY(p->alloc(&p->d_weights, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK) * WPAD));
   VK_TRY(p->alloc(&p->d_var, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK)));
   if (g.fast) VK_TRY(p->alloc(&p->d_kpm, kpm_elems(S, std::max(1, p->NK))));
-  VK_TRY(p->alloc(&p->d_inexact, (size_t)1));
+  VK_TRY(p->alloc(&p->d_inexact, (size_t)g.K));
   if (g.fast && d->accum == VK_ACCUM_FIXED) {
     VK_TRY(p->alloc(&p->d_fxb, fxb_words(S, std::max(1, p->NK))));
     VK_TRY(p->alloc(&p->d_fxc, fxc_floats(S, std::max(1, p->NK))));
-    VK_TRY(p->alloc(&p->d_fxq, (size_t)4));
+    VK_TRY(p->alloc(&p->d_fxq, (size_t)8));
   }
   VK_TRY(cudaMallocHost((void**)&p->h_models, (size_t)S * 3 * sizeof(double)));
   if (d->fit_variogram) {
@@ -345,6 +358,13 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   // timing, debugging)
   if (!(d->flags & VK_FLAG_SERIAL) && S > 1 && g.fast) {
     VK_TRY(cudaEventCreateWithFlags(&p->ev_kfork, cudaEventDisableTiming));
+    VK_TRY(cudaEventCreateWithFlags(&p->ev_hstats, cudaEventDisableTiming));
+    VK_TRY(cudaEventCreateWithFlags(&p->ev_hbins, cudaEventDisableTiming));
+    // off by default: C4 measured 1.325 / 1.334 / 1.325 / 1.334 ms per step
+    // with 0 / 2 / 4 / 8 head parts -- the head fits themselves (~0.1-0.2 ms
+    // of TRF latency) and not the statistics gate the first predictions
+    const char* hp = std::getenv("VK_HEAD_PARTS");
+    p->head_parts = std::min(S - 1, std::max(0, hp ? std::atoi(hp) : 0));
     // fits and solves are latency chains: their streams get the highest
     // priority so a part's solve CTAs are placed ahead of the streaming CTAs
     // of parts already predicting; predicts run at the lowest priority
@@ -396,6 +416,14 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     return cudaEventRecord(p->ev[(size_t)slot * (VK_N_STAGES + 1) + stage], st);
   };
   VK_CUDA(mark(0));
+  // VK_CHAIN_TRACE (debug): per-part fit / solve / predict completion times
+  static const bool trace = std::getenv("VK_CHAIN_TRACE") != nullptr;
+  cudaEvent_t t_start = nullptr, t_pre[5] = {};     // draw, head bins, bins, head stats, stats
+  if (trace) {
+    cudaEventCreate(&t_start);
+    cudaEventRecord(t_start, st);
+    for (auto& e : t_pre) cudaEventCreate(&e);
+  }
   if (!d.fit_variogram) {
     if (!models) return set_err(VK_E_INVALID_ARGUMENT, "models required when fit_variogram == 0");
     std::memcpy(p->h_models, models, (size_t)S * 3 * sizeof(double));
@@ -410,6 +438,13 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   // (highest priority: the draw's small grids are placed first and the
   // statistics pass fills the remaining SMs)
   const bool side_bins = d.fit_variogram && p->chain[0] != nullptr;
+  const bool fast = g.fast && predict_fast_supported(g.G, d.accum);
+  const bool chained = p->chain[0] != nullptr && fast;
+  // head parts: statistics of their planes and their bins are issued first
+  // and signalled separately, so the first chains' fits start while the rest
+  // of the volume is still being reduced
+  const int H = chained ? p->head_parts : 0;
+  const int kh = H > 0 ? g.parts[H - 1].e + 1 : 0;   // head planes [0, kh)
   BinsArgs ba;
   ba.known = known;
   ba.values = nullptr;
@@ -429,14 +464,38 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       kernels += 5;
       p->pairs_ready = true;
     }
-    if (side_bins) {
+    if (trace) cudaEventRecord(t_pre[0], p->side);
+    if (side_bins && H > 0) {
+      BinsArgs b1 = ba;
+      b1.part0 = 0;
+      b1.n_parts = H;
+      VK_CUDA(launch_bins(b1, p->side));
+      VK_CUDA(cudaEventRecord(p->ev_hbins, p->side));
+      if (trace) cudaEventRecord(t_pre[1], p->side);
+      b1.part0 = H;
+      b1.n_parts = S - H;
+      VK_CUDA(launch_bins(b1, p->side));
+      kernels += 2;
+    } else if (side_bins) {
       VK_CUDA(launch_bins(ba, p->side));
       ++kernels;
     }
+    if (trace) cudaEventRecord(t_pre[2], p->side);
     VK_CUDA(cudaEventRecord(p->ev_join, p->side));
   }
-  VK_CUDA(launch_plane_stats(known, g.K, P, p->d_stats, p->nchunk, st, p->d_inexact));
+  if (H > 0) {
+    VK_CUDA(launch_plane_stats(known, 0, kh, P, p->d_stats, p->nchunk, st, p->d_inexact));
+    VK_CUDA(cudaEventRecord(p->ev_hstats, st));
+    ++kernels;
+  }
+  if (trace) cudaEventRecord(t_pre[3], st);
+  VK_CUDA(launch_plane_stats(known, kh, g.K, P, p->d_stats, p->nchunk, st, p->d_inexact));
   ++kernels;
+  if (trace) cudaEventRecord(t_pre[4], st);
+  if (fast && d.accum == VK_ACCUM_FIXED) {
+    VK_CUDA(launch_quant_range(p->d_stats, g.K * p->nchunk, p->d_fxq, st));
+    ++kernels;
+  }
   VK_CUDA(mark(1));
   if (draw || side_bins) VK_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));   // "pairs" = residual wait
   if (d.fit_variogram && !side_bins) {
@@ -526,17 +585,25 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   pa.fxc = p->d_fxc;
   pa.fxq = p->d_fxq;
   pa.num_sms = p->num_sms;
-  const bool fast = g.fast && predict_fast_supported(g.G, d.accum);
   if (fast) VK_CUDA(prepare_predict_fast(pa, &p->fast_launch));
-  if (p->chain[0] && fast) {
+  if (chained) {
     // ---- overlapped schedule: part s runs fit -> solve -> predict on chain
     // stream s % NCH; a part whose variogram fit converges early streams its
     // planes while slower fits are still iterating.
     VK_CUDA(cudaEventRecord(p->ev_kfork, st));
     const int nch = std::min(S, vk_plan::NCH);
-    for (int c = 0; c < nch; ++c) VK_CUDA(cudaStreamWaitEvent(p->chain[c], p->ev_kfork, 0));
-    // VK_CHAIN_TRACE (debug): per-part fit / solve / predict completion times
-    static const bool trace = std::getenv("VK_CHAIN_TRACE") != nullptr;
+    // head chains start from their own statistics and bins; every other
+    // chain (and a head chain's later parts when S > NCH) from the fork
+    for (int c = 0; c < nch; ++c) {
+      if (c < H) {
+        VK_CUDA(cudaStreamWaitEvent(p->chain[c], p->ev_hstats, 0));
+        if (side_bins) VK_CUDA(cudaStreamWaitEvent(p->chain[c], p->ev_hbins, 0));
+        // fixed path: the quantisation range covers the whole volume
+        if (d.accum == VK_ACCUM_FIXED) VK_CUDA(cudaStreamWaitEvent(p->pchain[c], p->ev_kfork, 0));
+      } else {
+        VK_CUDA(cudaStreamWaitEvent(p->chain[c], p->ev_kfork, 0));
+      }
+    }
     std::vector<cudaEvent_t> tev;
     if (trace) {
       tev.resize(1 + 3 * S);
@@ -547,6 +614,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     // predicts): a chain's solve waits on its fit, and a waiting kernel at
     // the head of a hardware work queue would block the fits queued behind it
     for (int s = 0; s < S; ++s) {
+      if (s >= nch && s % nch < H && s < nch + H) VK_CUDA(cudaStreamWaitEvent(p->chain[s % nch], p->ev_kfork, 0));
       FitArgs f1 = fa;
       f1.part0 = s;
       f1.n_parts = 1;
@@ -594,6 +662,16 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     }
     if (trace) {
       cudaStreamSynchronize(st);
+      float f0 = 0;
+      cudaEventElapsedTime(&f0, t_start, tev[0]);
+      std::fprintf(stderr, "fork at %.3f ms after the step start\n", f0);
+      const char* names[5] = {"draw", "head bins", "bins", "head stats", "stats"};
+      for (int i = 0; i < 5; ++i) {
+        float t = -1;
+        if (cudaEventElapsedTime(&t, t_start, t_pre[i]) != cudaSuccess) t = -1;
+        std::fprintf(stderr, "  %s done at %.3f ms\n", names[i], t);
+      }
+      for (auto& e : t_pre) cudaEventDestroy(e);
       for (int s2 = 0; s2 < S; ++s2) {
         float f = 0, v = 0, q = 0;
         cudaEventElapsedTime(&f, tev[0], tev[1 + 3 * s2]);
@@ -602,6 +680,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
         std::fprintf(stderr, "chain %2d fit %.3f solve %.3f predict %.3f ms\n", s2, f, v, q);
       }
       for (auto& e : tev) cudaEventDestroy(e);
+      cudaEventDestroy(t_start);
     }
     VK_CUDA(mark(4));
     VK_CUDA(mark(5));
@@ -748,6 +827,79 @@ int vk_plan_stage_ms(vk_plan* p, int back, float* ms) {
     VK_CUDA(cudaEventElapsedTime(&t, e[i], e[i + 1]));
     ms[i] = t;
   }
+  return VK_OK;
+}
+
+namespace {
+// known planes of a downloaded volume, copied by host threads
+struct HostPlaneCopy {
+  char* dst;
+  const char* src;
+  size_t plane;
+  std::vector<int> z;     // destination plane of known slice k
+};
+void CUDART_CB host_plane_copy(void* arg) {
+  std::unique_ptr<HostPlaneCopy> j(static_cast<HostPlaneCopy*>(arg));
+  static const int env_threads = std::getenv("VK_HOST_COPY_THREADS") ? std::atoi(std::getenv("VK_HOST_COPY_THREADS")) : 0;
+  const int K = (int)j->z.size();
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = std::max(1, std::min({K, env_threads > 0 ? env_threads : std::min(8, hw)}));
+  auto work = [&](int t) {
+    for (int k = t; k < K; k += nt) std::memcpy(j->dst + (size_t)j->z[k] * j->plane, j->src + (size_t)k * j->plane, j->plane);
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+}  // namespace
+
+int vk_plan_download(vk_plan* p, const float* out_dev, const float* known_host, float* out_host, void* stream) {
+  if (!p || !out_dev || !known_host || !out_host) return set_err(VK_E_INVALID_ARGUMENT, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Geometry& g = p->geo;
+  const size_t plane = (size_t)g.H * g.W * sizeof(float);
+  if (!p->io) {
+    VK_CUDA(cudaStreamCreateWithFlags(&p->io, cudaStreamNonBlocking));
+    VK_CUDA(cudaEventCreateWithFlags(&p->ev_io_fork, cudaEventDisableTiming));
+    VK_CUDA(cudaEventCreateWithFlags(&p->ev_io_join, cudaEventDisableTiming));
+  }
+  const int K = g.K;
+  bool regular = K >= 2 && g.known_z[0] == 0 && g.known_z[K - 1] == g.T - 1;
+  const int f = K >= 2 ? g.known_z[1] - g.known_z[0] : 1;
+  for (int k = 1; regular && k < K; ++k) regular = g.known_z[k] - g.known_z[k - 1] == f;
+  char* oh = reinterpret_cast<char*>(out_host);
+  const char* od = reinterpret_cast<const char*>(out_dev);
+  // known planes: copied on the host from the caller's input (the device
+  // holds bit-identical copies, kriging.py:481) by a host function on the
+  // plan's io stream -- worker threads, concurrent with the DMA below, and
+  // ordered after everything the caller queued before this call (the fork
+  // is recorded before the download is queued, so the two overlap)
+  VK_CUDA(cudaEventRecord(p->ev_io_fork, st));
+  VK_CUDA(cudaStreamWaitEvent(p->io, p->ev_io_fork, 0));
+  auto* job = new HostPlaneCopy{oh, reinterpret_cast<const char*>(known_host), plane, g.known_z};
+  const cudaError_t ce = cudaLaunchHostFunc(p->io, host_plane_copy, job);
+  if (ce != cudaSuccess) {
+    delete job;
+    VK_CUDA(ce);
+  }
+  // interpolated planes: device to host on the caller's stream
+  if (regular) {
+    if (f > 1)     // every gap's f - 1 interpolated planes: one strided copy
+      VK_CUDA(cudaMemcpy2DAsync(oh + plane, f * plane, od + plane, f * plane, (f - 1) * plane, K - 1,
+                                cudaMemcpyDeviceToHost, st));
+  } else {
+    int z = 0;
+    for (int k = 0; k <= K; ++k) {                 // runs of missing planes between known ones
+      const int z1 = k < K ? g.known_z[k] : g.T;
+      if (z1 > z)
+        VK_CUDA(cudaMemcpyAsync(oh + (size_t)z * plane, od + (size_t)z * plane, (size_t)(z1 - z) * plane,
+                                cudaMemcpyDeviceToHost, st));
+      z = z1 + 1;
+    }
+  }
+  VK_CUDA(cudaEventRecord(p->ev_io_join, p->io));
+  VK_CUDA(cudaStreamWaitEvent(st, p->ev_io_join, 0));
   return VK_OK;
 }
 

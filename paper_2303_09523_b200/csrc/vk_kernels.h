@@ -37,7 +37,7 @@ struct SampleGeom {
   int32_t W;
 };
 
-cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out, int nchunk,
+cudaError_t launch_plane_stats(const float* known, int k0, int k1, int64_t P, ChunkStat* out, int nchunk,
                                cudaStream_t st, int* inexact = nullptr);
 // One pair class to draw (numpy-identical PCG64 + Lemire; triu when all
 // pairs fit), with its table and the sample geometry for the lags.
@@ -62,6 +62,7 @@ struct BinsArgs {
   int64_t max_pairs;
   int n_bins, nblk, S;
   double* partial;          // [S][nblk][n_bins]
+  int part0 = 0, n_parts = 0;   // parts [part0, part0 + n_parts) of this launch (n_parts <= 0: all S)
 };
 cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st);
 
@@ -127,11 +128,12 @@ struct PredictArgs {
   int S;                       // parts in the plan
   void* fxb;                   // fixed path: [S][NK][32][8] u32 B fragments
   void* fxc;                   // fixed path: [S][NK][8] float4 epilogue constants
-  void* fxq;                   // fixed path: float4 quantisation (L, 1/step, step, 0)
+  void* fxq;                   // fixed path: float4 (L, 1/step, step, 0) + double2 (L, step),
+                               // written by launch_quant_range from the statistics pass
   int max_chunk;               // gaps per unit so that a unit spans <= 4 parts (0: none)
   void* kpm;                   // [S][NK][16][NSTP] Acc mirror-pair stencils (fast path)
-  const int* sd_inexact;       // device flag from the stats pass: 0 -> every known value is an
-                               // integer below 2^23, so A +- B is exact in fp32
+  const int* sd_inexact;       // [K] per-plane flags from the stats pass: 0 -> every value of the
+                               // plane is an integer below 2^23, so A +- B is exact in fp32
   int num_sms;
 };
 // doubles the K+- table needs (fast path)
@@ -153,6 +155,7 @@ int predict_fast_supported(int G, int accum);
 cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st);
 // fixed-point tensor-core path (vk_predict_fixed.cu)
 cudaError_t occupancy_fixed(int G, int* occ);
+cudaError_t launch_quant_range(const ChunkStat* stats, int n, void* fxq, cudaStream_t st);
 cudaError_t launch_predict_fixed(const void* tmap, int occ, const PredictArgs& a, cudaStream_t st);
 // generic per-voxel fill (vk_generic.cu); synchronous on `st`
 struct GenericResult {

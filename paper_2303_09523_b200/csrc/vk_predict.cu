@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
       mbar_wait(&full[sq_b % FT_STAGES], (sq_b / FT_STAGES) & 1);
       const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
       const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
-      const bool sd_exact = a.sd_inexact != nullptr && *a.sd_inexact == 0;
+      const bool sd_exact = a.sd_inexact != nullptr && (a.sd_inexact[k] | a.sd_inexact[k + 1]) == 0;
       auto row_steps = [&](auto exact_c) {
       constexpr bool EXACT = decltype(exact_c)::value;
 #pragma unroll 1

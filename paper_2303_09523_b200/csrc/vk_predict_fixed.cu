@@ -37,6 +37,7 @@
 // the mirror-pair stencil table.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cfloat>
 #include <cstdint>
 #include "vk_kernels.h"
 #include "vk_tma.cuh"
@@ -73,33 +74,19 @@ __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], ui
 }
 
 // volume-wide quantisation range from the per-part known ranges
-__device__ __forceinline__ void quant_range(const PredictArgs& a, double* L, double* R) {
-  double lo = a.lohi[0], hi = a.lohi[1];
-  for (int s = 1; s < a.S; ++s) {
-    lo = fmin(lo, a.lohi[2 * s]);
-    hi = fmax(hi, a.lohi[2 * s + 1]);
-  }
-  *L = lo;
-  *R = hi - lo;
-}
-
 }  // namespace
 
 // ---- tables: one warp per (part, kind) -----------------------------------
 // fxb [s][kind][lane][8] u32 : B fragments, reg 2*b + r = weight byte b,
 //                              k-half r (plane A / plane B)
 // fxc [s][kind][8] float4    : (c0 hi, c0 lo, cG, cH) per missing plane j
-// fxq float4                 : (L, 1/step, step, 0)
+// fxq float4                 : (L, 1/step, step, 0), then double2 (L, step)
 template <int G>
 __global__ void __launch_bounds__(32) fixed_table_kernel(PredictArgs a) {
   const int s = a.part0 + blockIdx.x / a.NK, kind = blockIdx.x % a.NK;
   const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
-  double L, R;
-  quant_range(a, &L, &R);
-  const double step = R > 0 ? R / 16777215.0 : 0.0;
-  if (blockIdx.x == 0 && lane == 0)
-    *reinterpret_cast<float4*>(a.fxq) =
-        make_float4((float)L, step > 0 ? (float)(1.0 / step) : 0.f, (float)step, 0.f);
+  const double2 Ls = reinterpret_cast<const double2*>(a.fxq)[1];
+  const double L = Ls.x, step = Ls.y;
   // weights of missing plane g (patterns are identical for every gap here)
   const double* w = nullptr;
   if (g < G) w = a.weights + (((int64_t)s * a.NP + a.gap_pattern[g]) * a.NK + kind) * WPAD;
@@ -134,6 +121,41 @@ __global__ void __launch_bounds__(32) fixed_table_kernel(PredictArgs a) {
     const float hi = (float)c0;
     reinterpret_cast<float4*>(a.fxc)[((size_t)s * a.NK + kind) * 8 + lane] =
         make_float4(hi, (float)(c0 - (double)hi), (float)ldexp(step, 32 - P), (float)ldexp(step, 16 - P));
+  }
+}
+
+// The quantisation range is the volume's known range: the union of every
+// part's clamp range (min/max of the non-empty statistics chunks, as the fit
+// kernel reduces them per part), computed once from the statistics pass so a
+// part's tables never depend on other parts' fits (chained schedule).
+__global__ void __launch_bounds__(256) quant_range_kernel(const ChunkStat* __restrict__ stats, int n, void* fxq) {
+  double mn = DBL_MAX, mx = -DBL_MAX;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const ChunkStat cs = stats[i];
+    if (cs.n <= 0) continue;
+    mn = fmin(mn, cs.mn);
+    mx = fmax(mx, cs.mx);
+  }
+  for (int o = 16; o; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __shared__ double sh[2][8];
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = mn;
+    sh[1][threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      mn = fmin(mn, sh[0][w]);
+      mx = fmax(mx, sh[1][w]);
+    }
+    if (mn > mx) mn = mx = 0.0;                    // no finite known value: the fit reports it
+    const double L = mn, R = mx - mn;
+    const double step = R > 0 ? R / 16777215.0 : 0.0;
+    reinterpret_cast<float4*>(fxq)[0] = make_float4((float)L, step > 0 ? (float)(1.0 / step) : 0.f, (float)step, 0.f);
+    reinterpret_cast<double2*>(fxq)[1] = make_double2(L, step);
   }
 }
 
@@ -471,6 +493,11 @@ cudaError_t occupancy_fixed(int G, int* occ) {
 #undef VK_CASE
     default: return cudaErrorNotSupported;
   }
+}
+
+cudaError_t launch_quant_range(const ChunkStat* stats, int n, void* fxq, cudaStream_t st) {
+  quant_range_kernel<<<1, 256, 0, st>>>(stats, n, fxq);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_predict_fixed(const void* tmap, int occ, const PredictArgs& a, cudaStream_t st) {

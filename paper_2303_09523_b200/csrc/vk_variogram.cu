@@ -41,9 +41,9 @@ __device__ __forceinline__ double warp_max(double v) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ data, int64_t P,
-                                                          int nchunk, ChunkStat* __restrict__ out,
+                                                          int nchunk, int k0, ChunkStat* __restrict__ out,
                                                           int* __restrict__ inexact) {
-  const int k = blockIdx.y, c = blockIdx.x;
+  const int k = k0 + (int)blockIdx.y, c = blockIdx.x;
   const int64_t beg = (int64_t)c * STATS_CHUNK;
   const int64_t end = min(P, beg + (int64_t)STATS_CHUNK);
   const T* p = data + (int64_t)k * P;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ 
       notint |= (dv != rint(dv)) | (fabs(dv) >= 8388608.0);
     }
   }
-  if (inexact && __syncthreads_or(notint) && threadIdx.x == 0) atomicOr(inexact, 1);
+  if (inexact && __syncthreads_or(notint) && threadIdx.x == 0) atomicOr(inexact + k, 1);
   __shared__ double sh[5][8];
   s1 = warp_sum(s1); s2 = warp_sum(s2); bad = warp_sum(bad);
   mn = warp_min(mn); mx = warp_max(mx);
@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(256) bins_kernel(BinsArgs a) {
   // parts in reverse: the statistics pass streams the planes in order just
   // before, so the last parts' planes are still in L2 when their random
   // gathers start
-  const int s = a.S - 1 - (int)blockIdx.y, blk = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int n_parts = a.n_parts > 0 ? a.n_parts : a.S;
+  const int s = a.part0 + n_parts - 1 - (int)blockIdx.y, blk = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const PairTable t = a.tables[a.part_class[s]];
   const int64_t npairs = (int64_t)t.scal[2];
   const int64_t per = (npairs + a.nblk - 1) / a.nblk;
@@ -480,21 +481,22 @@ extern "C" int vk_debug_fit_profile(unsigned long long* out, int reset) {
 }
 #endif
 
-cudaError_t launch_plane_stats(const float* known, int K, int64_t P, ChunkStat* out, int nchunk,
+cudaError_t launch_plane_stats(const float* known, int k0, int k1, int64_t P, ChunkStat* out, int nchunk,
                                cudaStream_t st, int* inexact) {
-  dim3 grid(nchunk, K);
+  if (k1 <= k0) return cudaSuccess;
+  dim3 grid(nchunk, k1 - k0);
   if (inexact) {
-    cudaError_t e = cudaMemsetAsync(inexact, 0, sizeof(int), st);
+    cudaError_t e = cudaMemsetAsync(inexact + k0, 0, sizeof(int) * (size_t)(k1 - k0), st);
     if (e != cudaSuccess) return e;
   }
-  plane_stats_kernel<float><<<grid, 256, 0, st>>>(known, P, nchunk, out, inexact);
+  plane_stats_kernel<float><<<grid, 256, 0, st>>>(known, P, nchunk, k0, out, inexact);
   return cudaGetLastError();
 }
 
 cudaError_t launch_plane_stats_f64(const double* values, int64_t m, ChunkStat* out, int nchunk,
                                    cudaStream_t st) {
   dim3 grid(nchunk, 1);
-  plane_stats_kernel<double><<<grid, 256, 0, st>>>(values, m, nchunk, out, nullptr);
+  plane_stats_kernel<double><<<grid, 256, 0, st>>>(values, m, nchunk, 0, out, nullptr);
   return cudaGetLastError();
 }
 
@@ -547,7 +549,7 @@ cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int
 }
 
 cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
-  dim3 grid(a.nblk, a.S);
+  dim3 grid(a.nblk, a.n_parts > 0 ? a.n_parts : a.S);
   const size_t smem = (size_t)a.n_bins * 256 * sizeof(double);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -159,6 +159,29 @@ class KrigingPlan:
             self._h, known.data_ptr(), mptr, out.data_ptr(), vptr,
             _stream_handle(stream)))
 
+    def download(self, out, known_host, out_host=None, stream=None):
+        """Reconstructed volume -> host (``vk_plan_download``): interpolated
+        planes from the device ``out``, known planes from the caller's host
+        input ``known_host`` (CPU float32 [K,H,W]; pinned for overlap).
+        Returns the host float32 [depth,H,W] tensor (pinned if allocated
+        here).  Stream-ordered: synchronise before reading it."""
+        torch = _torch()
+        K, H, W = self.n_known, self.height, self.width
+        if not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous()
+                and tuple(out.shape) == (self.depth, H, W)):
+            raise ValueError("out must be a contiguous CUDA float32 [depth,H,W] tensor")
+        if not (not known_host.is_cuda and known_host.dtype == torch.float32 and known_host.is_contiguous()
+                and tuple(known_host.shape) == (K, H, W)):
+            raise ValueError(f"known_host must be a contiguous CPU float32 [{K},{H},{W}] tensor")
+        if out_host is None:
+            out_host = torch.empty((self.depth, H, W), dtype=torch.float32, pin_memory=True)
+        elif not (not out_host.is_cuda and out_host.dtype == torch.float32 and out_host.is_contiguous()
+                  and tuple(out_host.shape) == (self.depth, H, W)):
+            raise ValueError("out_host must be a contiguous CPU float32 [depth,H,W] tensor")
+        raise_for_status(self.lib.vk_plan_download(self._h, out.data_ptr(), known_host.data_ptr(),
+                                                   out_host.data_ptr(), _stream_handle(stream)))
+        return out_host
+
     def finish(self, stream=None):
         """Synchronise; return (models [S,3], lohi [S,2]) or raise."""
         models = np.zeros((self.n_subparts, 3))

@@ -254,7 +254,7 @@ def test_streaming_variance_all_fast_gaps(cuda, f, accum):
 def test_integer_data_fast_sd_path_is_bit_identical(cuda):
     """Integer-valued known planes take the fp32 S/D form in the fp64
     streaming kernel (A +- B exact in fp32); one non-integer voxel switches the
-    whole volume to the general form.  Voxels whose windows do not reach the
+    gaps that read its plane to the general form (per-plane flags).  Voxels whose windows do not reach the
     changed voxel must come out bit-identical from both."""
     torch = cuda
     from paper_2303_09523_b200 import VariogramModel, ZPartKriging

@@ -96,3 +96,34 @@ def test_large_round_trip(cuda, tmp_path):
     v = load_volume(p)
     assert torch.equal(v.missing_mask.cpu(), torch.from_numpy(m))
     assert np.array_equal(v.data.cpu().numpy(), d, equal_nan=True)
+
+
+def test_plan_download_regular_and_irregular(cuda):
+    """vk_plan_download: interpolated planes from the device, known planes
+    from the host input -- the same bytes as a full device-to-host copy."""
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.kriging import KrigingPlan, VariogramModel
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("spine", 40, 52, 9, 4, n_subparts=2, seed=3)
+    ks = known_slices(cfg)
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts)
+    out, _ = zk.run(torch.from_numpy(ks).cuda())
+    host = zk.download(out, torch.from_numpy(ks).pin_memory())
+    zk.finish()
+    assert host.is_pinned() and torch.equal(host, out.cpu())
+    # irregular known planes (runs of 1, 2, 3 and 4 missing planes)
+    kz = np.array([0, 2, 5, 9, 10, 15], np.int32)
+    T, H, W = 16, 24, 28
+    r = np.random.default_rng(4)
+    known = (r.random((len(kz), H, W)) * 100).astype(np.float32)
+    plan = KrigingPlan(H, W, T, kz, fit=False)
+    m = VariogramModel("exponential", 0.5, 500.0, 6.0)
+    outd = torch.full((T, H, W), float("nan"), device="cuda")
+    plan.execute(torch.from_numpy(known).cuda(), outd, models=np.array([[m.nugget, m.sill, m.range_len]]))
+    h2 = plan.download(outd, torch.from_numpy(known))
+    plan.finish()
+    ref = outd.cpu()
+    assert torch.equal(h2[kz], torch.from_numpy(known))
+    miss = np.setdiff1d(np.arange(T), kz)
+    assert torch.equal(h2[miss].view(torch.int32), ref[miss].view(torch.int32))
