@@ -55,6 +55,7 @@ int status_from_part(int ps) {
     case PS_INSUFFICIENT: return VK_E_INSUFFICIENT_SAMPLES;
     case PS_DEGENERATE: return VK_E_DEGENERATE_LAGS;
     case PS_FIT_FAILED: return VK_E_FIT_FAILED;
+    case PS_NONFINITE: return VK_E_INVALID_GRID;
     default: return VK_E_CUDA;
   }
 }
@@ -920,8 +921,14 @@ int vk_plan_finish(vk_plan* p, void* stream, int32_t* failed_part, double* model
   for (int s = 0; s < S; ++s) {
     if (ps[s] != PS_OK) {
       if (failed_part) *failed_part = s;
-      return set_err(status_from_part(ps[s]), "sub-part " + std::to_string(s) + ": status " +
-                                                  std::to_string(ps[s]));
+      const char* why = ps[s] == PS_NONFINITE      ? "known voxels must be finite"
+                        : ps[s] == PS_INSUFFICIENT ? "too few samples: need >= 30 pairs"
+                        : ps[s] == PS_DEGENERATE   ? "all sample pairs are co-located"
+                        : ps[s] == PS_FIT_FAILED   ? "variogram fit failed"
+                        : ps[s] == PS_SINGULAR     ? "extended kriging matrix is singular"
+                                                   : "device status";
+      return set_err(status_from_part(ps[s]), "sub-part " + std::to_string(s) + ": " + why + " (status " +
+                                                  std::to_string(ps[s]) + ")");
     }
   }
   for (int i = 0; i < p->n_sys; ++i) {

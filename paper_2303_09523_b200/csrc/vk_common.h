@@ -28,6 +28,7 @@ enum PartStatus : int32_t {
   PS_FIT_FAILED = 4,
   PS_PAIRS_SHORT = 5,
   PS_NEED_SCALAR_FIT = 6,   // internal: handed to the scalar TRF kernel
+  PS_NONFINITE = 7,         // a known value of the part is NaN / inf
 };
 
 // Variogram model parameters as the reference's VariogramModel

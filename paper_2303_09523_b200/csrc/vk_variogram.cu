@@ -60,27 +60,52 @@ __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ 
   bool notint = false;
   const bool vec = sizeof(T) == 4 && ((P & 3) == 0) && ((end - beg) & 3) == 0;
   if (vec) {
-    // 128-bit loads, 4 in flight per thread
+    // 128-bit loads, 4 in flight per thread.  Fast form: no per-element
+    // finiteness test (a non-finite value poisons s1 / s2 and the thread
+    // redoes its elements with `take` below), min / max and the integer test
+    // in fp32 (exact on f32 data); the fp64 shifted sums are unchanged, so
+    // the chunk statistics are bit-identical to the careful form.
     const float4* q = reinterpret_cast<const float4*>(p + beg);
     const int64_t n4 = (end - beg) >> 2;
+    float fmn = FLT_MAX, fmx = -FLT_MAX;
+    auto fast = [&](float x) {
+      const double d = (double)x - shift;
+      s1 += d;
+      s2 = fma(d, d, s2);
+      fmn = fminf(fmn, x);
+      fmx = fmaxf(fmx, x);
+      notint |= x != rintf(x);
+    };
     for (int64_t i = threadIdx.x; i < n4; i += 4 * (int64_t)blockDim.x) {
       float4 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t k = i + (int64_t)u * blockDim.x;
-        v[u] = k < n4 ? __ldg(q + k) : make_float4(NAN, NAN, NAN, NAN);
+        v[u] = k < n4 ? __ldg(q + k) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (i + (int64_t)u * blockDim.x >= n4) continue;
-        take(v[u].x); take(v[u].y); take(v[u].z); take(v[u].w);
-        // integer-valued with |v| < 2^23: A +- B of two such values is exact
-        // in fp32 (the streaming kernel's fp64 path then forms S, D in fp32)
-        notint |= (v[u].x != rintf(v[u].x)) | (fabsf(v[u].x) >= 8388608.0f) |
-                  (v[u].y != rintf(v[u].y)) | (fabsf(v[u].y) >= 8388608.0f) |
-                  (v[u].z != rintf(v[u].z)) | (fabsf(v[u].z) >= 8388608.0f) |
-                  (v[u].w != rintf(v[u].w)) | (fabsf(v[u].w) >= 8388608.0f);
+        fast(v[u].x); fast(v[u].y); fast(v[u].z); fast(v[u].w);
       }
+    }
+    // integer-valued with |v| < 2^23: A +- B of two such values is exact in
+    // fp32 (the streaming kernel's fp64 path then forms S, D in fp32)
+    notint |= fmaxf(fabsf(fmn), fabsf(fmx)) >= 8388608.0f;
+    if (s1 - s1 == 0.0 && s2 - s2 == 0.0) {
+      if (fmn <= fmx) {
+        mn = (double)fmn;
+        mx = (double)fmx;
+      }
+    } else {                                        // non-finite values: careful form
+      s1 = 0.0; s2 = 0.0; mn = DBL_MAX; mx = -DBL_MAX; bad = 0.0;
+      for (int64_t i = threadIdx.x; i < n4; i += 4 * (int64_t)blockDim.x)
+        for (int u = 0; u < 4; ++u) {
+          const int64_t k = i + (int64_t)u * blockDim.x;
+          if (k >= n4) continue;
+          const float4 w = __ldg(q + k);
+          take(w.x); take(w.y); take(w.z); take(w.w);
+        }
     }
   } else {
     for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
@@ -365,7 +390,8 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
     a.lohi[2 * s + 1] = mx;
   }
   int status = PS_OK;
-  if (bad > 0 || n <= 0) status = PS_FIT_FAILED;
+  if (bad > 0) status = PS_NONFINITE;
+  else if (n <= 0) status = PS_FIT_FAILED;
   if (!a.fit) { if (lane == 0) a.status[s] = status; return; }
   const double svar = m2 / n;
   const int64_t m = a.part_m[s];

@@ -277,3 +277,28 @@ def test_integer_data_fast_sd_path_is_bit_identical(cuda):
     # gaps 0..6 never read plane 8; rows/cols away from (60, 120) in gap 7
     assert np.array_equal(a[:7 * cfg.factor + 1], b[:7 * cfg.factor + 1])
     assert np.array_equal(a[:, :50], b[:, :50])
+
+
+@pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan])
+def test_non_finite_known_value_fails_its_part(cuda, bad):
+    """A non-finite known voxel (the reference rejects it in
+    VolumeGrid.validate, model.py:115-117) fails its sub-part's fit; the
+    statistics pass's careful form counts it, and a clean rerun on the same
+    plan reproduces a fresh plan's output bit for bit."""
+    torch = cuda
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    cfg = small_config("spine", 64, 96, 17, 4, n_subparts=4, seed=9)
+    ks = known_slices(cfg)
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts)
+    poisoned = ks.copy()
+    poisoned[9, 20, 33] = bad                       # part 2 (slices 8..12)
+    zk.run(torch.from_numpy(poisoned).cuda())
+    with pytest.raises(ValueError, match="sub-part 2: known voxels must be finite"):
+        zk.finish()
+    o1, _ = zk.run(torch.from_numpy(ks).cuda())
+    zk.finish()
+    fresh = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, cfg.n_subparts)
+    o2, _ = fresh.run(torch.from_numpy(ks).cuda())
+    fresh.finish()
+    assert torch.equal(o1, o2)
