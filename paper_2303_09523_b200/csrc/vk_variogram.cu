@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include "pcg64.h"
 #include "trf.h"
 #include "trf_warp.cuh"
@@ -39,11 +40,10 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// statistics of chunk c of plane k (one CTA)
 template <typename T>
-__global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ data, int64_t P,
-                                                          int nchunk, int k0, ChunkStat* __restrict__ out,
-                                                          int* __restrict__ inexact) {
-  const int k = k0 + (int)blockIdx.y, c = blockIdx.x;
+__device__ __forceinline__ void stats_chunk(const T* __restrict__ data, int64_t P, int nchunk, int k, int c,
+                                            ChunkStat* __restrict__ out, int* __restrict__ inexact) {
   const int64_t beg = (int64_t)c * STATS_CHUNK;
   const int64_t end = min(P, beg + (int64_t)STATS_CHUNK);
   const T* p = data + (int64_t)k * P;
@@ -132,6 +132,18 @@ __global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ 
     cs.m2 = cs.n > 0 ? fmax(a2 - a1 * a1 / cs.n, 0.0) : 0.0;
     cs.mn = amn; cs.mx = amx; cs.bad = ab;
     out[(int64_t)k * nchunk + c] = cs;
+  }
+}
+
+// CTAs walk the (plane, chunk) items of planes [k0, k0 + n_items / nchunk)
+// with a grid stride (one item per CTA unless the grid is persistent).
+template <typename T>
+__global__ void __launch_bounds__(256) plane_stats_kernel(const T* __restrict__ data, int64_t P, int nchunk,
+                                                          int k0, int n_items, ChunkStat* __restrict__ out,
+                                                          int* __restrict__ inexact) {
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    stats_chunk<T>(data, P, nchunk, k0 + it / nchunk, it % nchunk, out, inexact);
+    __syncthreads();                          // thread 0 has read the shared partials
   }
 }
 
@@ -510,19 +522,33 @@ extern "C" int vk_debug_fit_profile(unsigned long long* out, int reset) {
 cudaError_t launch_plane_stats(const float* known, int k0, int k1, int64_t P, ChunkStat* out, int nchunk,
                                cudaStream_t st, int* inexact) {
   if (k1 <= k0) return cudaSuccess;
-  dim3 grid(nchunk, k1 - k0);
   if (inexact) {
     cudaError_t e = cudaMemsetAsync(inexact + k0, 0, sizeof(int) * (size_t)(k1 - k0), st);
     if (e != cudaSuccess) return e;
   }
-  plane_stats_kernel<float><<<grid, 256, 0, st>>>(known, P, nchunk, k0, out, inexact);
+  // one CTA per (plane, chunk) item by default: persistent CTAs (one wave,
+  // VK_STATS_PERSISTENT=1) shorten the pass alone but hold every SM slot, so
+  // the concurrent high-priority pair draw starts later -- C4 step 1.304-1.308
+  // ms one CTA per item vs 1.313-1.319 ms persistent (same box, alternating)
+  static int slots = 0;
+  if (!slots) {
+    slots = 1 << 30;
+    if (const char* e = std::getenv("VK_STATS_PERSISTENT"); e && std::atoi(e) != 0) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, plane_stats_kernel<float>, 256, 0);
+      slots = std::max(1, sms * std::max(1, per));
+    }
+  }
+  const int n_items = (k1 - k0) * nchunk;
+  plane_stats_kernel<float><<<std::min(n_items, slots), 256, 0, st>>>(known, P, nchunk, k0, n_items, out, inexact);
   return cudaGetLastError();
 }
 
 cudaError_t launch_plane_stats_f64(const double* values, int64_t m, ChunkStat* out, int nchunk,
                                    cudaStream_t st) {
-  dim3 grid(nchunk, 1);
-  plane_stats_kernel<double><<<grid, 256, 0, st>>>(values, m, nchunk, 0, out, nullptr);
+  plane_stats_kernel<double><<<nchunk, 256, 0, st>>>(values, m, nchunk, 0, nchunk, out, nullptr);
   return cudaGetLastError();
 }
 
