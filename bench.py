@@ -254,7 +254,7 @@ def run_gpu(args, cfg, ks):
     has_halo = rank < world - 1
     K_loc = cfg.n_known + int(has_halo)
     H, W, f = cfg.height, cfg.width, cfg.factor
-    zk = ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, redraw_pairs=True,
+    zk = ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, redraw_pairs=not os.environ.get("VK_DIAG_NO_REDRAW"),
                       part_len=cfg.n_known // cfg.n_subparts, overlap=not args.serial)
     # per-stage / per-kernel times come from the serial schedule (one launch
     # per stage on one stream); the default chained schedule interleaves them

@@ -461,8 +461,9 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(cudaEventRecord(p->ev_fork, st));
     VK_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     if (draw) {
-      VK_CUDA(launch_pair_tables(p->d_jobs, p->jobs.data(), (int)p->jobs.size(), p->side));
-      kernels += 5;
+      int nl = 0;
+      VK_CUDA(launch_pair_tables(p->d_jobs, p->jobs.data(), (int)p->jobs.size(), p->side, &nl));
+      kernels += nl;
       p->pairs_ready = true;
     }
     if (trace) cudaEventRecord(t_pre[0], p->side);

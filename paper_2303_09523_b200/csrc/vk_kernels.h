@@ -51,8 +51,10 @@ struct PairJob {
 };
 PairJob make_pair_job(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t m,
                       int64_t max_pairs, int n_bins, SampleGeom geom, PairTable t);
-// all classes in 5 launches (blockIdx.y = class); h_jobs mirrors d_jobs
-cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st);
+// all classes in one cooperative launch, or 5 launches (blockIdx.y = class);
+// h_jobs mirrors d_jobs; *launches (optional) = kernels launched
+cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st,
+                               int* launches = nullptr);
 struct BinsArgs {
   const float* known;      // structured: known planes; sample i of part s = known[base_s + i]
   const double* values;    // explicit samples (fit_variogram API) or nullptr

@@ -22,6 +22,8 @@
 #include "trf.h"
 #include "trf_warp.cuh"
 #include "vk_kernels.h"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace vk {
 
@@ -582,7 +584,145 @@ int64_t pair_scratch_elems(int64_t m, int64_t max_pairs) {
   return (n_raw + PT_RAW - 1) / PT_RAW;
 }
 
-cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st) {
+// The whole draw in one cooperative launch (blockIdx.y = class): count the
+// accepted Lemire halves of each thread's PT_RAW raw outputs (the LCG state
+// at the chunk start is kept in registers), block scan, grid sync, block
+// offsets from the per-block totals, scatter by regenerating the chunk,
+// grid sync, lag maximum, grid sync, digitize.  Same arithmetic and outputs
+// as the five-kernel form above, without four launch gaps and tails.
+__global__ void __launch_bounds__(PT_BLOCK) pair_draw_kernel(const PairJob* jobs) {
+  cg::grid_group grid = cg::this_grid();
+  const PairJob& J = jobs[blockIdx.y];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t g = (int64_t)blockIdx.x * PT_BLOCK + tid;
+  const int64_t nb_gen = J.triu ? 0 : (J.n_thr + PT_BLOCK - 1) / PT_BLOCK;
+  if (blockIdx.x == 0 && tid == 0) {
+    *J.t.hbits = 0ull;
+    for (int b = 0; b < MAX_BINS; ++b) J.t.counts[b] = 0;
+  }
+  const u128 inc = ((u128)J.inc_hi << 64) | J.inc_lo;
+  const u128 mul = pcg_mult();
+  const int64_t r0 = g * PT_RAW;
+  const bool gen = !J.triu && r0 < J.n_raw;
+  const int64_t r1 = gen ? min(J.n_raw, r0 + PT_RAW) : r0;
+  u128 s0 = 0;
+  int c = 0;
+  if (gen) {
+    s0 = pcg_advance(((u128)J.st_hi << 64) | J.st_lo, inc, (uint64_t)r0);
+    u128 s = s0;
+    for (int64_t r = r0; r < r1; ++r) {
+      s = s * mul + inc;
+      const uint64_t raw = pcg_output(s);
+      c += ((uint32_t)((uint64_t)(uint32_t)raw * J.m) >= J.thr);
+      c += ((uint32_t)((uint64_t)(uint32_t)(raw >> 32) * J.m) >= J.thr);
+    }
+  }
+  // block-exclusive scan of the counts
+  __shared__ int wsum[PT_BLOCK / 32];
+  __shared__ int64_t boff, total;
+  int incl = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int before = 0, btot = 0;
+  for (int w = 0; w < PT_BLOCK / 32; ++w) {
+    before += w < warp ? wsum[w] : 0;
+    btot += wsum[w];
+  }
+  const int excl = before + incl - c;
+  if (tid == 0 && blockIdx.x < nb_gen) J.t.cnt[blockIdx.x] = btot;
+  grid.sync();
+  if (warp == 0) {
+    int64_t a = 0, t = 0;
+    for (int64_t b = lane; b < nb_gen; b += 32) {
+      const int64_t v = J.t.cnt[b];
+      a += b < (int64_t)blockIdx.x ? v : 0;
+      t += v;
+    }
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    if (lane == 0) {
+      boff = a;
+      total = t;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0 && !J.triu) J.t.off[J.n_thr] = total;
+  if (J.triu) {
+    // np.triu_indices(m, 1): row-major upper triangle (all pairs fit)
+    const int64_t m = J.m;
+    for (int64_t i = g; i < m - 1; i += (int64_t)gridDim.x * PT_BLOCK) {
+      const int64_t o = i * (m - 1) - i * (i - 1) / 2;
+      for (int64_t j = i + 1; j < m; ++j) {
+        J.t.ii[o + (j - i - 1)] = (int32_t)i;
+        J.t.jj[o + (j - i - 1)] = (int32_t)j;
+      }
+    }
+  } else if (gen) {
+    int64_t pos = boff + excl;
+    u128 s = s0;
+    for (int64_t r = r0; r < r1 && pos < J.need; ++r) {
+      s = s * mul + inc;
+      const uint64_t raw = pcg_output(s);
+      for (int h = 0; h < 2 && pos < J.need; ++h) {
+        const uint64_t prod = (uint64_t)(uint32_t)(h ? (raw >> 32) : raw) * J.m;
+        if ((uint32_t)prod >= J.thr) {
+          const int32_t v = (int32_t)(prod >> 32);
+          if (pos < J.max_pairs) J.t.ii[pos] = v; else J.t.jj[pos - J.max_pairs] = v;
+          ++pos;
+        }
+      }
+    }
+  }
+  grid.sync();
+  double lmax = 0.0;
+  for (int64_t p = g; p < J.npairs; p += (int64_t)gridDim.x * PT_BLOCK) {
+    const int64_t i = J.t.ii[p], j = J.t.jj[p];
+    if (i == j) continue;
+    lmax = fmax(lmax, sample_lag(J.geom, i, j));
+  }
+  lmax = warp_max(lmax);
+  if (lane == 0 && lmax > 0.0) atomicMax(J.t.hbits, (unsigned long long)__double_as_longlong(lmax));
+  grid.sync();
+  __shared__ unsigned long long h[MAX_BINS];
+  if (tid < MAX_BINS) h[tid] = 0ull;
+  __syncthreads();
+  const int n_bins = J.n_bins;
+  const double hmax = __longlong_as_double((long long)*J.t.hbits);
+  const double step = hmax / (double)n_bins;   // np.linspace(0, hmax, n_bins + 1)
+  for (int64_t p = g; p < J.npairs; p += (int64_t)gridDim.x * PT_BLOCK) {
+    const int64_t i = J.t.ii[p], j = J.t.jj[p];
+    uint8_t b = 255;
+    if (i != j) {
+      const double lag = sample_lag(J.geom, i, j);
+      if (lag > 0.0) {
+        int cb = 0;                                // digitize: #edges <= lag
+        for (int e = 0; e < n_bins; ++e) cb += (__dmul_rn((double)e, step) <= lag);
+        cb += (hmax <= lag);
+        cb = min(max(cb - 1, 0), n_bins - 1);
+        b = (uint8_t)cb;
+        atomicAdd(&h[cb], 1ull);
+      }
+    }
+    J.t.bin[p] = b;
+  }
+  __syncthreads();
+  if (tid < n_bins && h[tid]) atomicAdd((unsigned long long*)&J.t.counts[tid], h[tid]);
+  if (blockIdx.x == 0 && tid == 0) {
+    J.t.scal[0] = hmax;
+    J.t.scal[1] = hmax;                              // lag_max == hmax when any lag > 0
+    J.t.scal[2] = (double)J.npairs;
+    J.t.scal[3] = (!J.triu && total < J.need) ? (double)PS_PAIRS_SHORT : 0.0;
+  }
+}
+
+cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st,
+                               int* launches) {
   int64_t max_thr = 1, max_pairs = 1, max_m = 1;
   for (int c = 0; c < n_jobs; ++c) {
     max_thr = std::max(max_thr, h_jobs[c].n_thr);
@@ -591,6 +731,30 @@ cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int
   }
   const unsigned nb = (unsigned)std::max<int64_t>((max_thr + PT_BLOCK - 1) / PT_BLOCK,
                                                   std::min<int64_t>(1024, (max_m + PT_BLOCK - 1) / PT_BLOCK));
+  // one cooperative launch when the grid fits on the device at once; the
+  // five-kernel form otherwise (or with VK_PAIR_DRAW_SPLIT=1)
+  static int coop_slots = -1;
+  if (coop_slots < 0) {
+    int dev = 0, sms = 0, per = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pair_draw_kernel, PT_BLOCK, 0);
+    const char* e = std::getenv("VK_PAIR_DRAW_SPLIT");
+    coop_slots = (coop && !(e && std::atoi(e) != 0)) ? sms * per : 0;
+  }
+  {
+    // enough blocks for the lag / digitize passes too (4 pairs per thread)
+    const int64_t want = std::max<int64_t>(nb, (max_pairs + 4 * PT_BLOCK - 1) / (4 * PT_BLOCK));
+    const int64_t cap = coop_slots / std::max(1, n_jobs);
+    if (cap >= nb) {
+      dim3 grid((unsigned)std::min(want, cap), n_jobs);
+      void* args[] = {(void*)&d_jobs};
+      if (launches) *launches = 1;
+      return cudaLaunchCooperativeKernel((void*)pair_draw_kernel, grid, dim3(PT_BLOCK), args, 0, st);
+    }
+  }
+  if (launches) *launches = 5;
   pair_count_kernel<<<dim3(nb, n_jobs), PT_BLOCK, 0, st>>>(d_jobs);
   pair_scan_kernel<<<n_jobs, 1024, 0, st>>>(d_jobs);
   pair_scatter_kernel<<<dim3(nb, n_jobs), PT_BLOCK, 0, st>>>(d_jobs);
