@@ -114,6 +114,7 @@ struct vk_plan {
   FastLaunch fast_launch;             // cached TMA descriptor + occupancy
   int ring = 0;                       // timing ring size (0 = off)
   int64_t n_exec = 0;                 // executes recorded so far
+  int64_t n_runs = 0;                 // executes issued (diagnostics)
   std::vector<cudaEvent_t> ev;        // [ring][VK_N_STAGES + 1]
 
   template <typename T>
@@ -621,7 +622,10 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       f1.part0 = s;
       f1.n_parts = 1;
       f1.reserve_smem = p->fit_reserve;
-      VK_CUDA(launch_fit(f1, p->chain[s % nch]));
+      // VK_DIAG_SKIP (diagnostics only: results reuse the previous execute's
+      // models / weights): bit 1 skips fits, bit 2 skips solves after the first execute
+      static const int diag_skip = std::getenv("VK_DIAG_SKIP") ? std::atoi(std::getenv("VK_DIAG_SKIP")) : 0;
+      if (!(diag_skip & 1) || p->n_runs == 0) VK_CUDA(launch_fit(f1, p->chain[s % nch]));
       ++kernels;
       if (trace) cudaEventRecord(tev[1 + 3 * s], p->chain[s % nch]);
     }
@@ -629,7 +633,8 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       SolveArgs s1 = sa;
       s1.sys0 = p->sys_begin[s];
       s1.n_sys = p->sys_begin[s + 1] - p->sys_begin[s];
-      VK_CUDA(launch_solve(s1, p->chain[s % nch]));
+      static const int diag_skip2 = std::getenv("VK_DIAG_SKIP") ? std::atoi(std::getenv("VK_DIAG_SKIP")) : 0;
+      if (!(diag_skip2 & 2) || p->n_runs == 0) VK_CUDA(launch_solve(s1, p->chain[s % nch]));
       kernels += (s1.n_sys > 0);
       if (trace) cudaEventRecord(tev[2 + 3 * s], p->chain[s % nch]);
     }
@@ -704,6 +709,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   }
   VK_CUDA(mark(6));
   if (p->ring) ++p->n_exec;
+  ++p->n_runs;
   p->kernels = kernels;
   return VK_OK;
 }

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
   int cols[4], pq = 0;
   for (int c = 0; c < 4; ++c)
     if (dcols & (1 << c)) cols[pq++] = c;
-  const int N = n + pq, ld = N + 1;
+  const int N = n + pq, ld = (N + 1) | 1;     // odd: row-strided lane accesses are bank-conflict free
   double* A = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + (size_t)wid * slice);
   double* xsol = A + (size_t)N * ld;
   int* rel = reinterpret_cast<int*>(xsol + N);
@@ -122,26 +122,43 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
         }
         __syncwarp();
       }
+      // column scale and rank-1 update, lanes over rows: each lane keeps its
+      // row's multiplier in a register and streams the pivot row (broadcast
+      // loads) in batches of 8 columns, loads before stores (dgetf2's
+      // arithmetic: l = a_rk * (1 / a_kk), a_rj -= l * a_kj)
       const double inv = 1.0 / A[k * ld + k];
-      for (int r = k + 1 + lane; r < N; r += 32) A[r * ld + k] *= inv;
-      __syncwarp();
-      const int colsn = ld - k - 1;
-      for (int j = lane; j < colsn; j += 32) {
-        const double ukj = A[k * ld + k + 1 + j];
-        for (int r = k + 1; r < N; ++r) A[r * ld + k + 1 + j] -= A[r * ld + k] * ukj;
+      const double* Ak = A + (size_t)k * ld;
+      for (int r = k + 1 + lane; r < N; r += 32) {
+        double* Ar = A + (size_t)r * ld;
+        const double l = Ar[k] * inv;
+        Ar[k] = l;
+        int j = k + 1;
+        for (; j + 8 <= ld; j += 8) {
+          double u[8], v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) u[t] = Ak[j + t];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[t] = Ar[j + t];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) Ar[j + t] = fma(-l, u[t], v[t]);
+        }
+        for (; j < ld; ++j) Ar[j] = fma(-l, Ak[j], Ar[j]);
       }
       __syncwarp();
     }
     if (!fail) {
-      // back substitution U x = y, rows from the bottom (lane-parallel dots)
+      // back substitution U x = y, column oriented as dtrsm (Left, Upper,
+      // NoTrans) does it: x_i = y_i / u_ii, then y_r -= x_i u_ri for r < i,
+      // lanes over rows -- no reductions
       bool finite = true;
+      for (int r = lane; r < N; r += 32) xsol[r] = A[(size_t)r * ld + N];
+      __syncwarp();
       for (int i = N - 1; i >= 0; --i) {
-        double part = 0.0;
-        for (int j = i + 1 + lane; j < N; j += 32) part += A[i * ld + j] * xsol[j];
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        const double xi = (A[i * ld + N] - part) / A[i * ld + i];
-        if (lane == 0) xsol[i] = xi;
+        const double xi = xsol[i] / A[(size_t)i * ld + i];
         finite = finite && (xi - xi == 0.0);
+        __syncwarp();
+        if (lane == 0) xsol[i] = xi;
+        for (int r = lane; r < i; r += 32) xsol[r] = fma(-xi, A[(size_t)r * ld + i], xsol[r]);
         __syncwarp();
       }
       // unbiasedness residual max_c |sum_i Q_ic w_i - q0_c|  (kriging.py:223)
@@ -189,7 +206,7 @@ cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
   if (a.n_sys == 0) return cudaSuccess;
   const int N = a.max_n + 4;
   const int maxd2 = 18 + a.max_dz * a.max_dz;
-  const size_t slice = (((size_t)N * (N + 1) + N) * sizeof(double) + (size_t)a.max_n * 3 * sizeof(int) +
+  const size_t slice = (((size_t)N * (N + 2) + N) * sizeof(double) + (size_t)a.max_n * 3 * sizeof(int) +
                         (size_t)(maxd2 + 3) * sizeof(double) + 127) / 128 * 128;
   int ws = (int)std::max<size_t>(1, std::min<size_t>(SOLVE_WARPS_MAX, (size_t)(96 * 1024) / slice));
   const size_t smem = slice * ws;
