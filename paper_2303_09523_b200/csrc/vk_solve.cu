@@ -23,6 +23,9 @@ constexpr int SOLVE_WARPS_MAX = 4;
 
 // One warp per system; `ws` systems per CTA, each with its own shared-memory
 // slice [A | b] (N x (N+1)), solution and relative offsets.
+// UPD_SLOTS: 8-column slots of the LU update (ld <= 8 UPD_SLOTS); YS: 32-row
+// slots of the back substitution (N <= 32 YS)
+template <int UPD_SLOTS, int YS>
 __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a, int ws, size_t slice) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -42,7 +45,8 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
   const int N = n + pq, ld = (N + 1) | 1;     // odd: row-strided lane accesses are bank-conflict free
   double* A = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + (size_t)wid * slice);
   double* xsol = A + (size_t)N * ld;
-  int* rel = reinterpret_cast<int*>(xsol + N);
+  double* rinv = xsol + N;
+  int* rel = reinterpret_cast<int*>(rinv + N);
   for (int i = lane; i < n; i += 32) {
     const int pl = a.taps[3 * (off + i) + 2];
     rel[3 * i + 0] = a.taps[3 * (off + i) + 0];
@@ -106,12 +110,19 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
       int bi = N;
       for (int r = k + lane; r < N; r += 32) {
         const double v = fabs(A[r * ld + k]);
-        if (v > best) { best = v; bi = r; }
+        if (v > best) { best = v; bi = r; }        // NaN never wins, as in idamax
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      // first maximal |pivot| across lanes with integer warp reductions on
+      // the bit pattern of the non-negative double (order preserving), then
+      // the smallest row among the lanes holding the maximum
+      {
+        const unsigned long long key = best > 0.0 ? (unsigned long long)__double_as_longlong(best) : 0ull;
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        const bool win = hi == mhi && lo == mlo;
+        bi = (int)__reduce_min_sync(0xffffffffu, win ? (unsigned)bi : 0xffffffffu);
+        best = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
       }
       if (!(best > 0.0)) { fail = true; break; }   // exact zero pivot: dgesv info > 0
       if (bi != k) {
@@ -142,25 +153,52 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
 #pragma unroll
           for (int t = 0; t < 8; ++t) Ar[j + t] = fma(-l, u[t], v[t]);
         }
-        for (; j < ld; ++j) Ar[j] = fma(-l, Ak[j], Ar[j]);
+        if (j < ld) {                                 // tail: one predicated batch
+          double u[8], v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) u[t] = j + t < ld ? Ak[j + t] : 0.0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[t] = j + t < ld ? Ar[j + t] : 0.0;
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (j + t < ld) Ar[j + t] = fma(-l, u[t], v[t]);
+        }
       }
       __syncwarp();
     }
     if (!fail) {
       // back substitution U x = y, column oriented as dtrsm (Left, Upper,
-      // NoTrans) does it: x_i = y_i / u_ii, then y_r -= x_i u_ri for r < i,
-      // lanes over rows -- no reductions
+      // NoTrans): x_i = y_i / u_ii, then y_r -= x_i u_ri for r < i.  y lives
+      // in registers (lane r holds rows r and r + 32); the reciprocals of the
+      // diagonal are formed off the dependent chain, which is then one
+      // multiply, one shuffle and one FMA per row
       bool finite = true;
-      for (int r = lane; r < N; r += 32) xsol[r] = A[(size_t)r * ld + N];
+      for (int r = lane; r < N; r += 32) rinv[r] = 1.0 / A[(size_t)r * ld + r];
+      double y[YS];
+#pragma unroll
+      for (int t = 0; t < YS; ++t) {
+        const int r = lane + 32 * t;
+        y[t] = r < N ? A[(size_t)r * ld + N] : 0.0;
+      }
       __syncwarp();
       for (int i = N - 1; i >= 0; --i) {
-        const double xi = xsol[i] / A[(size_t)i * ld + i];
+        const int ti = i >> 5;
+        double src = y[0];
+#pragma unroll
+        for (int t = 1; t < YS; ++t) src = ti == t ? y[t] : src;
+        const double xi = __shfl_sync(0xffffffffu, src, i & 31) * rinv[i];
         finite = finite && (xi - xi == 0.0);
-        __syncwarp();
-        if (lane == 0) xsol[i] = xi;
-        for (int r = lane; r < i; r += 32) xsol[r] = fma(-xi, A[(size_t)r * ld + i], xsol[r]);
-        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < YS; ++t) {
+          const int r = lane + 32 * t;
+          if (r < i) y[t] = fma(-xi, A[(size_t)r * ld + i], y[t]);
+          else if (r == i) y[t] = xi;
+        }
       }
+#pragma unroll
+      for (int t = 0; t < YS; ++t)
+        if (lane + 32 * t < N) xsol[lane + 32 * t] = y[t];
+      __syncwarp();
       // unbiasedness residual max_c |sum_i Q_ic w_i - q0_c|  (kriging.py:223)
       double resid = 0.0;
       for (int c = 0; c < pq; ++c) {
@@ -206,15 +244,22 @@ cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
   if (a.n_sys == 0) return cudaSuccess;
   const int N = a.max_n + 4;
   const int maxd2 = 18 + a.max_dz * a.max_dz;
-  const size_t slice = (((size_t)N * (N + 2) + N) * sizeof(double) + (size_t)a.max_n * 3 * sizeof(int) +
+  const size_t slice = (((size_t)N * (N + 2) + 2 * N) * sizeof(double) + (size_t)a.max_n * 3 * sizeof(int) +
                         (size_t)(maxd2 + 3) * sizeof(double) + 127) / 128 * 128;
   int ws = (int)std::max<size_t>(1, std::min<size_t>(SOLVE_WARPS_MAX, (size_t)(96 * 1024) / slice));
   const size_t smem = slice * ws;
+  // plane stencils of the streaming path (2 planes x 16 taps + drift) take
+  // the small instance; windows of up to NPMAX planes the general one
+  const bool small = N + 2 <= 48 && N <= 64;
+  const void* fn = small ? (const void*)solve_kernel<6, 2> : (const void*)solve_kernel<(NPMAX * 16 + 4 + 2 + 7) / 8, (NPMAX * 16 + 4 + 31) / 32>;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  solve_kernel<<<(a.n_sys + ws - 1) / ws, 32 * ws, smem, st>>>(a, ws, slice);
+  if (small)
+    solve_kernel<6, 2><<<(a.n_sys + ws - 1) / ws, 32 * ws, smem, st>>>(a, ws, slice);
+  else
+    solve_kernel<(NPMAX * 16 + 4 + 2 + 7) / 8, (NPMAX * 16 + 4 + 31) / 32><<<(a.n_sys + ws - 1) / ws, 32 * ws, smem, st>>>(a, ws, slice);
   return cudaGetLastError();
 }
 
