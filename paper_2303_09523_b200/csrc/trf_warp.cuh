@@ -27,6 +27,7 @@ __device__ unsigned long long g_fit_prof[12];  // cycles: jac, svd, trsolve, sel
 #define VK_PACC(slot, a, b)
 #endif
 
+template <int KIND>
 struct WarpTrf {
   const TrfProblem& P;
   int lane, m;
@@ -39,31 +40,44 @@ struct WarpTrf {
     w = row ? P.w[l] : 0.0;
   }
 
+  // branch-free (lanes without a row evaluate h = 0 and are masked): the
+  // kind is a template parameter, so independent evaluations interleave
   __device__ double resid(const double* x) const {
-    if (!row) return 0.0;
     Model md;
     md.nugget = pymax(x[0], 0.0);
     md.sill = md.nugget + pymax(x[1], 0.0);
     md.range_len = pymax(x[2], 1e-6);
-    return w * (semivariance(P.kind, md, h) - gemp);
+    const double f = w * (semivariance_k<KIND>(md, h) - gemp);
+    return row ? f : 0.0;
   }
 
+  // 2-point Jacobian (scipy approx_derivative with bounds): the three steps
+  // first, then the three perturbed residuals, then the quotients
   __device__ void jac(const double* x, double f0, const double* lb, const double* ub, double* J) const {
     const double rstep = 1.4901161193847656e-08;
+    double hh[3], f1[3];
+#pragma unroll
     for (int i = 0; i < 3; ++i) {
       const double sign = (x[i] >= 0.0) ? 1.0 : -1.0;
-      double hh = rstep * sign * fmax(1.0, fabs(x[i]));
+      double hi = rstep * sign * fmax(1.0, fabs(x[i]));
       const double ld = x[i] - lb[i], ud = ub[i] - x[i];
-      const double xt = x[i] + hh;
+      const double xt = x[i] + hi;
       const bool violated = (xt < lb[i]) || (xt > ub[i]);
-      const bool fitting = fabs(hh) <= fmax(ld, ud);
-      if (violated && fitting) hh = -hh;
-      if (!fitting) hh = (ud >= ld) ? ud : -ld;
+      const bool fitting = fabs(hi) <= fmax(ld, ud);
+      if (violated && fitting) hi = -hi;
+      if (!fitting) hi = (ud >= ld) ? ud : -ld;
+      hh[i] = hi;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
       double x1[3] = {x[0], x[1], x[2]};
-      x1[i] = x[i] + hh;
-      const double f1 = resid(x1);
-      const double dx = (x[i] + hh) - x[i];
-      J[i] = row ? (f1 - f0) / dx : 0.0;
+      x1[i] = x[i] + hh[i];
+      f1[i] = resid(x1);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double dx = (x[i] + hh[i]) - x[i];
+      J[i] = row ? (f1[i] - f0) / dx : 0.0;
     }
   }
 

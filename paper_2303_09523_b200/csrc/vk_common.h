@@ -55,6 +55,26 @@ VK_HD double semivariance(int kind, const Model& m, double h) {
   return m.nugget + psill * shape;
 }
 
+// gamma(h) for a compile-time kind, without the h == 0 branch folded into
+// control flow (same arithmetic as semivariance): straight-line code the
+// device fit can interleave across independent evaluations.
+template <int KIND>
+VK_HD double semivariance_k(const Model& m, double h) {
+  const double psill = m.sill - m.nugget;
+  const double r = m.range_len;
+  double shape;
+  if constexpr (KIND == KIND_EXPONENTIAL) {
+    shape = 1.0 - exp((-3.0 * h) / r);
+  } else if constexpr (KIND == KIND_GAUSSIAN) {
+    const double t = h / r;
+    shape = 1.0 - exp(-3.0 * (t * t));
+  } else {
+    const double t = fmin(h / r, 1.0);
+    shape = 1.5 * t - 0.5 * pow(t, 3.0);
+  }
+  return h == 0.0 ? 0.0 : m.nugget + psill * shape;
+}
+
 // C(h) = sill - gamma(h); unit white noise when sill <= 0 -- kriging.py:74-84.
 VK_HD double covariance(int kind, const Model& m, double h) {
   if (m.sill <= 0.0) return h == 0.0 ? 1.0 : 0.0;

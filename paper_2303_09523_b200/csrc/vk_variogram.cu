@@ -447,9 +447,11 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
     if (lane == 0) a.status[s] = PS_NEED_SCALAR_FIT;
     return;
   }
-  WarpTrf wt(P, lane);
   VK_PT(t_f0);
-  const TrfResult r = wt.fit(x0, lb, ub);
+  TrfResult r;
+  if (P.kind == KIND_EXPONENTIAL) r = WarpTrf<KIND_EXPONENTIAL>(P, lane).fit(x0, lb, ub);
+  else if (P.kind == KIND_GAUSSIAN) r = WarpTrf<KIND_GAUSSIAN>(P, lane).fit(x0, lb, ub);
+  else r = WarpTrf<KIND_SPHERICAL>(P, lane).fit(x0, lb, ub);
   VK_PT(t_f1);
   VK_PACC(5, t_f0, t_f1);
   if (lane != 0) return;
