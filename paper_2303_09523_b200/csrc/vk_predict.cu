@@ -191,14 +191,24 @@ __global__ void __launch_bounds__(256) fast_stencil_kernel(PredictArgs a) {
     const int kind = r >> 4, t = r & 15;
     Acc* dst = reinterpret_cast<Acc*>(a.kpm) + (((size_t)s * a.NK + kind) * 16 + t) * NSTP;
     for (int q = 0; q < NSTP; ++q) dst[q] = (Acc)0;
+    // interior kind: stencils are x<->y symmetric up to solver rounding
+    // (isotropic covariance, drift span closed under x <-> y); the table
+    // holds the transposition average so the streaming kernel may pair taps
+    const int kin = a.kmap[NKIND1 + AXIS_INTERIOR] * a.nkx + a.kmap[AXIS_INTERIOR];
+    const bool symm = kind == kin && a.kmap[AXIS_INTERIOR] >= 0 && a.kmap[NKIND1 + AXIS_INTERIOR] >= 0;
+    const int tt = (t & 3) * 4 + (t >> 2);                 // transposed tap
     // patterns are identical for every gap on the fast path (each missing
     // plane reads exactly its two bracketing known planes)
     for (int pr = 0; pr < NPAIR + (MID ? 1 : 0); ++pr) {
       const int pj = a.gap_pattern[pr], pm = a.gap_pattern[G - 1 - pr];
       const double* wj = a.weights + (((int64_t)s * a.NP + pj) * a.NK + kind) * WPAD;
       const double* wm = a.weights + (((int64_t)s * a.NP + pm) * a.NK + kind) * WPAD;
-      const double av = 0.5 * (wj[t] + wm[16 + t]);
-      const double bv = 0.5 * (wj[16 + t] + wm[t]);
+      double av = 0.5 * (wj[t] + wm[16 + t]);
+      double bv = 0.5 * (wj[16 + t] + wm[t]);
+      if (symm && tt != t) {
+        av = 0.5 * (av + 0.5 * (wj[tt] + wm[16 + tt]));
+        bv = 0.5 * (bv + 0.5 * (wj[16 + tt] + wm[tt]));
+      }
       if (pr < NPAIR) {
         dst[L::plus(pr)] = (Acc)(0.5 * (av + bv));
         dst[L::minus(pr)] = (Acc)(0.5 * (av - bv));
@@ -222,17 +232,6 @@ __device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
   return d;
 }
 
-template <typename Acc>
-struct Pair2;
-template <>
-struct Pair2<double> {
-  using T = double2;
-};
-template <>
-struct Pair2<float> {
-  using T = float2;
-};
-
 
 // Streaming kernel.  No CTA-wide barrier inside a unit: each warp waits only
 // for the TMA of the two planes its gap reads and, when done with plane k,
@@ -248,7 +247,13 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
   constexpr int NPAIR = L::NPAIR;
   constexpr bool MID = L::MID;
   constexpr int NSTP = L::NSTP;                            // padded: 16-byte aligned taps
-  using P2 = typename Pair2<Acc>::T;
+  // staged stencils use the run layout of StLayout<G, float> for both
+  // accumulators ([K+_0 .. K+_{n-1}, K_mid, pad | K-_0 .. K-_{n-1}, pad]): the
+  // fp64 table in global memory is interleaved and is permuted while staging
+  using LR = StLayout<G, float>;
+  constexpr int NPP = LR::NPP, NMP = LR::NMP;
+  constexpr int NSTP_S = NSTP > LR::NSTP ? NSTP : LR::NSTP;
+  constexpr bool F64 = std::is_same<Acc, double>::value;
   constexpr int FT_STAGES = ft_stages(G);
   extern __shared__ __align__(128) float ring[];           // FT_STAGES x FT_BUF_FLOATS
   __shared__ __align__(8) uint64_t full[FT_STAGES];
@@ -256,7 +261,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
   // mirror-pair stencils of the unit's parts (<= FT_WPARTS) x row kinds of the
   // tile (interior x kind), double-buffered by unit so staging the next
   // unit's needs no barrier beyond the unit-start one
-  __shared__ __align__(16) Acc s_w[2][FT_WPARTS * 4 * 16 * NSTP];
+  __shared__ __align__(16) Acc s_w[2][FT_WPARTS * 4 * 16 * NSTP_S];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = a.H, W = a.W;
   const int64_t P = a.P;
@@ -300,12 +305,18 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
     if (npu > FT_WPARTS) __trap();
     Acc* sw = s_w[((u - blockIdx.x) / gridDim.x) & 1];
     {
-      const int per_k = 16 * NSTP, n = npu * nky * per_k;
+      const int per_k = 16 * NSTP_S, n = npu * nky * per_k;
       for (int i = tid; i < n; i += FT_THREADS) {
         const int e = i % per_k, q = i / per_k;
+        const int t = e / NSTP_S, d = e - t * NSTP_S;
         const int iy = q % nky, pi = q / nky;
         const int kind = a.kmap[NKIND1 + kyl[iy]] * a.nkx + kint;
-        sw[i] = kpm[((size_t)(s_first + pi) * a.NK + kind) * per_k + e];
+        int src = d;                                       // fp32: already the run layout
+        if constexpr (F64) {
+          if (d < NPP) src = d < NPAIR ? L::plus(d) : ((MID && d == NPAIR) ? L::mid() : -1);
+          else src = (d - NPP < NPAIR) ? L::minus(d - NPP) : -1;
+        }
+        sw[i] = src >= 0 ? kpm[(((size_t)(s_first + pi) * a.NK + kind) * 16 + t) * NSTP + src] : (Acc)0;
       }
     }
     const uint32_t seq0 = load_seq;
@@ -338,20 +349,80 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
       const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
       const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
       const bool sd_exact = a.sd_inexact != nullptr && (a.sd_inexact[k] | a.sd_inexact[k + 1]) == 0;
-      auto row_steps = [&](auto exact_c) {
-      constexpr bool EXACT = decltype(exact_c)::value;
-#pragma unroll 1
-      for (int rs = 0; rs < FT_TY / WY; ++rs) {
-        const int r = wy + rs * WY;                        // tile row (warp-uniform)
-        const int gy = y0 + r;
-        if (gy >= H || !col_ok) continue;
+      // x<->y symmetric interior rows (fp64, integer planes): pair sums of S
+      // and D are exact in fp32 when |known| < 2^22 (|S1 + S2| <= 2^24)
+      const bool sym_ok = F64 && sd_exact && fmaxf(fabsf(lo), fabsf(hi)) < 4194304.f;
+      // one 7-wide row of the two planes' tiles (columns x-1 .. x+COLS+1)
+      auto load_rows = [&](int rr, float* fa, float* fb) {
+        const float* ra = bufA + rr * FT_SX + COLS * lc;
+        const float* rb = bufB + rr * FT_SX + COLS * lc;
+        if constexpr (COLS == 4) {
+          const float4 a0 = *reinterpret_cast<const float4*>(ra);
+          const float4 a1 = *reinterpret_cast<const float4*>(ra + 4);
+          const float2 a2 = *reinterpret_cast<const float2*>(ra + 8);
+          const float4 b0 = *reinterpret_cast<const float4*>(rb);
+          const float4 b1 = *reinterpret_cast<const float4*>(rb + 4);
+          const float2 b2 = *reinterpret_cast<const float2*>(rb + 8);
+          fa[0] = a0.w; fa[1] = a1.x; fa[2] = a1.y; fa[3] = a1.z; fa[4] = a1.w; fa[5] = a2.x; fa[6] = a2.y;
+          fb[0] = b0.w; fb[1] = b1.x; fb[2] = b1.y; fb[3] = b1.z; fb[4] = b1.w; fb[5] = b2.x; fb[6] = b2.y;
+        } else {
+          const float a0 = ra[3];
+          const float2 a1 = *reinterpret_cast<const float2*>(ra + 4);
+          const float2 a2 = *reinterpret_cast<const float2*>(ra + 6);
+          const float b0 = rb[3];
+          const float2 b1 = *reinterpret_cast<const float2*>(rb + 4);
+          const float2 b2 = *reinterpret_cast<const float2*>(rb + 6);
+          fa[0] = a0; fa[1] = a1.x; fa[2] = a1.y; fa[3] = a2.x; fa[4] = a2.y;
+          fb[0] = b0; fb[1] = b1.x; fb[2] = b1.y; fb[3] = b2.x; fb[4] = b2.y;
+        }
+      };
+      // stores of one row step: known planes through, G predictions clamped
+      auto emit = [&](int gy, int kyr, const float* selfA, const float* selfB, auto out_of) {
+        const int64_t pix = (int64_t)gy * W + gx;
+        // known planes pass through bit-exactly (kriging.py:481)
+        st_cs_cols<COLS>(a.out + zk * P + pix, selfA);
+        if (copy_b) st_cs_cols<COLS>(a.out + (zk + G + 1) * P + pix, selfB);
+        if (VAR) {
+          for (int c = 0; c < COLS; ++c) a.var[zk * P + pix + c] = 0.0;
+          if (copy_b)
+            for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          float o[COLS];
+#pragma unroll
+          for (int c = 0; c < COLS; ++c) o[c] = fminf(fmaxf(out_of(j, c), lo), hi);
+          float* dst = a.out + (zk + 1 + j) * P + pix;
+          double* vdst = VAR ? a.var + (zk + 1 + j) * P + pix : nullptr;
+          const double vj =
+              VAR ? a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
+                             a.kmap[NKIND1 + kyr] * a.nkx + kint]
+                  : 0.0;
+          if (!xb0 && !xb1) {
+            st_cs_cols<COLS>(dst, o);
+            if (VAR)
+              for (int c = 0; c < COLS; ++c) vdst[c] = vj;
+          } else {
+#pragma unroll
+            for (int c = 0; c < COLS; ++c) {
+              const int xx = gx + c;
+              if (xx >= 1 && xx <= W - 3) {
+                dst[c] = o[c];
+                if (VAR) vdst[c] = vj;
+              }
+            }
+          }
+        }
+      };
+      // general row step: 16 taps, one window row at a time
+      auto row_general = [&](auto exact_c, int r, int gy, int kyr) {
+        constexpr bool EXACT = decltype(exact_c)::value;
         int iy = 0;                                        // row kind (border rows of edge tiles)
-        const int kyr = axis_kind(gy, H);
         for (int q = 1; q < nky; ++q)
           if (kyl[q] == kyr) iy = q;
-        const Acc* wk = sw + (size_t)((s - s_first) * nky + iy) * 16 * NSTP;
+        const Acc* wk = sw + (size_t)((s - s_first) * nky + iy) * 16 * NSTP_S;
         constexpr bool PAIRED = L::PAIRED;
-        constexpr int QP = PAIRED ? L::NPP / 2 : 1, QM = (PAIRED && L::NMP > 0) ? L::NMP / 2 : 1;
+        constexpr int QP = PAIRED ? NPP / 2 : 1, QM = (PAIRED && NMP > 0) ? NMP / 2 : 1;
         Acc accS[NPAIR > 0 ? NPAIR : 1][COLS], accD[NPAIR > 0 ? NPAIR : 1][COLS], accC[COLS];
         uint64_t aP[QP][COLS], aM[QM][COLS];               // fp32: stencil pairs (FFMA2)
 #pragma unroll
@@ -367,28 +438,8 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
         float selfA[COLS], selfB[COLS];
 #pragma unroll
         for (int oy = -1; oy <= 2; ++oy) {
-          const float* ra = bufA + (r + 1 + oy) * FT_SX + COLS * lc;
-          const float* rb = bufB + (r + 1 + oy) * FT_SX + COLS * lc;
           float fa[COLS + 3], fb[COLS + 3];
-          if constexpr (COLS == 4) {
-            const float4 a0 = *reinterpret_cast<const float4*>(ra);
-            const float4 a1 = *reinterpret_cast<const float4*>(ra + 4);
-            const float2 a2 = *reinterpret_cast<const float2*>(ra + 8);
-            const float4 b0 = *reinterpret_cast<const float4*>(rb);
-            const float4 b1 = *reinterpret_cast<const float4*>(rb + 4);
-            const float2 b2 = *reinterpret_cast<const float2*>(rb + 8);
-            fa[0] = a0.w; fa[1] = a1.x; fa[2] = a1.y; fa[3] = a1.z; fa[4] = a1.w; fa[5] = a2.x; fa[6] = a2.y;
-            fb[0] = b0.w; fb[1] = b1.x; fb[2] = b1.y; fb[3] = b1.z; fb[4] = b1.w; fb[5] = b2.x; fb[6] = b2.y;
-          } else {
-            const float a0 = ra[3];
-            const float2 a1 = *reinterpret_cast<const float2*>(ra + 4);
-            const float2 a2 = *reinterpret_cast<const float2*>(ra + 6);
-            const float b0 = rb[3];
-            const float2 b1 = *reinterpret_cast<const float2*>(rb + 4);
-            const float2 b2 = *reinterpret_cast<const float2*>(rb + 6);
-            fa[0] = a0; fa[1] = a1.x; fa[2] = a1.y; fa[3] = a2.x; fa[4] = a2.y;
-            fb[0] = b0; fb[1] = b1.x; fb[2] = b1.y; fb[3] = b2.x; fb[4] = b2.y;
-          }
+          load_rows(r + 1 + oy, fa, fb);
           if (oy == 0) {
 #pragma unroll
             for (int c = 0; c < COLS; ++c) { selfA[c] = fa[c + 1]; selfB[c] = fb[c + 1]; }
@@ -410,97 +461,157 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
 #pragma unroll
           for (int ox = -1; ox <= 2; ++ox) {
             const int t = (oy + 1) * 4 + (ox + 1);
-            const Acc* wt = wk + t * NSTP;
+            const Acc* wt = wk + t * NSTP_S;
             if constexpr (PAIRED) {
               // two stencils per FFMA2 against the broadcast S (or D) value
 #pragma unroll
-              for (int q = 0; q < L::NPP / 2; ++q) {
+              for (int q = 0; q < NPP / 2; ++q) {
                 const uint64_t w2 = reinterpret_cast<const uint64_t*>(wt)[q];
 #pragma unroll
                 for (int c = 0; c < COLS; ++c)
                   aP[q][c] = f2fma(w2, f2pack(S[c + ox + 1], S[c + ox + 1]), aP[q][c]);
               }
 #pragma unroll
-              for (int q = 0; q < L::NMP / 2; ++q) {
-                const uint64_t w2 = reinterpret_cast<const uint64_t*>(wt + L::NPP)[q];
+              for (int q = 0; q < NMP / 2; ++q) {
+                const uint64_t w2 = reinterpret_cast<const uint64_t*>(wt + NPP)[q];
 #pragma unroll
                 for (int c = 0; c < COLS; ++c)
                   aM[q][c] = f2fma(w2, f2pack(D[c + ox + 1], D[c + ox + 1]), aM[q][c]);
               }
             } else {
+              double kp[NPP > 0 ? NPP : 2], km[NMP > 0 ? NMP : 2];
+#pragma unroll
+              for (int q = 0; q < NPP / 2; ++q) {
+                const double2 v = reinterpret_cast<const double2*>(wt)[q];
+                kp[2 * q] = v.x;
+                kp[2 * q + 1] = v.y;
+              }
+#pragma unroll
+              for (int q = 0; q < NMP / 2; ++q) {
+                const double2 v = reinterpret_cast<const double2*>(wt + NPP)[q];
+                km[2 * q] = v.x;
+                km[2 * q + 1] = v.y;
+              }
 #pragma unroll
               for (int p = 0; p < NPAIR; ++p) {
-                const P2 w2 = reinterpret_cast<const P2*>(wt)[p];
 #pragma unroll
                 for (int c = 0; c < COLS; ++c) {
-                  accS[p][c] = fma(w2.x, S[c + ox + 1], accS[p][c]);
-                  accD[p][c] = fma(w2.y, D[c + ox + 1], accD[p][c]);
+                  accS[p][c] = fma(kp[p], S[c + ox + 1], accS[p][c]);
+                  accD[p][c] = fma(km[p], D[c + ox + 1], accD[p][c]);
                 }
               }
               if (MID) {
-                const Acc wc = wt[2 * NPAIR];
 #pragma unroll
-                for (int c = 0; c < COLS; ++c) accC[c] = fma(wc, S[c + ox + 1], accC[c]);
+                for (int c = 0; c < COLS; ++c) accC[c] = fma(kp[NPAIR], S[c + ox + 1], accC[c]);
               }
             }
           }
         }
-        const int64_t pix = (int64_t)gy * W + gx;
-        // known planes pass through bit-exactly (kriging.py:481)
-        st_cs_cols<COLS>(a.out + zk * P + pix, selfA);
-        if (copy_b) st_cs_cols<COLS>(a.out + (zk + G + 1) * P + pix, selfB);
-        if (VAR) {
-          for (int c = 0; c < COLS; ++c) a.var[zk * P + pix + c] = 0.0;
-          if (copy_b)
-            for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-          float o[COLS];
+        emit(gy, kyr, selfA, selfB, [&](int j, int c) -> float {
+          Acc t;
+          if constexpr (PAIRED) {
+            auto pv = [&](int i) { return (i & 1) ? f2hi(aP[i >> 1][c]) : f2lo(aP[i >> 1][c]); };
+            auto mv = [&](int i) { return (i & 1) ? f2hi(aM[i >> 1][c]) : f2lo(aM[i >> 1][c]); };
+            if (MID && j == NPAIR) t = pv(NPAIR);
+            else if (j < NPAIR) t = pv(j) + mv(j);
+            else t = pv(G - 1 - j) - mv(G - 1 - j);
+          } else {
+            if (MID && j == NPAIR) t = accC[c];
+            else if (j < NPAIR) t = accS[j][c] + accD[j][c];
+            else t = accS[G - 1 - j][c] - accD[G - 1 - j][c];
+          }
+          return (float)t;
+        });
+      };
+      // x<->y symmetric interior row step (fp64, integer planes).  Interior
+      // stencils satisfy K(ox, oy) = K(oy, ox) (isotropic covariance; the
+      // drift span is closed under x <-> y; the table is symmetrised), so
+      // sum_t K_t v_t = sum_diag K v + sum_{ox<oy} K (v(ox,oy) + v(oy,ox)):
+      // 10 DFMA per stencil instead of 16.  The 4 x (COLS+3) windows of S
+      // and then D are held in fp32 registers (exact integers) so the
+      // transposed partner of each tap is a register, and each pair sum is
+      // exact in fp32 (|known| < 2^22) before its one conversion.
+      auto row_sym = [&](int r, int gy) {
+        if constexpr (F64) {
+          const Acc* wk = sw + (size_t)((s - s_first) * nky + 0) * 16 * NSTP_S;   // interior rows: iy = 0
+          double accS[NPAIR > 0 ? NPAIR : 1][COLS], accD[NPAIR > 0 ? NPAIR : 1][COLS], accC[COLS];
+          float selfA[COLS], selfB[COLS];
+          float Wv[4][COLS + 3];
 #pragma unroll
           for (int c = 0; c < COLS; ++c) {
-            Acc t;
-            if constexpr (PAIRED) {
-              auto pv = [&](int i) { return (i & 1) ? f2hi(aP[i >> 1][c]) : f2lo(aP[i >> 1][c]); };
-              auto mv = [&](int i) { return (i & 1) ? f2hi(aM[i >> 1][c]) : f2lo(aM[i >> 1][c]); };
-              if (MID && j == NPAIR) t = pv(NPAIR);
-              else if (j < NPAIR) t = pv(j) + mv(j);
-              else t = pv(G - 1 - j) - mv(G - 1 - j);
-            } else {
-              if (MID && j == NPAIR) t = accC[c];
-              else if (j < NPAIR) t = accS[j][c] + accD[j][c];
-              else t = accS[G - 1 - j][c] - accD[G - 1 - j][c];
-            }
-            o[c] = fminf(fmaxf((float)t, lo), hi);
-          }
-          float* dst = a.out + (zk + 1 + j) * P + pix;
-          double* vdst = VAR ? a.var + (zk + 1 + j) * P + pix : nullptr;
-          const double vj =
-              VAR ? a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
-                             a.kmap[NKIND1 + kyr] * a.nkx + kint]
-                    : 0.0;
-          if (!xb0 && !xb1) {
-            st_cs_cols<COLS>(dst, o);
-            if (VAR)
-              for (int c = 0; c < COLS; ++c) vdst[c] = vj;
-          } else {
+            accC[c] = 0.0;
 #pragma unroll
-            for (int c = 0; c < COLS; ++c) {
-              const int xx = gx + c;
-              if (xx >= 1 && xx <= W - 3) {
-                dst[c] = o[c];
-                if (VAR) vdst[c] = vj;
+            for (int p = 0; p < NPAIR; ++p) { accS[p][c] = 0.0; accD[p][c] = 0.0; }
+          }
+#pragma unroll
+          for (int ph = 0; ph < 2; ++ph) {                 // 0: S = A + B, 1: D = A - B
+#pragma unroll
+            for (int oy = -1; oy <= 2; ++oy) {
+              float fa[COLS + 3], fb[COLS + 3];
+              load_rows(r + 1 + oy, fa, fb);
+              if (ph == 0 && oy == 0) {
+#pragma unroll
+                for (int c = 0; c < COLS; ++c) { selfA[c] = fa[c + 1]; selfB[c] = fb[c + 1]; }
+              }
+#pragma unroll
+              for (int i = 0; i < COLS + 3; ++i) Wv[oy + 1][i] = ph == 0 ? fa[i] + fb[i] : fa[i] - fb[i];
+            }
+#pragma unroll
+            for (int by = 0; by < 4; ++by) {
+#pragma unroll
+              for (int bx = 0; bx <= by; ++bx) {            // tap (ox, oy) = (bx - 1, by - 1)
+                const Acc* wt = wk + (by * 4 + bx) * NSTP_S + (ph == 0 ? 0 : NPP);
+                constexpr int NW = NPP > NMP ? NPP : NMP;
+                double kw[NW > 0 ? NW : 2];
+#pragma unroll
+                for (int q = 0; q < (ph == 0 ? NPP : NMP) / 2; ++q) {
+                  const double2 v = reinterpret_cast<const double2*>(wt)[q];
+                  kw[2 * q] = v.x;
+                  kw[2 * q + 1] = v.y;
+                }
+#pragma unroll
+                for (int c = 0; c < COLS; ++c) {
+                  const float v = bx == by ? Wv[by][c + bx] : Wv[by][c + bx] + Wv[bx][c + by];
+                  const double pd = (double)v;
+                  if (ph == 0) {
+#pragma unroll
+                    for (int p = 0; p < NPAIR; ++p) accS[p][c] = fma(kw[p], pd, accS[p][c]);
+                    if (MID) accC[c] = fma(kw[NPAIR], pd, accC[c]);
+                  } else {
+#pragma unroll
+                    for (int p = 0; p < NPAIR; ++p) accD[p][c] = fma(kw[p], pd, accD[p][c]);
+                  }
+                }
               }
             }
           }
+          emit(gy, AXIS_INTERIOR, selfA, selfB, [&](int j, int c) -> float {
+            double t;
+            if (MID && j == NPAIR) t = accC[c];
+            else if (j < NPAIR) t = accS[j][c] + accD[j][c];
+            else t = accS[G - 1 - j][c] - accD[G - 1 - j][c];
+            return (float)t;
+          });
         }
-      }
       };
-      if constexpr (std::is_same<Acc, double>::value) {
-        if (sd_exact) row_steps(std::true_type{});
-        else row_steps(std::false_type{});
+      auto row_steps = [&](auto exact_c, auto sym_c) {
+        constexpr bool SYM = decltype(sym_c)::value;
+#pragma unroll 1
+        for (int rs = 0; rs < FT_TY / WY; ++rs) {
+          const int r = wy + rs * WY;                      // tile row (warp-uniform)
+          const int gy = y0 + r;
+          if (gy >= H || !col_ok) continue;
+          const int kyr = axis_kind(gy, H);
+          if (SYM && kyr == AXIS_INTERIOR) row_sym(r, gy);
+          else row_general(exact_c, r, gy, kyr);
+        }
+      };
+      if constexpr (F64) {
+        if (sym_ok) row_steps(std::true_type{}, std::true_type{});
+        else if (sd_exact) row_steps(std::true_type{}, std::false_type{});
+        else row_steps(std::false_type{}, std::false_type{});
       } else {
-        row_steps(std::false_type{});
+        row_steps(std::false_type{}, std::false_type{});
       }
       // ---- border columns x in {0, W-2, W-1}: one thread per (row, column),
       // all G planes with the column's window kind, same mirror-pair form

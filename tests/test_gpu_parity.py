@@ -302,3 +302,28 @@ def test_non_finite_known_value_fails_its_part(cuda, bad):
     o2, _ = fresh.run(torch.from_numpy(ks).cuda())
     fresh.finish()
     assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("scale", [1.0, 1500.0])
+def test_symmetric_interior_rows_parity(cuda, scale):
+    """Integer planes take the x<->y symmetric interior row form (pair sums
+    exact in fp32 while |known| < 2^22, checked with the part's clamp
+    range); a part holding a larger integer keeps the 16-tap form.  Both against the oracle at the fp64
+    gate, with the oracle's models, for the three kinds of the fast path's
+    G (1, 3, 7)."""
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    for f in (2, 4, 8):
+        cfg = small_config("spine", 44, 140, 5, f, n_subparts=1, seed=900 + f)
+        ks = np.rint(known_slices(cfg) * scale).astype(np.float32)
+        if scale > 1:
+            ks[0, 0, 0] = 6_000_000.0           # one part-wide magnitude above 2^22
+        ref, _, rmodels = O.reconstruct_zparts(ks, f, 1)
+        zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, f, 1, fit=False)
+        assert zk.plan.info["fast_path"] == 1
+        out, _ = zk.run(torch.from_numpy(ks).cuda(),
+                        models=[VariogramModel("exponential", m.nugget, m.sill, m.range_len)
+                                for m in rmodels])
+        zk.finish()
+        assert np.abs(out.cpu().numpy().astype(np.float64) - ref).max() <= TOL64 * _rng(ks)
