@@ -139,6 +139,20 @@ __device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
                : "memory");
 }
 
+// predicated streaming stores (one instruction each, no branch)
+__device__ __forceinline__ void st_cs_f4_if(float* p, const float* v, bool c) {
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %5, 0; @q st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};}"
+               ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "r"((unsigned)c) : "memory");
+}
+__device__ __forceinline__ void st_cs_f2_if(float* p, float x, float y, bool c) {
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %3, 0; @q st.global.cs.v2.f32 [%0], {%1, %2};}"
+               ::"l"(p), "f"(x), "f"(y), "r"((unsigned)c) : "memory");
+}
+__device__ __forceinline__ void st_cs_f1_if(float* p, float x, bool c) {
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.cs.f32 [%0], %1;}"
+               ::"l"(p), "f"(x), "r"((unsigned)c) : "memory");
+}
+
 template <int COLS>
 __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
   if constexpr (COLS == 4) {
@@ -150,6 +164,9 @@ __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
 
 #ifndef VK_FT_COLS
 #define VK_FT_COLS 4
+#endif
+#ifndef VK_FT_SYM32
+#define VK_FT_SYM32 1                    // x<->y symmetric interior rows in the fp32 kernel (G <= 4)
 #endif
 
 // Mirror-pair stencil table for the streaming kernel (one thread per
@@ -387,28 +404,38 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
           if (copy_b)
             for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
         }
+        float* dst = a.out + (zk + 1) * P + pix;
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
+        for (int j = 0; j < G; ++j, dst += P) {
           float o[COLS];
 #pragma unroll
           for (int c = 0; c < COLS; ++c) o[c] = fminf(fmaxf(out_of(j, c), lo), hi);
-          float* dst = a.out + (zk + 1 + j) * P + pix;
-          double* vdst = VAR ? a.var + (zk + 1 + j) * P + pix : nullptr;
-          const double vj =
-              VAR ? a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
-                             a.kmap[NKIND1 + kyr] * a.nkx + kint]
-                  : 0.0;
-          if (!xb0 && !xb1) {
-            st_cs_cols<COLS>(dst, o);
-            if (VAR)
-              for (int c = 0; c < COLS; ++c) vdst[c] = vj;
+          if constexpr (COLS == 4 && !VAR) {
+            // border columns (x = 0, W-2, W-1) belong to the border pass:
+            // predicated stores, no divergent branch (groups at x = 0 and
+            // x = W-4 hold them; W % 4 == 0 on the streaming path)
+            st_cs_f4_if(dst, o, !xb0 && !xb1);
+            st_cs_f1_if(dst + 1, o[1], xb0);
+            st_cs_f2_if(dst + 2, o[2], o[3], xb0);
+            st_cs_f2_if(dst, o[0], o[1], xb1 && !xb0);
           } else {
+            double* vdst = VAR ? a.var + (zk + 1 + j) * P + pix : nullptr;
+            const double vj =
+                VAR ? a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
+                               a.kmap[NKIND1 + kyr] * a.nkx + kint]
+                    : 0.0;
+            if (!xb0 && !xb1) {
+              st_cs_cols<COLS>(dst, o);
+              if (VAR)
+                for (int c = 0; c < COLS; ++c) vdst[c] = vj;
+            } else {
 #pragma unroll
-            for (int c = 0; c < COLS; ++c) {
-              const int xx = gx + c;
-              if (xx >= 1 && xx <= W - 3) {
-                dst[c] = o[c];
-                if (VAR) vdst[c] = vj;
+              for (int c = 0; c < COLS; ++c) {
+                const int xx = gx + c;
+                if (xx >= 1 && xx <= W - 3) {
+                  dst[c] = o[c];
+                  if (VAR) vdst[c] = vj;
+                }
               }
             }
           }
@@ -532,35 +559,45 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
       // transposed partner of each tap is a register, and each pair sum is
       // exact in fp32 (|known| < 2^22) before its one conversion.
       auto row_sym = [&](int r, int gy) {
-        if constexpr (F64) {
-          const Acc* wk = sw + (size_t)((s - s_first) * nky + 0) * 16 * NSTP_S;   // interior rows: iy = 0
-          double accS[NPAIR > 0 ? NPAIR : 1][COLS], accD[NPAIR > 0 ? NPAIR : 1][COLS], accC[COLS];
-          float selfA[COLS], selfB[COLS];
-          float Wv[4][COLS + 3];
+        const Acc* wk = sw + (size_t)((s - s_first) * nky + 0) * 16 * NSTP_S;   // interior rows: iy = 0
+        constexpr int QP = NPP / 2, QM = NMP > 0 ? NMP / 2 : 1;
+        double accS[F64 && NPAIR > 0 ? NPAIR : 1][COLS], accD[F64 && NPAIR > 0 ? NPAIR : 1][COLS];
+        double accC[F64 ? COLS : 1];
+        uint64_t aP[F64 ? 1 : QP][COLS], aM[F64 ? 1 : QM][COLS];   // fp32: stencil pairs (FFMA2)
+        float selfA[COLS], selfB[COLS];
+        float Wv[4][COLS + 3];
 #pragma unroll
-          for (int c = 0; c < COLS; ++c) {
+        for (int c = 0; c < COLS; ++c) {
+          if constexpr (F64) {
             accC[c] = 0.0;
 #pragma unroll
             for (int p = 0; p < NPAIR; ++p) { accS[p][c] = 0.0; accD[p][c] = 0.0; }
+          } else {
+#pragma unroll
+            for (int q = 0; q < QP; ++q) aP[q][c] = 0;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) aM[q][c] = 0;
           }
+        }
 #pragma unroll
-          for (int ph = 0; ph < 2; ++ph) {                 // 0: S = A + B, 1: D = A - B
+        for (int ph = 0; ph < 2; ++ph) {                   // 0: S = A + B, 1: D = A - B
 #pragma unroll
-            for (int oy = -1; oy <= 2; ++oy) {
-              float fa[COLS + 3], fb[COLS + 3];
-              load_rows(r + 1 + oy, fa, fb);
-              if (ph == 0 && oy == 0) {
+          for (int oy = -1; oy <= 2; ++oy) {
+            float fa[COLS + 3], fb[COLS + 3];
+            load_rows(r + 1 + oy, fa, fb);
+            if (ph == 0 && oy == 0) {
 #pragma unroll
-                for (int c = 0; c < COLS; ++c) { selfA[c] = fa[c + 1]; selfB[c] = fb[c + 1]; }
-              }
-#pragma unroll
-              for (int i = 0; i < COLS + 3; ++i) Wv[oy + 1][i] = ph == 0 ? fa[i] + fb[i] : fa[i] - fb[i];
+              for (int c = 0; c < COLS; ++c) { selfA[c] = fa[c + 1]; selfB[c] = fb[c + 1]; }
             }
 #pragma unroll
-            for (int by = 0; by < 4; ++by) {
+            for (int i = 0; i < COLS + 3; ++i) Wv[oy + 1][i] = ph == 0 ? fa[i] + fb[i] : fa[i] - fb[i];
+          }
 #pragma unroll
-              for (int bx = 0; bx <= by; ++bx) {            // tap (ox, oy) = (bx - 1, by - 1)
-                const Acc* wt = wk + (by * 4 + bx) * NSTP_S + (ph == 0 ? 0 : NPP);
+          for (int by = 0; by < 4; ++by) {
+#pragma unroll
+            for (int bx = 0; bx <= by; ++bx) {              // tap (ox, oy) = (bx - 1, by - 1)
+              const Acc* wt = wk + (by * 4 + bx) * NSTP_S + (ph == 0 ? 0 : NPP);
+              if constexpr (F64) {
                 constexpr int NW = NPP > NMP ? NPP : NMP;
                 double kw[NW > 0 ? NW : 2];
 #pragma unroll
@@ -582,17 +619,42 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
                     for (int p = 0; p < NPAIR; ++p) accD[p][c] = fma(kw[p], pd, accD[p][c]);
                   }
                 }
+              } else {
+                uint64_t kw[QP > QM ? QP : QM];
+#pragma unroll
+                for (int q = 0; q < (ph == 0 ? QP : (NMP > 0 ? QM : 0)); ++q)
+                  kw[q] = reinterpret_cast<const uint64_t*>(wt)[q];
+#pragma unroll
+                for (int c = 0; c < COLS; ++c) {
+                  const float v = bx == by ? Wv[by][c + bx] : Wv[by][c + bx] + Wv[bx][c + by];
+                  const uint64_t vv = f2pack(v, v);
+                  if (ph == 0) {
+#pragma unroll
+                    for (int q = 0; q < QP; ++q) aP[q][c] = f2fma(kw[q], vv, aP[q][c]);
+                  } else if (NMP > 0) {
+#pragma unroll
+                    for (int q = 0; q < QM; ++q) aM[q][c] = f2fma(kw[q], vv, aM[q][c]);
+                  }
+                }
               }
             }
           }
-          emit(gy, AXIS_INTERIOR, selfA, selfB, [&](int j, int c) -> float {
+        }
+        emit(gy, AXIS_INTERIOR, selfA, selfB, [&](int j, int c) -> float {
+          if constexpr (F64) {
             double t;
             if (MID && j == NPAIR) t = accC[c];
             else if (j < NPAIR) t = accS[j][c] + accD[j][c];
             else t = accS[G - 1 - j][c] - accD[G - 1 - j][c];
             return (float)t;
-          });
-        }
+          } else {
+            auto pv = [&](int i) { return (i & 1) ? f2hi(aP[i >> 1][c]) : f2lo(aP[i >> 1][c]); };
+            auto mv = [&](int i) { return (i & 1) ? f2hi(aM[i >> 1][c]) : f2lo(aM[i >> 1][c]); };
+            if (MID && j == NPAIR) return pv(NPAIR);
+            if (j < NPAIR) return pv(j) + mv(j);
+            return pv(G - 1 - j) - mv(G - 1 - j);
+          }
+        });
       };
       auto row_steps = [&](auto exact_c, auto sym_c) {
         constexpr bool SYM = decltype(sym_c)::value;
@@ -611,7 +673,11 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
         else if (sd_exact) row_steps(std::true_type{}, std::false_type{});
         else row_steps(std::false_type{}, std::false_type{});
       } else {
-        row_steps(std::false_type{}, std::false_type{});
+        // fp32: pair sums round like every other fp32 operation (1e-3 gate)
+        // (measured: C5 (G = 3) 2.757 -> 2.654 ms; C4 (G = 7) 0.628 -> 0.635 ms,
+        // so the 16-tap form stays for G > 4)
+        if (VK_FT_SYM32 && G <= 4) row_steps(std::false_type{}, std::true_type{});
+        else row_steps(std::false_type{}, std::false_type{});
       }
       // ---- border columns x in {0, W-2, W-1}: one thread per (row, column),
       // all G planes with the column's window kind, same mirror-pair form
