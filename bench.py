@@ -328,17 +328,24 @@ def run_gpu(args, cfg, ks):
     alg_bytes = 4 * (K_loc + T) * H * W + (8 * T * H * W if args.variance else 0)
     pred_avg = float(np.mean(pred_ms))
     achieved = alg_bytes / (pred_avg / 1e3) / 1e9
-    # fp64 pipe cap of the streaming kernel: 16 DFMA per voxel (mirror-pair
-    # stencils) + 2 DADD (S/D) at the measured 58 DFMA/clk/SM (tools/
-    # fp64_microbench.cu, profiles/fp64_microbench_r01.json)
-    fp64_cap = 148 * 58 * sm_max * 1e6 / 18
+    # fp64 pipe cap of the streaming kernel at the measured 58 DFMA/clk/SM
+    # (tools/fp64_microbench.cu, profiles/fp64_microbench_r01.json).  FP64
+    # pipe operations per voxel: integer planes below 2^22 take the x<->y
+    # symmetric interior rows -- 10 DFMA + 20/G pair-sum conversions + 1
+    # output conversion + 2*floor(G/2)/G mirror-pair DADDs; other data the
+    # 16-tap form -- 16 DFMA + 2 DADD (S, D) + 1 + 2*floor(G/2)/G
+    G = f - 1
+    sym = bool(np.all(ks == np.rint(ks)) and float(np.abs(ks).max()) < 2.0 ** 22)
+    fp64_ops = (10 + 20 / G if sym else 18) + 1 + 2 * (G // 2) / G
+    fp64_cap = 148 * 58 * sm_max * 1e6 / fp64_ops
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": _profile_traffic(args.accum),
             "kernel": "predict_fast_kernel", "bytes_per_launch": alg_bytes,
             "launch_ms": pred_avg, "peak_kind": peak_kind,
             "launch_ms_from": "serial schedule, CUDA events around the prediction launch",
             "fp64_pipe_frac": (vox_local / (pred_avg / 1e3)) / fp64_cap
-            if args.accum == "fp64" else None}
+            if args.accum == "fp64" else None,
+            "fp64_ops_per_voxel": round(fp64_ops, 3) if args.accum == "fp64" else None}
     stages = {k2: v / args.steps for k2, v in stage_acc.items()}
     stages["sum_serial"] = serial_ms
 

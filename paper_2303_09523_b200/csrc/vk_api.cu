@@ -688,6 +688,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       }
       for (auto& e : tev) cudaEventDestroy(e);
       cudaEventDestroy(t_start);
+      (void)cudaGetLastError();                  // elapsed-time queries on unrecorded events
     }
     VK_CUDA(mark(4));
     VK_CUDA(mark(5));

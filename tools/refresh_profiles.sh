@@ -14,4 +14,14 @@ $CMD --serial > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-c
   --log-file $O/launches_serial.csv $CMD --serial > $O/ncu_serial.log 2>&1
 $CMD > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/launches_chained.csv $CMD > $O/ncu_chained.log 2>&1
-echo done
+echo bench+launches done
+# one full ncu capture per prediction mode (traffic, pipes, stalls) and of
+# the stage kernels (solve / fit / bins / pair draw / stats)
+NCMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-pipelined --serial"
+for m in fp64 fp32; do
+  ncu --set full --clock-control none --import-source on -k regex:predict_fast_kernel -s 2 -c 1 \
+    -o $O/predict_$m $NCMD --accum $m > $O/ncu_predict_$m.log 2>&1
+done
+ncu --set full --clock-control none --import-source on -k "regex:(solve|fit|bins|pair_draw|plane_stats)_kernel" \
+  -s 10 -c 5 -o $O/stages $NCMD > $O/ncu_stages.log 2>&1
+echo ncu done
