@@ -118,8 +118,15 @@ constexpr int FT_BUF_FLOATS = ((FT_SX * FT_SY * 4 + 127) / 128) * 128 / 4;
 // registers, so three CTAs share an SM (3-deep ring); larger G keeps 128
 // registers, two CTAs and a 4-deep ring (C5 fp32: 58.9 -> 60.6 % of the HBM
 // roofline; C4 (G = 7) spills at 80 registers and stays at two CTAs).
-__host__ __device__ constexpr int ft_stages(int G) { return G <= 4 ? 3 : 4; }
-__host__ __device__ constexpr int ft_minb(int G) { return G <= 4 ? 3 : VK_FT_MINB; }
+#ifndef VK_FT_F32_MINB3
+#define VK_FT_F32_MINB3 0                // fp32 kernel: three CTAs per SM at every G
+#endif
+__host__ __device__ constexpr int ft_stages(int G, bool f32 = false) {
+  return (G <= 4 || (f32 && VK_FT_F32_MINB3)) ? 3 : 4;
+}
+__host__ __device__ constexpr int ft_minb(int G, bool f32 = false) {
+  return (G <= 4 || (f32 && VK_FT_F32_MINB3)) ? 3 : VK_FT_MINB;
+}
 constexpr int FT_WPARTS = 4;             // parts whose stencils a unit stages
 
 template <typename Acc>
@@ -166,7 +173,10 @@ __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
 #define VK_FT_COLS 4
 #endif
 #ifndef VK_FT_SYM32
-#define VK_FT_SYM32 1                    // x<->y symmetric interior rows in the fp32 kernel (G <= 4)
+#define VK_FT_SYM32 1                    // x<->y symmetric interior rows in the fp32 kernel
+#endif
+#ifndef VK_FT_SYM32_MAXG
+#define VK_FT_SYM32_MAXG 4               // ... for gaps of up to this many missing planes
 #endif
 
 // Mirror-pair stencil table for the streaming kernel (one thread per
@@ -257,7 +267,7 @@ __device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
 // FP64 pipe of an SM sub-partition sees a mix of DFMA-heavy and
 // load/convert/store phases instead of all warps in lock step.
 template <int G, typename Acc, bool VAR, int COLS = VK_FT_COLS>
-__global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
+__global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float>::value))
     predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
                         int n_tiles, int chunk, int n_units) {
   using L = StLayout<G, Acc>;
@@ -271,7 +281,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
   constexpr int NPP = LR::NPP, NMP = LR::NMP;
   constexpr int NSTP_S = NSTP > LR::NSTP ? NSTP : LR::NSTP;
   constexpr bool F64 = std::is_same<Acc, double>::value;
-  constexpr int FT_STAGES = ft_stages(G);
+  constexpr int FT_STAGES = ft_stages(G, std::is_same<Acc, float>::value);
   extern __shared__ __align__(128) float ring[];           // FT_STAGES x FT_BUF_FLOATS
   __shared__ __align__(8) uint64_t full[FT_STAGES];
   __shared__ int released[FT_STAGES];                      // warps done with the slot's plane
@@ -676,7 +686,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G))
         // fp32: pair sums round like every other fp32 operation (1e-3 gate)
         // (measured: C5 (G = 3) 2.757 -> 2.654 ms; C4 (G = 7) 0.628 -> 0.635 ms,
         // so the 16-tap form stays for G > 4)
-        if (VK_FT_SYM32 && G <= 4) row_steps(std::false_type{}, std::true_type{});
+        if (VK_FT_SYM32 && G <= VK_FT_SYM32_MAXG) row_steps(std::false_type{}, std::true_type{});
         else row_steps(std::false_type{}, std::false_type{});
       }
       // ---- border columns x in {0, W-2, W-1}: one thread per (row, column),
@@ -781,11 +791,11 @@ int predict_fast_supported(int G, int accum) {
   return G >= 1 && G <= 8;
 }
 
-static size_t fast_smem(int G) { return (size_t)ft_stages(G) * FT_BUF_FLOATS * sizeof(float); }
+static size_t fast_smem(int G, bool f32) { return (size_t)ft_stages(G, f32) * FT_BUF_FLOATS * sizeof(float); }
 
 template <int G, typename Acc>
 static cudaError_t occupancy_t(int* occ) {
-  const size_t smem = fast_smem(G);
+  const size_t smem = fast_smem(G, std::is_same<Acc, float>::value);
   cudaError_t e = cudaFuncSetAttribute(predict_fast_kernel<G, Acc, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
@@ -813,7 +823,7 @@ cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st) {
 
 template <int G, typename Acc>
 static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
-  const size_t smem = fast_smem(G);
+  const size_t smem = fast_smem(G, std::is_same<Acc, float>::value);
   const int ntx = (a.W + FT_TX - 1) / FT_TX, nty = (a.H + FT_TY - 1) / FT_TY;
   const int n_tiles = ntx * nty, n_gaps = a.gap1 - a.gap0;
   if (n_gaps <= 0) return cudaSuccess;
