@@ -270,9 +270,8 @@ def run_gpu(args, cfg, ks):
 
     def step():
         if world > 1:
-            halo = exchange_halo(stack[0], rank, world)
-            if halo is not None:
-                stack[cfg.n_known].copy_(halo)
+            # the next rank's first plane lands in the halo slot directly
+            exchange_halo(stack[0], rank, world, out=stack[cfg.n_known] if has_halo else None)
         zk.run(stack, out, var)
 
     for _ in range(max(3, args.warmup)):
@@ -490,9 +489,7 @@ def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):
         stream.wait_event(ev_in[b])
         stream.wait_event(ev_out[b])                   # output buffer downloaded (step i-2)
         if world > 1:
-            halo = exchange_halo(dev_in[b][0], rank, world)
-            if halo is not None:
-                dev_in[b][K].copy_(halo)
+            exchange_halo(dev_in[b][0], rank, world, out=dev_in[b][K] if has_halo else None)
         out, var = bufs[b]
         zk1.run(dev_in[b], out, var)
         ev_done[b].record(stream)

@@ -53,8 +53,9 @@ def strong_shard(n_known: int, n_parts: int, rank: int, world: int) -> Shard:
     return Shard(rank, world, k0, k1, not last, p0, per, q)
 
 
-def exchange_halo(first_plane, rank: int, world: int, group=None):
-    """Send our first known plane to rank-1; receive rank+1's (or None)."""
+def exchange_halo(first_plane, rank: int, world: int, group=None, out=None):
+    """Send our first known plane to rank-1; receive rank+1's (or None) into
+    ``out`` when given (e.g. the stack's trailing halo slot, no extra copy)."""
     import torch
     import torch.distributed as dist
     ops = []
@@ -62,7 +63,7 @@ def exchange_halo(first_plane, rank: int, world: int, group=None):
     if rank > 0:
         ops.append(dist.P2POp(dist.isend, first_plane.contiguous(), rank - 1, group))
     if rank < world - 1:
-        halo = torch.empty_like(first_plane)
+        halo = out if out is not None else torch.empty_like(first_plane)
         ops.append(dist.P2POp(dist.irecv, halo, rank + 1, group))
     if ops:
         for req in dist.batch_isend_irecv(ops):

@@ -46,6 +46,12 @@ def _worker(rank, world, port, ks, factor, n_parts, result_q):
     sh = strong_shard(ks.shape[0], n_parts, rank, world)
     owned = torch.from_numpy(ks[sh.k0:sh.k1 + 1].copy())
     vol = reconstruct_sharded(owned, factor, sh, reconstruct=_oracle_reconstruct)
+    # halo received in place (bench.py: straight into the stack's trailing slot)
+    from paper_2303_09523_b200.zshard import exchange_halo
+    slot = torch.full((2,) + ks.shape[1:], -1.0)
+    exchange_halo(owned[0].contiguous(), rank, world, out=slot[1] if rank < world - 1 else None)
+    if rank < world - 1:
+        assert torch.equal(slot[1], torch.from_numpy(ks[sh.k1 + 1]))   # rank + 1 owns k1 + 1 first
     if rank == 0:
         result_q.put(vol.numpy())
     dist.barrier()
