@@ -852,7 +852,10 @@ void CUDART_CB host_plane_copy(void* arg) {
   static const int env_threads = std::getenv("VK_HOST_COPY_THREADS") ? std::atoi(std::getenv("VK_HOST_COPY_THREADS")) : 0;
   const int K = (int)j->z.size();
   const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  const int nt = std::max(1, std::min({K, env_threads > 0 ? env_threads : std::min(8, hw)}));
+  // 4 threads: the copy shares host memory bandwidth with the concurrent
+  // device-to-host DMA (C4 e2e 39.3 / 37.9 / 38.0 / 39.3 ms per step with
+  // 8 / 4 / 2 / 16 threads on a 16-core host)
+  const int nt = std::max(1, std::min({K, env_threads > 0 ? env_threads : std::min(4, hw)}));
   auto work = [&](int t) {
     for (int k = t; k < K; k += nt) std::memcpy(j->dst + (size_t)j->z[k] * j->plane, j->src + (size_t)k * j->plane, j->plane);
   };
