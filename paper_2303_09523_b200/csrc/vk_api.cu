@@ -110,6 +110,9 @@ struct vk_plan {
   cudaEvent_t ev_hstats = nullptr, ev_hbins = nullptr;
   int head_parts = 0;
   std::vector<int> sys_begin;         // [S + 1] system range of each part
+  std::vector<int> sys_canon;         // [S] end of each part's solved (canonical) systems
+  int n_derived = 0;
+  int32_t *d_der_src = nullptr, *d_der_flags = nullptr;
   std::vector<int> gap_begin;         // [S + 1] gap range of each part (fast path)
   FastLaunch fast_launch;             // cached TMA descriptor + occupancy
   int ring = 0;                       // timing ring size (0 = off)
@@ -196,6 +199,81 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   }
   Geometry& g = p->geo;
   if (d->flags & VK_FLAG_FORCE_GENERIC) g.fast = false;
+  // ---- systems that are exact images of another system of the same part:
+  // the z-mirror of a plane pattern (offsets negated and reversed; the
+  // covariance is isotropic and the drift span {1, x, y, z} closed under
+  // z -> -z) and the x<->y transpose of a window kind.  Their weights are the
+  // solved system's with the planes reversed and / or the in-plane taps
+  // transposed (bit-identical variance), so only one system per orbit is
+  // solved (C4: 40 of 112 per part).  The reference solves each separately;
+  // the two solutions agree to solver rounding.  Within each part the solved
+  // systems come first.
+  std::vector<int32_t> der_src, der_flags;
+  {
+    const int NPq = (int)g.patterns.size(), NKq = g.n_kinds();
+    std::map<std::vector<int>, int> pat_index;
+    for (int q = 0; q < NPq; ++q) pat_index[g.patterns[q]] = q;
+    std::vector<int> pmir(NPq, -1), ktr(std::max(1, NKq), -1);
+    for (int q = 0; q < NPq; ++q) {
+      std::vector<int> m(g.patterns[q].rbegin(), g.patterns[q].rend());
+      for (int& v : m) v = -v;
+      auto it = pat_index.find(m);
+      if (it != pat_index.end()) pmir[q] = it->second;
+    }
+    for (int yc = 0; yc < g.nky; ++yc)
+      for (int xc = 0; xc < g.nkx; ++xc) {
+        const int y2 = g.ky_map[g.kx_list[xc]], x2 = g.kx_map[g.ky_list[yc]];
+        if (y2 >= 0 && x2 >= 0) ktr[yc * g.nkx + xc] = y2 * g.nkx + x2;
+      }
+    auto swapxy = [](int dc) { return (dc & 9) | ((dc & 2) << 1) | ((dc & 4) >> 1); };
+    const int n = (int)g.sys_part.size();
+    std::vector<int> order, src_of(n, -1), flag_of(n, 0);
+    std::vector<int> new_part, new_stencil;
+    p->sys_canon.assign(g.S, -1);                // -1: part without systems (fixed below)
+    int i0 = 0;
+    while (i0 < n) {
+      const int s = g.sys_part[i0];
+      int i1 = i0;
+      while (i1 < n && g.sys_part[i1] == s) ++i1;
+      std::map<int, int> by_stc;                  // stencil -> system index in this part
+      for (int i = i0; i < i1; ++i) by_stc[g.sys_stencil[i]] = i;
+      for (int i = i0; i < i1; ++i) {
+        const int stc = g.sys_stencil[i], pq = stc / std::max(1, NKq), kq = stc % std::max(1, NKq);
+        const int dc = g.stencils[stc].drift_cols;
+        int best = stc, bflag = 0;
+        for (int fl = 1; fl < 4; ++fl) {
+          const int p2 = (fl & 1) ? pmir[pq] : pq, k2 = (fl & 2) ? ktr[kq] : kq;
+          if (p2 < 0 || k2 < 0) continue;
+          const int stc2 = p2 * NKq + k2;
+          if (!by_stc.count(stc2)) continue;
+          if (g.patterns[p2].size() != g.patterns[pq].size()) continue;
+          if (g.stencils[stc2].drift_cols != ((fl & 2) ? swapxy(dc) : dc)) continue;
+          if (stc2 < best) { best = stc2; bflag = fl; }
+        }
+        if (best != stc) { src_of[i] = by_stc[best]; flag_of[i] = bflag | ((int)g.patterns[pq].size() << 8); }
+      }
+      // a system whose representative is itself derived solves itself (the
+      // orbit minimum is always solved, so this only guards odd orbits)
+      for (int i = i0; i < i1; ++i)
+        if (src_of[i] >= 0 && src_of[src_of[i]] >= 0) { src_of[i] = -1; flag_of[i] = 0; }
+      for (int i = i0; i < i1; ++i) if (src_of[i] < 0) order.push_back(i);
+      p->sys_canon[s] = (int)order.size();
+      for (int i = i0; i < i1; ++i) if (src_of[i] >= 0) order.push_back(i);
+      i0 = i1;
+    }
+    std::vector<int> new_index(n);
+    for (int j = 0; j < n; ++j) new_index[order[j]] = j;
+    der_src.assign(n, -1);
+    der_flags.assign(n, 0);
+    for (int j = 0; j < n; ++j) {
+      const int i = order[j];
+      new_part.push_back(g.sys_part[i]);
+      new_stencil.push_back(g.sys_stencil[i]);
+      if (src_of[i] >= 0) { der_src[j] = new_index[src_of[i]]; der_flags[j] = flag_of[i]; ++p->n_derived; }
+    }
+    g.sys_part.swap(new_part);
+    g.sys_stencil.swap(new_stencil);
+  }
   const int64_t P = (int64_t)g.H * g.W;
   if (d->fit_variogram) {
     for (const PartInfo& pi : g.parts)
@@ -265,6 +343,10 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   VK_TRY(p->put(&p->d_miss_planes, g.miss_planes));
   VK_TRY(p->put(&p->d_sys_part, g.sys_part));
   VK_TRY(p->put(&p->d_sys_stencil, g.sys_stencil));
+  if (!der_src.empty()) {
+    VK_TRY(p->put(&p->d_der_src, der_src));
+    VK_TRY(p->put(&p->d_der_flags, der_flags));
+  }
   VK_TRY(p->put(&p->d_st_off, st_off));
   VK_TRY(p->put(&p->d_st_n, st_n));
   VK_TRY(p->put(&p->d_st_drift, st_drift));
@@ -340,6 +422,8 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   p->sys_begin.assign(S + 1, 0);
   for (int i = 0; i < p->n_sys; ++i) p->sys_begin[g.sys_part[i] + 1]++;
   for (int s = 0; s < S; ++s) p->sys_begin[s + 1] += p->sys_begin[s];
+  for (int s = 0; s < S; ++s)
+    if (p->sys_canon[s] < 0) p->sys_canon[s] = p->sys_begin[s];
   p->gap_begin.assign(S + 1, 0);
   if (g.fast) {
     for (int s = 0; s <= S; ++s) p->gap_begin[s] = (s < S) ? g.parts[s].b : g.K - 1;
@@ -550,6 +634,8 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   sa.sys_status = p->d_sys_status;
   sa.max_n = p->max_n;
   sa.max_dz = p->max_dz;
+  sa.der_src = p->d_der_src;
+  sa.der_flags = p->d_der_flags;
   PredictArgs pa;
   pa.known = known;
   pa.out = out;
@@ -632,10 +718,16 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     for (int s = 0; s < S; ++s) {
       SolveArgs s1 = sa;
       s1.sys0 = p->sys_begin[s];
-      s1.n_sys = p->sys_begin[s + 1] - p->sys_begin[s];
+      s1.n_sys = p->sys_canon[s] - p->sys_begin[s];          // solved systems of the part
+      SolveArgs d1 = sa;
+      d1.sys0 = p->sys_canon[s];
+      d1.n_sys = p->sys_begin[s + 1] - p->sys_canon[s];      // its mirror / transpose images
       static const int diag_skip2 = std::getenv("VK_DIAG_SKIP") ? std::atoi(std::getenv("VK_DIAG_SKIP")) : 0;
-      if (!(diag_skip2 & 2) || p->n_runs == 0) VK_CUDA(launch_solve(s1, p->chain[s % nch]));
-      kernels += (s1.n_sys > 0);
+      if (!(diag_skip2 & 2) || p->n_runs == 0) {
+        VK_CUDA(launch_solve(s1, p->chain[s % nch]));
+        VK_CUDA(launch_derive(d1, p->chain[s % nch]));
+      }
+      kernels += (s1.n_sys > 0) + (d1.n_sys > 0 && d1.der_src);
       if (trace) cudaEventRecord(tev[2 + 3 * s], p->chain[s % nch]);
     }
     for (int s = 0; s < S; ++s) {
@@ -697,7 +789,8 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     ++kernels;
     VK_CUDA(mark(4));
     VK_CUDA(launch_solve(sa, st));
-    if (p->n_sys) ++kernels;
+    VK_CUDA(launch_derive(sa, st));
+    if (p->n_sys) kernels += 1 + (p->n_derived > 0);
     VK_CUDA(mark(5));
     if (fast) {
       VK_CUDA(launch_predict_fast_prepared(p->fast_launch, pa, st));

@@ -103,8 +103,15 @@ struct SolveArgs {
   int32_t* sys_status;       // [n_sys]
   int max_n;                 // max neighbours over stencils (smem sizing)
   int max_dz;                // max |plane offset| or offset difference over patterns
+  // derived systems (z-mirror / x<->y transpose images of a solved system of
+  // the same part): source system or -1, flags bit 0 mirror, bit 1 transpose,
+  // bits 8.. planes of the pattern.  launch_solve skips them; launch_derive
+  // fills their weights, variance and status from the source.
+  const int32_t* der_src = nullptr;
+  const int32_t* der_flags = nullptr;
 };
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st);
+cudaError_t launch_derive(const SolveArgs& a, cudaStream_t st);
 
 struct PredictArgs {
   const float* known;        // [K][H][W]

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sys = a.sys0 + blockIdx.x * ws + wid;
   if (wid >= ws || sys >= a.sys0 + a.n_sys) return;
+  if (a.der_src && a.der_src[sys] >= 0) return;   // filled by derive_kernel
   const int s = a.sys_part[sys], stc = a.sys_stencil[sys];
   const int n = a.st_n[stc], off = a.st_off[stc], dcols = a.st_drift[stc];
   const int pat = a.st_pattern[stc];
@@ -238,7 +239,37 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
   if (lane == 0) a.sys_status[sys] = done ? PS_OK : PS_SINGULAR;
 }
 
+// Derived systems: weights of the source system with the planes reversed
+// (z-mirror) and / or the in-plane taps transposed (x<->y), variance and
+// status copied.  One thread per (system, padded weight slot).
+__global__ void __launch_bounds__(256) derive_kernel(SolveArgs a) {
+  const int64_t total = (int64_t)a.n_sys * WPAD;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int sys = a.sys0 + (int)(i / WPAD), e = (int)(i % WPAD);
+    const int src = a.der_src[sys];
+    if (src < 0) continue;
+    const int fl = a.der_flags[sys], np = fl >> 8;
+    const int64_t dslot = (int64_t)a.sys_part[sys] * a.NP * a.NK + a.sys_stencil[sys];
+    const int64_t sslot = (int64_t)a.sys_part[src] * a.NP * a.NK + a.sys_stencil[src];
+    const int pl = e >> 4, t = e & 15;
+    const int spl = (fl & 1) ? np - 1 - pl : pl;
+    const int stp = (fl & 2) ? (t & 3) * 4 + (t >> 2) : t;
+    a.weights[dslot * WPAD + e] = pl < np ? a.weights[sslot * WPAD + spl * 16 + stp] : 0.0;
+    if (e == 0) {
+      a.var[dslot] = a.var[sslot];
+      a.sys_status[sys] = a.sys_status[src];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_derive(const SolveArgs& a, cudaStream_t st) {
+  if (a.n_sys <= 0 || !a.der_src) return cudaSuccess;
+  const int64_t total = (int64_t)a.n_sys * WPAD;
+  derive_kernel<<<(unsigned)std::min<int64_t>(1024, (total + 255) / 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st) {
   if (a.n_sys == 0) return cudaSuccess;
