@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256) generic_solve_kernel(SolveCtx ctx, const 
         if (tid == 0) { const double t = x[k]; x[k] = x[pi]; x[pi] = t; }
       }
       __syncthreads();
-      const double rp = 1.0 / pv;
+      const double rp = __drcp_rn(pv);                 // = 1.0 / pv, correctly rounded
       for (int i = k + 1 + tid; i < N; i += nt) A[(int64_t)i * N + k] *= rp;
       __syncthreads();
       const int rem = N - k - 1;

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
       // row's multiplier in a register and streams the pivot row (broadcast
       // loads) in batches of 8 columns, loads before stores (dgetf2's
       // arithmetic: l = a_rk * (1 / a_kk), a_rj -= l * a_kj)
-      const double inv = 1.0 / A[k * ld + k];
+      const double inv = __drcp_rn(A[k * ld + k]);   // = 1.0 / a_kk (both correctly rounded), no division call
       const double* Ak = A + (size_t)k * ld;
       for (int r = k + 1 + lane; r < N; r += 32) {
         double* Ar = A + (size_t)r * ld;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(32 * SOLVE_WARPS_MAX) solve_kernel(SolveArgs a
       // diagonal are formed off the dependent chain, which is then one
       // multiply, one shuffle and one FMA per row
       bool finite = true;
-      for (int r = lane; r < N; r += 32) rinv[r] = 1.0 / A[(size_t)r * ld + r];
+      for (int r = lane; r < N; r += 32) rinv[r] = __drcp_rn(A[(size_t)r * ld + r]);
       double y[YS];
 #pragma unroll
       for (int t = 0; t < YS; ++t) {
