@@ -327,3 +327,36 @@ def test_symmetric_interior_rows_parity(cuda, scale):
                                 for m in rmodels])
         zk.finish()
         assert np.abs(out.cpu().numpy().astype(np.float64) - ref).max() <= TOL64 * _rng(ks)
+
+
+@pytest.mark.parametrize("drift", ["linear", "constant"])
+def test_orbit_derived_systems_match_direct_solves(cuda, drift):
+    """Only one system per z-mirror / x<->y-transpose orbit is solved on the
+    device; the others are permuted copies (vk_solve.cu derive_kernel).  Every
+    system the plan holds -- solved or derived -- against the oracle's direct
+    solve of that stencil (kriging.py:159-245), weights and variance."""
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    f, G = 8, 7
+    cfg = small_config("spine", 24, 40, 3, f, n_subparts=1, seed=5)
+    ks = known_slices(cfg)
+    m = O.Model("exponential", 3.0, 900.0, 11.0)
+    zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, f, 1, fit=False, drift=drift)
+    zk.run(torch.from_numpy(ks).cuda(), models=[VariogramModel("exponential", m.nugget, m.sill, m.range_len)])
+    zk.finish()
+    w, v, ids = zk.plan.systems()
+    assert len(ids) == G * 16                       # 7 patterns x 4 x 4 kinds, all present
+    for i, (s, p, ky, kx) in enumerate(ids):
+        dz = (-(p + 1), G - p)                      # pattern p = missing plane p of a gap
+        rel, slots = [], []
+        for pl in range(2):
+            for oy in range(ky // 3 - 1, ky % 3 + 1):
+                for ox in range(kx // 3 - 1, kx % 3 + 1):
+                    rel.append((ox, oy, dz[pl]))
+                    slots.append(pl * 16 + (oy + 1) * 4 + (ox + 1))
+        ew, ev = O.stencil_weights(np.array(rel, float), m, drift)
+        got = w[i, slots]
+        assert np.abs(got - ew).max() <= 1e-9 * max(1.0, np.abs(ew).max()), (s, p, ky, kx)
+        assert abs(v[i] - ev) <= 1e-9 * m.sill, (s, p, ky, kx)
+        assert np.all(np.delete(w[i], slots) == 0.0)
