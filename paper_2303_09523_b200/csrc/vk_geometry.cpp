@@ -227,4 +227,84 @@ std::string build_geometry(int H, int W, int T, const int* known_z, int K, int S
   return "";
 }
 
+// Systems that are exact images of another system of the same part:
+// the z-mirror of a plane pattern (offsets negated and reversed; the
+// covariance is isotropic and the drift span {1, x, y, z} closed under
+// z -> -z) and the x<->y transpose of a window kind.  Their weights are the
+// solved system's with the planes reversed and / or the in-plane taps
+// transposed (bit-identical variance), so only one system per orbit is
+// solved (C4: 40 of 112 per part).  The reference solves each separately;
+// the two solutions agree to solver rounding.  Within each part the solved
+// systems come first.
+void canonical_systems(Geometry* gp, std::vector<int>* sys_canon, std::vector<int32_t>* der_src,
+                       std::vector<int32_t>* der_flags, int* n_derived) {
+  Geometry& g = *gp;
+  *n_derived = 0;
+  {
+    const int NPq = (int)g.patterns.size(), NKq = g.n_kinds();
+    std::map<std::vector<int>, int> pat_index;
+    for (int q = 0; q < NPq; ++q) pat_index[g.patterns[q]] = q;
+    std::vector<int> pmir(NPq, -1), ktr(std::max(1, NKq), -1);
+    for (int q = 0; q < NPq; ++q) {
+      std::vector<int> m(g.patterns[q].rbegin(), g.patterns[q].rend());
+      for (int& v : m) v = -v;
+      auto it = pat_index.find(m);
+      if (it != pat_index.end()) pmir[q] = it->second;
+    }
+    for (int yc = 0; yc < g.nky; ++yc)
+      for (int xc = 0; xc < g.nkx; ++xc) {
+        const int y2 = g.ky_map[g.kx_list[xc]], x2 = g.kx_map[g.ky_list[yc]];
+        if (y2 >= 0 && x2 >= 0) ktr[yc * g.nkx + xc] = y2 * g.nkx + x2;
+      }
+    auto swapxy = [](int dc) { return (dc & 9) | ((dc & 2) << 1) | ((dc & 4) >> 1); };
+    const int n = (int)g.sys_part.size();
+    std::vector<int> order, src_of(n, -1), flag_of(n, 0);
+    std::vector<int> new_part, new_stencil;
+    sys_canon->assign(g.S, -1);                  // -1: part without systems (the caller fixes)
+    int i0 = 0;
+    while (i0 < n) {
+      const int s = g.sys_part[i0];
+      int i1 = i0;
+      while (i1 < n && g.sys_part[i1] == s) ++i1;
+      std::map<int, int> by_stc;                  // stencil -> system index in this part
+      for (int i = i0; i < i1; ++i) by_stc[g.sys_stencil[i]] = i;
+      for (int i = i0; i < i1; ++i) {
+        const int stc = g.sys_stencil[i], pq = stc / std::max(1, NKq), kq = stc % std::max(1, NKq);
+        const int dc = g.stencils[stc].drift_cols;
+        int best = stc, bflag = 0;
+        for (int fl = 1; fl < 4; ++fl) {
+          const int p2 = (fl & 1) ? pmir[pq] : pq, k2 = (fl & 2) ? ktr[kq] : kq;
+          if (p2 < 0 || k2 < 0) continue;
+          const int stc2 = p2 * NKq + k2;
+          if (!by_stc.count(stc2)) continue;
+          if (g.patterns[p2].size() != g.patterns[pq].size()) continue;
+          if (g.stencils[stc2].drift_cols != ((fl & 2) ? swapxy(dc) : dc)) continue;
+          if (stc2 < best) { best = stc2; bflag = fl; }
+        }
+        if (best != stc) { src_of[i] = by_stc[best]; flag_of[i] = bflag | ((int)g.patterns[pq].size() << 8); }
+      }
+      // a system whose representative is itself derived solves itself (the
+      // orbit minimum is always solved, so this only guards odd orbits)
+      for (int i = i0; i < i1; ++i)
+        if (src_of[i] >= 0 && src_of[src_of[i]] >= 0) { src_of[i] = -1; flag_of[i] = 0; }
+      for (int i = i0; i < i1; ++i) if (src_of[i] < 0) order.push_back(i);
+      (*sys_canon)[s] = (int)order.size();
+      for (int i = i0; i < i1; ++i) if (src_of[i] >= 0) order.push_back(i);
+      i0 = i1;
+    }
+    std::vector<int> new_index(n);
+    for (int j = 0; j < n; ++j) new_index[order[j]] = j;
+    der_src->assign(n, -1);
+    der_flags->assign(n, 0);
+    for (int j = 0; j < n; ++j) {
+      const int i = order[j];
+      new_part.push_back(g.sys_part[i]);
+      new_stencil.push_back(g.sys_stencil[i]);
+      if (src_of[i] >= 0) { (*der_src)[j] = new_index[src_of[i]]; (*der_flags)[j] = flag_of[i]; ++*n_derived; }
+    }
+    g.sys_part.swap(new_part);
+    g.sys_stencil.swap(new_stencil);
+  }
+}
+
 }  // namespace vk

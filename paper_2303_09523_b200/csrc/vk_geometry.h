@@ -64,4 +64,13 @@ struct Geometry {
 std::string build_geometry(int H, int W, int T, const int* known_z, int K, int S,
                            int part_len, int drift, Geometry* g);
 
+// Orders each part's systems so that the solved ones come first and marks
+// the z-mirror / x<->y-transpose images of a solved system of the same part:
+// der_src[i] = index of the solved system (-1: solved), der_flags[i] = bit 0
+// mirror (planes reversed), bit 1 transpose (in-plane taps), bits 8.. planes
+// of the pattern; sys_canon[s] = end of part s's solved systems (-1 for a
+// part without systems).  Reorders g->sys_part / g->sys_stencil.
+void canonical_systems(Geometry* g, std::vector<int>* sys_canon, std::vector<int32_t>* der_src,
+                       std::vector<int32_t>* der_flags, int* n_derived);
+
 }  // namespace vk

@@ -96,3 +96,36 @@ int vkh_geometry(int H, int W, int T, const int* known_z, int K, int S, int drif
 }
 
 }
+
+extern "C" {
+
+// Orbit reduction of the stencil systems (vk_geometry.cpp canonical_systems).
+// n_out[0] = systems, n_out[1] = derived; sys[n*4] = (part, pattern, ky, kx)
+// in the reordered list; src[n], flags[n]; canon[S]; pat_off[NP*8] (pad 99).
+int vkh_orbits(int H, int W, int T, const int* known_z, int K, int S, int drift, int32_t* n_out,
+               int32_t* sys, int32_t* src, int32_t* flags, int32_t* canon, int32_t* pat_off) {
+  vk::Geometry g;
+  if (!vk::build_geometry(H, W, T, known_z, K, S, 0, drift, &g).empty()) return 1;
+  std::vector<int> sc;
+  std::vector<int32_t> ds, df;
+  int nd = 0;
+  vk::canonical_systems(&g, &sc, &ds, &df, &nd);
+  const int n = (int)g.sys_part.size();
+  n_out[0] = n;
+  n_out[1] = nd;
+  for (int i = 0; i < n; ++i) {
+    const vk::StencilGeom& sg = g.stencils[g.sys_stencil[i]];
+    sys[i * 4 + 0] = g.sys_part[i];
+    sys[i * 4 + 1] = sg.pattern;
+    sys[i * 4 + 2] = sg.ky;
+    sys[i * 4 + 3] = sg.kx;
+    src[i] = ds[i];
+    flags[i] = df[i];
+  }
+  for (int s2 = 0; s2 < g.S; ++s2) canon[s2] = sc[s2];
+  for (size_t p = 0; p < g.patterns.size(); ++p)
+    for (int k = 0; k < 8; ++k) pat_off[p * 8 + k] = k < (int)g.patterns[p].size() ? g.patterns[p][k] : 99;
+  return 0;
+}
+
+}

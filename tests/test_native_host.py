@@ -148,3 +148,70 @@ def test_geometry_errors(shim):
     assert rc == 1 and err.startswith("NoKnownNeighbors")
     rc, err, *_ = _geometry(shim, 8, 8, (np.array([3, 2]), 5))
     assert rc == 1 and err.startswith("Invalid")
+
+
+@pytest.mark.parametrize("H,W,f,K,S", [(24, 40, 8, 3, 1), (20, 36, 4, 9, 2), (16, 16, 2, 7, 3)])
+@pytest.mark.parametrize("drift", [0, 1])
+def test_orbit_derived_systems(shim, H, W, f, K, S, drift):
+    """Only one system per z-mirror / x<->y-transpose orbit is solved
+    (vk_geometry.cpp canonical_systems); every derived system, rebuilt from
+    its source's oracle solution by reversing planes / transposing taps, must
+    equal the oracle's direct solve of its own stencil (kriging.py:159-245),
+    and each part lists its solved systems first."""
+    kz = np.arange(K, dtype=np.int32) * f
+    T = int(kz[-1]) + 1
+    nmax = T * 8 * 64
+    n_out = np.zeros(2, np.int32)
+    sys_ = np.zeros(nmax * 4, np.int32)
+    src = np.zeros(nmax, np.int32)
+    fl = np.zeros(nmax, np.int32)
+    canon = np.zeros(S, np.int32)
+    po = np.zeros(T * 8 * 8, np.int32)
+    assert shim.vkh_orbits(H, W, T, kz.ctypes.data_as(I32), K, S, drift, n_out.ctypes.data_as(I32),
+                           sys_.ctypes.data_as(I32), src.ctypes.data_as(I32), fl.ctypes.data_as(I32),
+                           canon.ctypes.data_as(I32), po.ctypes.data_as(I32)) == 0
+    n, nd = int(n_out[0]), int(n_out[1])
+    sys_ = sys_[:n * 4].reshape(n, 4)
+    src, fl = src[:n], fl[:n]
+    po = po.reshape(-1, 8)
+    assert nd == int((src >= 0).sum()) and nd > 0
+    if f == 8 and S == 1:
+        assert n == 112 and n - nd == 40            # 7 patterns x 16 kinds -> 4 x 10
+    m = O.Model("exponential", 2.0, 700.0, 9.0)
+    dr = "linear" if drift == 1 else "constant"
+    solved = {}
+
+    def solve(i):
+        if i not in solved:
+            _, p, ky, kx = sys_[i]
+            offs = [o for o in po[p] if o != 99]
+            rel, slots = [], []
+            for pl, dz in enumerate(offs):
+                for oy in range(ky // 3 - 1, ky % 3 + 1):
+                    for ox in range(kx // 3 - 1, kx % 3 + 1):
+                        rel.append((ox, oy, dz))
+                        slots.append(pl * 16 + (oy + 1) * 4 + (ox + 1))
+            w, v = O.stencil_weights(np.array(rel, float), m, dr)
+            pad = np.zeros(128)
+            pad[slots] = w
+            solved[i] = (pad, v, len(offs))
+        return solved[i]
+
+    begin = 0
+    for s in range(S):
+        end = begin + int((sys_[:, 0] == s).sum())
+        assert np.all(src[begin:canon[s]] < 0) and np.all(src[canon[s]:end] >= 0)
+        begin = end
+    for i in np.nonzero(src >= 0)[0]:
+        j = int(src[i])
+        assert src[j] < 0 and sys_[j, 0] == sys_[i, 0]
+        wj, vj, npl = solve(j)
+        wi, vi, _ = solve(int(i))
+        assert fl[i] >> 8 == npl
+        d = wj.reshape(8, 4, 4)
+        if fl[i] & 1:
+            d = np.concatenate([d[:npl][::-1], d[npl:]])
+        if fl[i] & 2:
+            d = d.transpose(0, 2, 1)
+        assert np.abs(d.reshape(-1) - wi).max() <= 1e-9 * max(1.0, np.abs(wi).max()), (i, j, fl[i])
+        assert abs(vi - vj) <= 1e-9 * m.sill
