@@ -244,6 +244,20 @@ int vk_decode_samples(const void* raw, int32_t sample_type, int64_t n, float* ou
 int vk_normalize_stack(const void* raw, int32_t sample_type, int64_t n, float* out, int32_t* minmax,
                        void* stream);
 
+/* Multi-GPU Z-sub-part sharding: an NCCL communicator per rank
+ * (NCCL is loaded at run time; VK_E_UNSUPPORTED when it is absent), the
+ * one-known-plane halo exchange -- rank r sends `first_plane` (n floats) to
+ * r - 1 and receives rank r + 1's first plane into `halo` (ranks below the
+ * last) -- and the gather of every rank's core planes on rank 0 (`out`
+ * holds sum(counts) floats there; counts[r] floats from rank r, in rank
+ * order).  Grouped point-to-point transfers on `stream`, asynchronous.
+ * `id` is 128 bytes (vk_comm_unique_id on one rank, broadcast by the host). */
+int vk_comm_unique_id(unsigned char* id);
+int vk_comm_create(const unsigned char* id, int32_t world, int32_t rank, void** comm);
+int vk_comm_destroy(void* comm);
+int vk_halo_exchange(void* comm, const float* first_plane, float* halo, int64_t n, void* stream);
+int vk_gather_core(void* comm, const float* core, const int64_t* counts, float* out, void* stream);
+
 const char* vk_status_string(int status);
 /* Message of the last failing call on this thread (for exceptions). */
 const char* vk_last_error(void);

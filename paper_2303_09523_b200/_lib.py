@@ -77,6 +77,11 @@ SIGNATURES = {
                                C.c_void_p]),
     "vk_gather_planes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
                                    C.c_void_p, C.c_void_p]),
+    "vk_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "vk_comm_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "vk_comm_destroy": (C.c_int, [C.c_void_p]),
+    "vk_halo_exchange": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "vk_gather_core": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vk_fill_generic": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                   C.c_int32, C.c_int32, C.c_void_p, C.c_double, C.c_double,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

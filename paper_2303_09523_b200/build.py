@@ -32,6 +32,7 @@ UNITS = {
     "vk_generic.cu": [],
     "vk_volio.cu": [],
     "vk_geometry.cpp": [],
+    "vk_comm.cpp": [],
 }
 
 
@@ -60,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", str(INCLUDE), "-I", str(CSRC), *extra, *exp, "-c", str(src),
                "-o", str(obj)]
-        if unit.endswith(".cpp"):
+        if unit.endswith(".cpp") and unit != "vk_comm.cpp":
             cmd.insert(1, "-x")
             cmd.insert(2, "cu")
         if verbose:
@@ -69,7 +70,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if force or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs),
-               "-cudart", "static"]
+               "-cudart", "static", "-ldl"]
         subprocess.run(cmd, check=True)
         os.replace(tmp, LIB)
     return LIB

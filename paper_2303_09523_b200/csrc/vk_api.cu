@@ -62,6 +62,11 @@ int status_from_part(int ps) {
 
 }  // namespace
 
+namespace vk {
+// error reporting for the other translation units of the C ABI (vk_comm.cpp)
+int comm_set_err(int status, const std::string& msg) { return set_err(status, msg); }
+}  // namespace vk
+
 struct vk_plan {
   vk_plan_desc desc;
   Geometry geo;

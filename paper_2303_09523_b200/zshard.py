@@ -99,6 +99,73 @@ def gather_volume(core, rank: int, world: int, group=None):
     return None
 
 
+class NativeComm:
+    """The C ABI's NCCL communicator (``vk_comm_*``): the halo exchange and
+    the gather of core planes as grouped send / receive on a CUDA stream,
+    without torch.distributed on the data path.  Rank 0 creates the unique
+    id; with more than one rank it is broadcast over ``group``
+    (torch.distributed, any backend)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import ctypes as C
+        from . import _lib
+        from .errors import raise_for_status
+        self._lib, self._raise = _lib.load(), raise_for_status
+        self.rank, self.world = int(rank), int(world)
+        idb = (C.c_ubyte * 128)()
+        if self.rank == 0:
+            self._raise(self._lib.vk_comm_unique_id(idb))
+        if self.world > 1:
+            import torch.distributed as dist
+            box = [bytes(idb)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            C.memmove(idb, box[0], 128)
+        h = C.c_void_p()
+        self._raise(self._lib.vk_comm_create(idb, self.world, self.rank, C.byref(h)))
+        self._h = h
+
+    def _stream(self, stream):
+        import torch
+        return (stream or torch.cuda.current_stream()).cuda_stream
+
+    def halo(self, first_plane, out=None, stream=None):
+        """Send ``first_plane`` to rank - 1; receive rank + 1's into ``out``
+        (allocated when None) on ranks below the last; returns it or None."""
+        import torch
+        first_plane = first_plane.contiguous()
+        if self.rank < self.world - 1 and out is None:
+            out = torch.empty_like(first_plane)
+        self._raise(self._lib.vk_halo_exchange(
+            self._h, first_plane.data_ptr(), out.data_ptr() if out is not None else None,
+            first_plane.numel(), self._stream(stream)))
+        return out if self.rank < self.world - 1 else None
+
+    def gather(self, core, counts, stream=None):
+        """Rank 0: every rank's ``core`` (counts[r] floats) concatenated in
+        rank order; other ranks send theirs and get None."""
+        import ctypes as C
+        import torch
+        core = core.contiguous()
+        cnt = (C.c_int64 * self.world)(*[int(c) for c in counts])
+        out = torch.empty(int(sum(counts)), dtype=torch.float32, device=core.device) \
+            if self.rank == 0 else None
+        self._raise(self._lib.vk_gather_core(self._h, core.data_ptr(), cnt,
+                                             out.data_ptr() if out is not None else None,
+                                             self._stream(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.vk_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def reconstruct_sharded(owned, factor: int, shard: Shard, reconstruct=None, group=None,
                         gather: bool = True, **kw):
     """Halo exchange -> local Z-part kriging -> (optional) gather on rank 0.

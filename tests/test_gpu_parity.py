@@ -360,3 +360,22 @@ def test_orbit_derived_systems_match_direct_solves(cuda, drift):
         assert np.abs(got - ew).max() <= 1e-9 * max(1.0, np.abs(ew).max()), (s, p, ky, kx)
         assert abs(v[i] - ev) <= 1e-9 * m.sill, (s, p, ky, kx)
         assert np.all(np.delete(w[i], slots) == 0.0)
+
+
+def test_native_comm_single_rank(cuda):
+    """The C ABI's NCCL halo exchange / gather (vk_comm.cpp) on a one-rank
+    communicator: no halo on the last (only) rank, the gather returns the
+    rank's own core planes; invalid arguments report ValueError."""
+    torch = cuda
+    from paper_2303_09523_b200.zshard import NativeComm
+    comm = NativeComm(0, 1)
+    plane = torch.arange(64 * 96, dtype=torch.float32, device="cuda").reshape(64, 96)
+    assert comm.halo(plane) is None
+    core = torch.randn(3, 64, 96, device="cuda")
+    got = comm.gather(core, [core.numel()])
+    torch.cuda.synchronize()
+    assert torch.equal(got.reshape(core.shape), core)
+    import ctypes as C
+    with pytest.raises(ValueError):
+        comm._raise(comm._lib.vk_comm_create(None, 1, 0, C.byref(C.c_void_p())))
+    comm.close()
