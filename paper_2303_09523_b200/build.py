@@ -26,6 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 UNITS = {
     "vk_api.cu": [],
     "vk_variogram.cu": [],
+    "vk_npstats.cu": [],
     "vk_solve.cu": [],
     "vk_predict.cu": [],
     "vk_predict_fixed.cu": [],

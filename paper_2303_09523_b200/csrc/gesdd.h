@@ -1,0 +1,874 @@
+// numpy.linalg.svd(J_augmented, full_matrices=False) for the (M x 3)
+// augmented Jacobian of the variogram fit, restated so the device TRF
+// (trf.h) gets the reference's factors bit for bit.
+//
+// numpy 2.3.5 calls LAPACK dgesdd(jobz='S') in its bundled OpenBLAS 0.3.30
+// (LAPACK reference Fortran, built without FMA; BLAS kernels for SKYLAKEX on
+// the hosts the reference was pinned on).  For M >= 5 rows and N = 3 columns
+// dgesdd takes its "M much larger than N" path 3:
+//   dgeqrf -> dgeqr2          A = Q R (Householder, dlarfg / dlarf)
+//   dorgqr -> dorg2r          Q explicitly
+//   dgebrd -> dgebd2          R = Q_B B P^T (B upper bidiagonal)
+//   dbdsdc('U','I') -> dlasdq -> dbdsqr   B = U_B S V_B^T (implicit QR)
+//   dormbr('Q','L','N'), dormbr('P','R','T')   U_R = Q_B U_B, V^T = V_B^T P^T
+//   dgemm                     U = Q U_R
+// (checked here: composing those exported routines reproduces numpy.linalg.svd
+// bit for bit).  Each routine below follows the published LAPACK algorithm;
+// the BLAS calls inside them follow the SKYLAKEX kernels' operation order:
+// dnrm2 accumulates squares in x87 80-bit registers (four accumulators, then
+// fsqrt and one rounding to double) -- emulated exactly with 64-bit integer
+// significands; dgemv_t / dgemv_n / daxpy (dger) / drot / dgemm as noted at
+// each function.  Storage is column-major (Fortran), 0-based.
+#pragma once
+#include <cstdint>
+#include <cmath>
+#include "vk_common.h"
+#include "npref.h"
+
+namespace vk {
+namespace lapack {
+
+using np::add;
+using np::sub;
+using np::mul;
+using np::div;
+using np::fma_;
+using np::sqrt_;
+
+constexpr int GMAXM = MAX_BINS + 3;
+constexpr double DL_EPS = 1.1102230246251565e-16;      // dlamch('E') = 2^-53
+constexpr double DL_SFMIN = 2.2250738585072014e-308;   // dlamch('S')
+constexpr double DL_HUGE = 1.7976931348623157e308;     // dlamch('O')
+
+VK_HD double fsign(double a, double b) { return copysign(fabs(a), b); }   // Fortran SIGN (gfortran: IEEE sign of b)
+
+// ---------------------------------------------------------------- dnrm2 (x87)
+struct Ext {            // value = m * 2^e, bit 63 of m set (m == 0: zero)
+  uint64_t m;
+  int e;
+};
+
+VK_HD int clz64(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+  return __clzll((long long)x);
+#else
+  return __builtin_clzll(x);
+#endif
+}
+
+VK_HD double u128_to_double(unsigned __int128 v) {
+  return (double)(uint64_t)(v >> 64) * 18446744073709551616.0 + (double)(uint64_t)v;
+}
+
+VK_HD int top_bit128(unsigned __int128 v) {
+  const uint64_t hi = (uint64_t)(v >> 64);
+  return hi ? 127 - clz64(hi) : 63 - clz64((uint64_t)v);
+}
+
+// v * 2^e rounded to a 64-bit significand, round to nearest even
+VK_HD Ext ext_round(unsigned __int128 v, int e) {
+  if (v == 0) return Ext{0, 0};
+  const int tb = top_bit128(v);
+  if (tb <= 63) return Ext{(uint64_t)v << (63 - tb), e - (63 - tb)};
+  const int sh = tb - 63;
+  uint64_t m = (uint64_t)(v >> sh);
+  const unsigned __int128 rem = v & ((((unsigned __int128)1) << sh) - 1);
+  const unsigned __int128 half = ((unsigned __int128)1) << (sh - 1);
+  if (rem > half || (rem == half && (m & 1))) {
+    m += 1;
+    if (m == 0) return Ext{1ull << 63, e + sh + 1};
+  }
+  return Ext{m, e + sh};
+}
+
+// fmul st(0), st(0) of a double loaded with fldl: x*x in extended precision
+VK_HD Ext ext_sq(double x) {
+  if (x == 0.0) return Ext{0, 0};
+  int ex;
+  const double fr = frexp(fabs(x), &ex);                // fr in [0.5, 1)
+  const uint64_t mx = (uint64_t)ldexp(fr, 53);          // exact 53-bit integer
+  return ext_round((unsigned __int128)mx * mx, 2 * (ex - 53));
+}
+
+// faddp of two non-negative extended values
+VK_HD Ext ext_add(Ext a, Ext b) {
+  if (a.m == 0) return b;
+  if (b.m == 0) return a;
+  if (b.e > a.e) { const Ext t = a; a = b; b = t; }
+  const int d = a.e - b.e;
+  const unsigned __int128 A = ((unsigned __int128)a.m) << 63;
+  unsigned __int128 B = ((unsigned __int128)b.m) << 63;
+  bool sticky = false;
+  if (d >= 127) {
+    sticky = true;
+    B = 0;
+  } else if (d > 0) {
+    sticky = (B & ((((unsigned __int128)1) << d) - 1)) != 0;
+    B >>= d;
+  }
+  unsigned __int128 s = A + B;
+  if (sticky) s |= 1;
+  return ext_round(s, a.e - 63);
+}
+
+// fsqrt (correctly rounded to 64 bits) then fstpl (rounded to double)
+VK_HD double ext_sqrt_to_double(Ext a) {
+  if (a.m == 0) return 0.0;
+  unsigned __int128 M;
+  int re;
+  if (((a.e % 2) + 2) % 2 == 0) { M = ((unsigned __int128)a.m) << 64; re = (a.e - 64) / 2; }
+  else { M = ((unsigned __int128)a.m) << 63; re = (a.e - 63) / 2; }
+  // r = floor(sqrt(M)) from a double estimate plus exact integer correction
+  uint64_t r = (uint64_t)sqrt(u128_to_double(M));
+  for (int it = 0; it < 4; ++it) {
+    const unsigned __int128 r2 = (unsigned __int128)r * r;
+    if (r2 > M) {
+      const double err = u128_to_double(r2 - M) / (2.0 * (double)r);
+      const uint64_t dr = (uint64_t)err + 1;
+      r -= dr;
+    } else {
+      const unsigned __int128 r12 = (unsigned __int128)(r + 1) * (r + 1);
+      if (r12 <= M) {
+        const double err = u128_to_double(M - r12) / (2.0 * (double)r);
+        r += (uint64_t)err + 1;
+      } else {
+        break;
+      }
+    }
+  }
+  while ((unsigned __int128)r * r > M) --r;
+  while ((unsigned __int128)(r + 1) * (r + 1) <= M) ++r;
+  const unsigned __int128 R = M - (unsigned __int128)r * r;
+  if (R > r) {                                           // sqrt(M) > r + 1/2
+    r += 1;
+    if (r == 0) { r = 1ull << 63; re += 1; }
+  }
+  // round the 64-bit significand to 53 bits, nearest even
+  uint64_t q = r >> 11;
+  const uint64_t rem = r & 0x7ff;
+  if (rem > 0x400 || (rem == 0x400 && (q & 1))) q += 1;
+  return ldexp((double)q, re + 11);
+}
+
+// OpenBLAS dnrm2 (interface: n == 1 -> |x|; kernel dnrm2_k SKYLAKEX, x87)
+VK_HD double dnrm2(int n, const double* x, int incx) {
+  if (n <= 0) return 0.0;
+  if (n == 1) return fabs(x[0]);
+  Ext acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  int i = 0;
+  const int n8 = n & ~7;
+  for (; i < n8; ++i) acc[i & 3] = ext_add(acc[i & 3], ext_sq(x[i * incx]));
+  for (; i < n; ++i) acc[0] = ext_add(acc[0], ext_sq(x[i * incx]));
+  const Ext t = ext_add(ext_add(ext_add(acc[2], acc[0]), acc[1]), acc[3]);
+  return ext_sqrt_to_double(t);
+}
+
+// ------------------------------------------------------------------ BLAS 1/2
+VK_HD void dscal(int n, double a, double* x, int incx) {
+  for (int i = 0; i < n; ++i) x[i * incx] = mul(x[i * incx], a);
+}
+
+// y := A^T x for an (m x n) column-major A (dgemv_t SKYLAKEX, alpha 1, beta 0)
+VK_HD void dgemv_t(int m, int n, const double* A, int lda, const double* x, double* y) {
+  const int m3 = m & 3, nb = m - m3;
+  for (int j = 0; j < n; ++j) {
+    const double* a = A + j * lda;
+    double acc = 0.0;
+    if (nb > 0) {
+      const int n4 = (n >> 2) << 2;   // columns through the 4x4 kernel (n >= 4 only)
+      const bool k4x1 = (j >= n4) && ((n & 3) & 1) && (j == n - 1);
+      if (!k4x1) {                                       // dgemv_kernel_4x2 (and 4x4)
+        double e = 0.0, o = 0.0;
+        for (int i = 0; i < nb; i += 2) {
+          e = add(e, mul(a[i], x[i]));
+          o = add(o, mul(a[i + 1], x[i + 1]));
+        }
+        acc = add(e, o);
+      } else {                                           // dgemv_kernel_4x1
+        double l0 = 0.0, l1 = 0.0, l2 = 0.0, l3 = 0.0;
+        for (int i = 0; i < nb; i += 4) {
+          l0 = add(l0, mul(a[i], x[i]));
+          l1 = add(l1, mul(a[i + 1], x[i + 1]));
+          l2 = add(l2, mul(a[i + 2], x[i + 2]));
+          l3 = add(l3, mul(a[i + 3], x[i + 3]));
+        }
+        acc = add(add(l0, l2), add(l1, l3));
+      }
+    }
+    const double* at = a + nb;
+    const double* xt = x + nb;
+    if (m3 == 3) acc = add(acc, fma_(at[2], xt[2], fma_(at[0], xt[0], mul(at[1], xt[1]))));
+    if (m3 == 2) acc = add(acc, fma_(at[0], xt[0], mul(at[1], xt[1])));
+    if (m3 == 1) acc = fma_(at[0], xt[0], acc);
+    y[j] = acc;
+  }
+}
+
+// y := A x for an (m x n) column-major A, m <= 3 rows (dgemv_n SKYLAKEX
+// row-tail paths, alpha 1, beta 0): the unrolled pair form when lda == 3 and
+// incx == 1, else one FMA per column.
+VK_HD void dgemv_n(int m, int n, const double* A, int lda, const double* x, int incx, double* y) {
+  for (int i = 0; i < m; ++i) {
+    double acc = 0.0;
+    if (m == 3 && lda == 3 && incx == 1) {
+      int k = 0;
+      for (; k + 4 <= n; k += 4) {
+        acc = add(acc, fma_(A[i + k * lda], x[k], mul(A[i + (k + 1) * lda], x[k + 1])));
+        acc = add(acc, fma_(A[i + (k + 2) * lda], x[k + 2], mul(A[i + (k + 3) * lda], x[k + 3])));
+      }
+      for (; k < n; ++k) acc = fma_(A[i + k * lda], x[k], acc);
+    } else {
+      for (int k = 0; k < n; ++k) acc = fma_(A[i + k * lda], x[k * incx], acc);
+    }
+    y[i] = acc;
+  }
+}
+
+// A += alpha x y^T (dger: per column daxpy with y0 = alpha*y[j], FMA update)
+VK_HD void dger(int m, int n, double alpha, const double* x, const double* y, int incy,
+                double* A, int lda) {
+  for (int j = 0; j < n; ++j) {
+    const double y0 = mul(alpha, y[j * incy]);
+    for (int i = 0; i < m; ++i) A[i + j * lda] = fma_(y0, x[i], A[i + j * lda]);
+  }
+}
+
+// drot SKYLAKEX: x' = c x + s y, y' = c y - s x
+VK_HD void drot(int n, double* x, int incx, double* y, int incy, double c, double s) {
+  for (int i = 0; i < n; ++i) {
+    const double xi = x[i * incx], yi = y[i * incy];
+    x[i * incx] = fma_(c, xi, mul(s, yi));
+    y[i * incy] = fma_(c, yi, -mul(s, xi));
+  }
+}
+
+VK_HD void dswap(int n, double* x, int incx, double* y, int incy) {
+  for (int i = 0; i < n; ++i) {
+    const double t = x[i * incx];
+    x[i * incx] = y[i * incy];
+    y[i * incy] = t;
+  }
+}
+
+// ------------------------------------------------------------------- LAPACK
+VK_HD double dlapy2(double x, double y) {
+  if (x != x) return x;
+  if (y != y) return y;
+  const double xa = fabs(x), ya = fabs(y);
+  const double w = fmax(xa, ya), z = fmin(xa, ya);
+  if (z == 0.0 || w > DL_HUGE) return w;
+  const double q = div(z, w);
+  return mul(w, sqrt_(add(1.0, mul(q, q))));
+}
+
+// dlarfg(n, alpha, x, incx, tau)
+VK_HD void dlarfg(int n, double* alpha, double* x, int incx, double* tau) {
+  if (n <= 1) { *tau = 0.0; return; }
+  double xnorm = dnrm2(n - 1, x, incx);
+  if (xnorm == 0.0) { *tau = 0.0; return; }
+  double beta = -fsign(dlapy2(*alpha, xnorm), *alpha);
+  const double safmin = DL_SFMIN / DL_EPS;
+  const double rsafmn = 1.0 / safmin;
+  int knt = 0;
+  if (fabs(beta) < safmin) {
+    do {
+      ++knt;
+      dscal(n - 1, rsafmn, x, incx);
+      beta = mul(beta, rsafmn);
+      *alpha = mul(*alpha, rsafmn);
+    } while (fabs(beta) < safmin && knt < 20);
+    xnorm = dnrm2(n - 1, x, incx);
+    beta = -fsign(dlapy2(*alpha, xnorm), *alpha);
+  }
+  *tau = div(sub(beta, *alpha), beta);
+  dscal(n - 1, div(1.0, sub(*alpha, beta)), x, incx);
+  for (int j = 0; j < knt; ++j) beta = mul(beta, safmin);
+  *alpha = beta;
+}
+
+// dlarf(side, m, n, v, incv, tau, C, ldc)
+VK_HD void dlarf(bool left, int m, int n, const double* v, int incv, double tau, double* C, int ldc) {
+  int lastv = 0, lastc = 0;
+  if (tau != 0.0) {
+    lastv = left ? m : n;
+    int i = (incv > 0) ? (lastv - 1) * incv : 0;
+    while (lastv > 0 && v[i] == 0.0) { --lastv; i -= incv; }
+    if (left) {                                           // iladlc(lastv, n, C, ldc)
+      lastc = n;
+      if (n > 0 && C[0 + (n - 1) * ldc] == 0.0 && C[(lastv - 1) + (n - 1) * ldc] == 0.0) {
+        lastc = 0;
+        for (int j = n - 1; j >= 0 && lastc == 0; --j)
+          for (int r = 0; r < lastv; ++r)
+            if (C[r + j * ldc] != 0.0) { lastc = j + 1; break; }
+      }
+    } else {                                              // iladlr(m, lastv, C, ldc)
+      lastc = m;
+      if (m > 0 && C[(m - 1) + 0] == 0.0 && C[(m - 1) + (lastv - 1) * ldc] == 0.0) {
+        lastc = 0;
+        for (int j = 0; j < lastv; ++j) {
+          int r = m;
+          while (r >= 1 && C[(r - 1) + j * ldc] == 0.0) --r;
+          if (r > lastc) lastc = r;
+        }
+      }
+    }
+  }
+  if (lastv <= 0 || lastc <= 0) return;
+  double w[GMAXM];
+  double vv[GMAXM];
+  for (int k = 0; k < lastv; ++k) vv[k] = v[k * incv];
+  if (left) {
+    dgemv_t(lastv, lastc, C, ldc, vv, w);
+    dger(lastv, lastc, -tau, vv, w, 1, C, ldc);
+  } else {
+    dgemv_n(lastc, lastv, C, ldc, v, incv, w);
+    dger(lastc, lastv, -tau, w, vv, 1, C, ldc);
+  }
+}
+
+// dgeqr2(m, n, A, lda, tau), n = 3
+VK_HD void dgeqr2(int m, int n, double* A, int lda, double* tau) {
+  const int k = m < n ? m : n;
+  for (int i = 0; i < k; ++i) {
+    dlarfg(m - i, &A[i + i * lda], &A[(i + 1 < m ? i + 1 : m - 1) + i * lda], 1, &tau[i]);
+    if (i < n - 1) {
+      const double aii = A[i + i * lda];
+      A[i + i * lda] = 1.0;
+      dlarf(true, m - i, n - i - 1, &A[i + i * lda], 1, tau[i], &A[i + (i + 1) * lda], lda);
+      A[i + i * lda] = aii;
+    }
+  }
+}
+
+// dorg2r(m, n, k, A, lda, tau), k = n
+VK_HD void dorg2r(int m, int n, int k, double* A, int lda, const double* tau) {
+  for (int i = k - 1; i >= 0; --i) {
+    if (i < n - 1) {
+      A[i + i * lda] = 1.0;
+      dlarf(true, m - i, n - i - 1, &A[i + i * lda], 1, tau[i], &A[i + (i + 1) * lda], lda);
+    }
+    if (i < m - 1) dscal(m - i - 1, -tau[i], &A[i + 1 + i * lda], 1);
+    A[i + i * lda] = sub(1.0, tau[i]);
+    for (int l = 0; l < i; ++l) A[l + i * lda] = 0.0;
+  }
+}
+
+// dgebd2(m, n, A, lda, d, e, tauq, taup), m >= n
+VK_HD void dgebd2(int m, int n, double* A, int lda, double* d, double* e, double* tauq, double* taup) {
+  for (int i = 0; i < n; ++i) {
+    dlarfg(m - i, &A[i + i * lda], &A[(i + 1 < m ? i + 1 : m - 1) + i * lda], 1, &tauq[i]);
+    d[i] = A[i + i * lda];
+    A[i + i * lda] = 1.0;
+    if (i < n - 1) dlarf(true, m - i, n - i - 1, &A[i + i * lda], 1, tauq[i], &A[i + (i + 1) * lda], lda);
+    A[i + i * lda] = d[i];
+    if (i < n - 1) {
+      dlarfg(n - i - 1, &A[i + (i + 1) * lda], &A[i + (i + 2 < n ? i + 2 : n - 1) * lda], lda, &taup[i]);
+      e[i] = A[i + (i + 1) * lda];
+      A[i + (i + 1) * lda] = 1.0;
+      dlarf(false, m - i - 1, n - i - 1, &A[i + (i + 1) * lda], lda, taup[i], &A[(i + 1) + (i + 1) * lda], lda);
+      A[i + (i + 1) * lda] = e[i];
+    } else {
+      taup[i] = 0.0;
+    }
+  }
+}
+
+// dlartg (LAPACK 3.10+ form)
+VK_HD void dlartg(double f, double g, double* c, double* s, double* r) {
+  const double safmin = 2.2250738585072014e-308;         // 2^-1022
+  const double safmax = 4.49423283715579e+307;           // 2^1022
+  const double rtmin = 1.4916681462400413e-154;          // sqrt(safmin)
+  const double rtmax = sqrt(safmax / 2);
+  const double f1 = fabs(f), g1 = fabs(g);
+  if (g == 0.0) {
+    *c = 1.0; *s = 0.0; *r = f;
+  } else if (f == 0.0) {
+    *c = 0.0; *s = fsign(1.0, g); *r = g1;
+  } else if (f1 > rtmin && f1 < rtmax && g1 > rtmin && g1 < rtmax) {
+    const double d = sqrt_(add(mul(f, f), mul(g, g)));
+    *c = div(f1, d);
+    *r = fsign(d, f);
+    *s = div(g, *r);
+  } else {
+    const double u = fmin(safmax, fmax(safmin, fmax(f1, g1)));
+    const double fs = div(f, u), gs = div(g, u);
+    const double d = sqrt_(add(mul(fs, fs), mul(gs, gs)));
+    *c = div(fabs(fs), d);
+    *r = fsign(d, f);
+    *s = div(gs, *r);
+    *r = mul(*r, u);
+  }
+}
+
+// dlas2: singular values of [[f, g], [0, h]]
+VK_HD void dlas2(double f, double g, double h, double* ssmin, double* ssmax) {
+  const double fa = fabs(f), ga = fabs(g), ha = fabs(h);
+  const double fhmn = fmin(fa, ha), fhmx = fmax(fa, ha);
+  if (fhmn == 0.0) {
+    *ssmin = 0.0;
+    if (fhmx == 0.0) {
+      *ssmax = ga;
+    } else {
+      const double q = div(fmin(fhmx, ga), fmax(fhmx, ga));
+      *ssmax = mul(fmax(fhmx, ga), sqrt_(add(1.0, mul(q, q))));
+    }
+  } else {
+    if (ga < fhmx) {
+      const double as = add(1.0, div(fhmn, fhmx));
+      const double at = div(sub(fhmx, fhmn), fhmx);
+      const double q = div(ga, fhmx);
+      const double au = mul(q, q);
+      const double c = div(2.0, add(sqrt_(add(mul(as, as), au)), sqrt_(add(mul(at, at), au))));
+      *ssmin = mul(fhmn, c);
+      *ssmax = div(fhmx, c);
+    } else {
+      const double au = div(fhmx, ga);
+      if (au == 0.0) {
+        *ssmin = div(mul(fhmn, fhmx), ga);
+        *ssmax = ga;
+      } else {
+        const double as = add(1.0, div(fhmn, fhmx));
+        const double at = div(sub(fhmx, fhmn), fhmx);
+        const double p1 = mul(as, au), p2 = mul(at, au);
+        const double c = div(1.0, add(sqrt_(add(1.0, mul(p1, p1))), sqrt_(add(1.0, mul(p2, p2)))));
+        double smin = mul(mul(fhmn, c), au);
+        smin = add(smin, smin);
+        *ssmin = smin;
+        *ssmax = div(ga, add(c, c));
+      }
+    }
+  }
+}
+
+// dlasv2: SVD of [[f, g], [0, h]]
+VK_HD void dlasv2(double f, double g, double h, double* ssmin, double* ssmax, double* snr,
+                  double* csr, double* snl, double* csl) {
+  double ft = f, fa = fabs(ft), ht = h, ha = fabs(h);
+  int pmax = 1;
+  const bool swap = ha > fa;
+  if (swap) {
+    pmax = 3;
+    double t = ft; ft = ht; ht = t;
+    t = fa; fa = ha; ha = t;
+  }
+  const double gt = g, ga = fabs(gt);
+  double clt, crt, slt, srt, smin, smax;
+  if (ga == 0.0) {
+    smin = ha; smax = fa;
+    clt = 1.0; crt = 1.0; slt = 0.0; srt = 0.0;
+  } else {
+    bool gasmal = true;
+    if (ga > fa) {
+      pmax = 2;
+      if (div(fa, ga) < DL_EPS) {
+        gasmal = false;
+        smax = ga;
+        if (ha > 1.0) smin = div(fa, div(ga, ha));
+        else smin = mul(div(fa, ga), ha);
+        clt = 1.0;
+        slt = div(ht, gt);
+        srt = 1.0;
+        crt = div(ft, gt);
+      }
+    }
+    if (gasmal) {
+      const double d = sub(fa, ha);
+      double l = (d == fa) ? 1.0 : div(d, fa);
+      const double m = div(gt, ft);
+      double t = sub(2.0, l);
+      const double mm = mul(m, m), tt = mul(t, t);
+      const double s = sqrt_(add(tt, mm));
+      const double r = (l == 0.0) ? fabs(m) : sqrt_(add(mul(l, l), mm));
+      const double a = mul(0.5, add(s, r));
+      smin = div(ha, a);
+      smax = mul(fa, a);
+      if (mm == 0.0) {
+        if (l == 0.0) t = mul(fsign(2.0, ft), fsign(1.0, gt));
+        else t = add(div(gt, fsign(d, ft)), div(m, t));
+      } else {
+        t = mul(add(div(m, add(s, t)), div(m, add(r, l))), add(1.0, a));
+      }
+      l = sqrt_(add(mul(t, t), 4.0));
+      crt = div(2.0, l);
+      srt = div(t, l);
+      clt = div(add(crt, mul(srt, m)), a);
+      slt = div(mul(div(ht, ft), srt), a);
+    }
+  }
+  if (swap) { *csl = srt; *snl = crt; *csr = slt; *snr = clt; }
+  else { *csl = clt; *snl = slt; *csr = crt; *snr = srt; }
+  double tsign = 1.0;
+  if (pmax == 1) tsign = mul(mul(fsign(1.0, *csr), fsign(1.0, *csl)), fsign(1.0, f));
+  if (pmax == 2) tsign = mul(mul(fsign(1.0, *snr), fsign(1.0, *csl)), fsign(1.0, g));
+  if (pmax == 3) tsign = mul(mul(fsign(1.0, *snr), fsign(1.0, *snl)), fsign(1.0, h));
+  *ssmax = fsign(smax, tsign);
+  *ssmin = fsign(smin, mul(mul(tsign, fsign(1.0, f)), fsign(1.0, h)));
+}
+
+// dlasr(side, 'V', direct, m, n, c, s, A, lda)
+VK_HD void dlasr(bool left, bool forward, int m, int n, const double* c, const double* s, double* A, int lda) {
+  if (left) {
+    for (int jj = 0; jj < m - 1; ++jj) {
+      const int j = forward ? jj : m - 2 - jj;
+      const double ct = c[j], st = s[j];
+      if (ct != 1.0 || st != 0.0) {
+        for (int i = 0; i < n; ++i) {
+          const double temp = A[(j + 1) + i * lda];
+          A[(j + 1) + i * lda] = sub(mul(ct, temp), mul(st, A[j + i * lda]));
+          A[j + i * lda] = add(mul(st, temp), mul(ct, A[j + i * lda]));
+        }
+      }
+    }
+  } else {
+    for (int jj = 0; jj < n - 1; ++jj) {
+      const int j = forward ? jj : n - 2 - jj;
+      const double ct = c[j], st = s[j];
+      if (ct != 1.0 || st != 0.0) {
+        for (int i = 0; i < m; ++i) {
+          const double temp = A[i + (j + 1) * lda];
+          A[i + (j + 1) * lda] = sub(mul(ct, temp), mul(st, A[i + j * lda]));
+          A[i + j * lda] = add(mul(st, temp), mul(ct, A[i + j * lda]));
+        }
+      }
+    }
+  }
+}
+
+// dbdsqr('U', n, ncvt = n, nru = n, ncc = 0, d, e, VT, ldvt, U, ldu); n <= 3.
+// Returns info (0 on convergence).
+VK_HD int dbdsqr(int n, double* d, double* e, double* VT, int ldvt, double* U, int ldu) {
+  const int ncvt = n, nru = n;
+  const double eps = DL_EPS, unfl = DL_SFMIN;
+  const int maxitr = 6;
+  if (n == 0) return 0;
+  if (n > 1) {
+    const int nm1 = n - 1, nm12 = nm1 + nm1, nm13 = nm12 + nm1;
+    double work[4 * 3];
+    int idir = 0;
+    const double tolmul = 0x1.8ace5422aa0dbp+6;           // max(10, min(100, eps**(-1/8))), glibc pow
+    const double tol = mul(tolmul, eps);
+    double smax = 0.0;
+    for (int i = 0; i < n; ++i) smax = fmax(smax, fabs(d[i]));
+    for (int i = 0; i < n - 1; ++i) smax = fmax(smax, fabs(e[i]));
+    double smin = 0.0, thresh;
+    {
+      double sminoa = fabs(d[0]);
+      if (sminoa != 0.0) {
+        double mu = sminoa;
+        for (int i = 1; i < n; ++i) {
+          mu = mul(fabs(d[i]), div(mu, add(mu, fabs(e[i - 1]))));
+          sminoa = fmin(sminoa, mu);
+          if (sminoa == 0.0) break;
+        }
+      }
+      sminoa = div(sminoa, sqrt_((double)n));
+      thresh = fmax(mul(tol, sminoa), mul((double)maxitr, mul((double)n, mul((double)n, unfl))));
+    }
+    const int maxitdivn = maxitr * n;
+    int iterdivn = 0, iter = -1, oldll = -1, oldm = -1;
+    int M = n;                                             // 1-based index of last unconverged
+    // 1-based accessors
+#define D_(i) d[(i) - 1]
+#define E_(i) e[(i) - 1]
+    while (true) {
+      if (M <= 1) break;
+      if (iter >= n) {
+        iter -= n;
+        ++iterdivn;
+        if (iterdivn >= maxitdivn) return 1;
+      }
+      // find diagonal block to work on
+      smax = fabs(D_(M));
+      int ll = 0;
+      bool split = false;
+      for (int lll = 1; lll <= M - 1; ++lll) {
+        ll = M - lll;
+        const double abss = fabs(D_(ll)), abse = fabs(E_(ll));
+        if (abse <= thresh) { split = true; break; }
+        smax = fmax(smax, fmax(abss, abse));
+      }
+      if (split) {
+        E_(ll) = 0.0;
+        if (ll == M - 1) { M -= 1; continue; }
+      } else {
+        ll = 0;
+      }
+      ll += 1;
+      if (ll == M - 1) {
+        double sigmn, sigmx, sinr, cosr, sinl, cosl;
+        dlasv2(D_(M - 1), E_(M - 1), D_(M), &sigmn, &sigmx, &sinr, &cosr, &sinl, &cosl);
+        D_(M - 1) = sigmx;
+        E_(M - 1) = 0.0;
+        D_(M) = sigmn;
+        drot(ncvt, &VT[(M - 2)], ldvt, &VT[(M - 1)], ldvt, cosr, sinr);
+        drot(nru, &U[(M - 2) * ldu], 1, &U[(M - 1) * ldu], 1, cosl, sinl);
+        M -= 2;
+        continue;
+      }
+      if (ll > oldm || M < oldll) {
+        if (fabs(D_(ll)) >= fabs(D_(M))) idir = 1;
+        else idir = 2;
+      }
+      bool restart = false;
+      if (idir == 1) {
+        if (fabs(E_(M - 1)) <= mul(fabs(tol), fabs(D_(M)))) { E_(M - 1) = 0.0; continue; }
+        double mu = fabs(D_(ll));
+        smin = mu;
+        for (int lll = ll; lll <= M - 1; ++lll) {
+          if (fabs(E_(lll)) <= mul(tol, mu)) { E_(lll) = 0.0; restart = true; break; }
+          mu = mul(fabs(D_(lll + 1)), div(mu, add(mu, fabs(E_(lll)))));
+          smin = fmin(smin, mu);
+        }
+      } else {
+        if (fabs(E_(ll)) <= mul(fabs(tol), fabs(D_(ll)))) { E_(ll) = 0.0; continue; }
+        double mu = fabs(D_(M));
+        smin = mu;
+        for (int lll = M - 1; lll >= ll; --lll) {
+          if (fabs(E_(lll)) <= mul(tol, mu)) { E_(lll) = 0.0; restart = true; break; }
+          mu = mul(fabs(D_(lll)), div(mu, add(mu, fabs(E_(lll)))));
+          smin = fmin(smin, mu);
+        }
+      }
+      if (restart) continue;
+      oldll = ll;
+      oldm = M;
+      double shift, r;
+      if (mul(mul((double)n, tol), div(smin, smax)) <= fmax(eps, mul(0.01, tol))) {
+        shift = 0.0;
+      } else {
+        double sll;
+        if (idir == 1) {
+          sll = fabs(D_(ll));
+          dlas2(D_(M - 1), E_(M - 1), D_(M), &shift, &r);
+        } else {
+          sll = fabs(D_(M));
+          dlas2(D_(ll), E_(ll), D_(ll + 1), &shift, &r);
+        }
+        if (sll > 0.0) {
+          const double q = div(shift, sll);
+          if (mul(q, q) < eps) shift = 0.0;
+        }
+      }
+      iter += M - ll;
+      if (shift == 0.0) {
+        if (idir == 1) {
+          double cs = 1.0, oldcs = 1.0, sn = 0.0, oldsn = 0.0;
+          for (int i = ll; i <= M - 1; ++i) {
+            dlartg(mul(D_(i), cs), E_(i), &cs, &sn, &r);
+            if (i > ll) E_(i - 1) = mul(oldsn, r);
+            dlartg(mul(oldcs, r), mul(D_(i + 1), sn), &oldcs, &oldsn, &D_(i));
+            work[i - ll] = cs;
+            work[i - ll + nm1] = sn;
+            work[i - ll + nm12] = oldcs;
+            work[i - ll + nm13] = oldsn;
+          }
+          const double hh = mul(D_(M), cs);
+          D_(M) = mul(hh, oldcs);
+          E_(M - 1) = mul(hh, oldsn);
+          dlasr(true, true, M - ll + 1, ncvt, &work[0], &work[n - 1], &VT[(ll - 1)], ldvt);
+          dlasr(false, true, nru, M - ll + 1, &work[nm12], &work[nm13], &U[(ll - 1) * ldu], ldu);
+          if (fabs(E_(M - 1)) <= thresh) E_(M - 1) = 0.0;
+        } else {
+          double cs = 1.0, oldcs = 1.0, sn = 0.0, oldsn = 0.0;
+          for (int i = M; i >= ll + 1; --i) {
+            dlartg(mul(D_(i), cs), E_(i - 1), &cs, &sn, &r);
+            if (i < M) E_(i) = mul(oldsn, r);
+            dlartg(mul(oldcs, r), mul(D_(i - 1), sn), &oldcs, &oldsn, &D_(i));
+            work[i - ll - 1] = cs;
+            work[i - ll - 1 + nm1] = -sn;
+            work[i - ll - 1 + nm12] = oldcs;
+            work[i - ll - 1 + nm13] = -oldsn;
+          }
+          const double hh = mul(D_(ll), cs);
+          D_(ll) = mul(hh, oldcs);
+          E_(ll) = mul(hh, oldsn);
+          dlasr(true, false, M - ll + 1, ncvt, &work[nm12], &work[nm13], &VT[(ll - 1)], ldvt);
+          dlasr(false, false, nru, M - ll + 1, &work[0], &work[n - 1], &U[(ll - 1) * ldu], ldu);
+          if (fabs(E_(ll)) <= thresh) E_(ll) = 0.0;
+        }
+      } else {
+        if (idir == 1) {
+          double f = mul(sub(fabs(D_(ll)), shift), add(fsign(1.0, D_(ll)), div(shift, D_(ll))));
+          double g = E_(ll);
+          double cosr, sinr, cosl, sinl;
+          for (int i = ll; i <= M - 1; ++i) {
+            dlartg(f, g, &cosr, &sinr, &r);
+            if (i > ll) E_(i - 1) = r;
+            f = add(mul(cosr, D_(i)), mul(sinr, E_(i)));
+            E_(i) = sub(mul(cosr, E_(i)), mul(sinr, D_(i)));
+            g = mul(sinr, D_(i + 1));
+            D_(i + 1) = mul(cosr, D_(i + 1));
+            dlartg(f, g, &cosl, &sinl, &r);
+            D_(i) = r;
+            f = add(mul(cosl, E_(i)), mul(sinl, D_(i + 1)));
+            D_(i + 1) = sub(mul(cosl, D_(i + 1)), mul(sinl, E_(i)));
+            if (i < M - 1) {
+              g = mul(sinl, E_(i + 1));
+              E_(i + 1) = mul(cosl, E_(i + 1));
+            }
+            work[i - ll] = cosr;
+            work[i - ll + nm1] = sinr;
+            work[i - ll + nm12] = cosl;
+            work[i - ll + nm13] = sinl;
+          }
+          E_(M - 1) = f;
+          dlasr(true, true, M - ll + 1, ncvt, &work[0], &work[n - 1], &VT[(ll - 1)], ldvt);
+          dlasr(false, true, nru, M - ll + 1, &work[nm12], &work[nm13], &U[(ll - 1) * ldu], ldu);
+          if (fabs(E_(M - 1)) <= thresh) E_(M - 1) = 0.0;
+        } else {
+          double f = mul(sub(fabs(D_(M)), shift), add(fsign(1.0, D_(M)), div(shift, D_(M))));
+          double g = E_(M - 1);
+          double cosr, sinr, cosl, sinl;
+          for (int i = M; i >= ll + 1; --i) {
+            dlartg(f, g, &cosr, &sinr, &r);
+            if (i < M) E_(i) = r;
+            f = add(mul(cosr, D_(i)), mul(sinr, E_(i - 1)));
+            E_(i - 1) = sub(mul(cosr, E_(i - 1)), mul(sinr, D_(i)));
+            g = mul(sinr, D_(i - 1));
+            D_(i - 1) = mul(cosr, D_(i - 1));
+            dlartg(f, g, &cosl, &sinl, &r);
+            D_(i) = r;
+            f = add(mul(cosl, E_(i - 1)), mul(sinl, D_(i - 1)));
+            D_(i - 1) = sub(mul(cosl, D_(i - 1)), mul(sinl, E_(i - 1)));
+            if (i > ll + 1) {
+              g = mul(sinl, E_(i - 2));
+              E_(i - 2) = mul(cosl, E_(i - 2));
+            }
+            work[i - ll - 1] = cosr;
+            work[i - ll - 1 + nm1] = -sinr;
+            work[i - ll - 1 + nm12] = cosl;
+            work[i - ll - 1 + nm13] = -sinl;
+          }
+          E_(ll) = f;
+          if (fabs(E_(ll)) <= thresh) E_(ll) = 0.0;
+          dlasr(true, false, M - ll + 1, ncvt, &work[nm12], &work[nm13], &VT[(ll - 1)], ldvt);
+          dlasr(false, false, nru, M - ll + 1, &work[0], &work[n - 1], &U[(ll - 1) * ldu], ldu);
+        }
+      }
+    }
+#undef D_
+#undef E_
+  }
+  // make singular values positive
+  for (int i = 0; i < n; ++i) {
+    if (d[i] < 0.0) {
+      d[i] = -d[i];
+      dscal(ncvt, -1.0, &VT[i], ldvt);
+    }
+  }
+  // sort into decreasing order
+  for (int i = 1; i <= n - 1; ++i) {
+    int isub = 1;
+    double smin = d[0];
+    for (int j = 2; j <= n + 1 - i; ++j) {
+      if (d[j - 1] <= smin) { isub = j; smin = d[j - 1]; }
+    }
+    if (isub != n + 1 - i) {
+      d[isub - 1] = d[n - i];
+      d[n - i] = smin;
+      dswap(ncvt, &VT[isub - 1], ldvt, &VT[n - i], ldvt);
+      dswap(nru, &U[(isub - 1) * ldu], 1, &U[(n - i) * ldu], 1);
+    }
+  }
+  return 0;
+}
+
+// dbdsdc('U', 'I', n): identity U, VT, then dlasdq -> dbdsqr, then the
+// selection sort of dlasdq / dbdsdc (no-ops on dbdsqr's sorted output unless
+// values tie, which the same code then resolves identically).
+VK_HD int dbdsdc(int n, double* d, double* e, double* U, int ldu, double* VT, int ldvt) {
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      U[i + j * ldu] = (i == j) ? 1.0 : 0.0;
+      VT[i + j * ldvt] = (i == j) ? 1.0 : 0.0;
+    }
+  const int info = dbdsqr(n, d, e, VT, ldvt, U, ldu);
+  if (info) return info;
+  // dlasdq sort (ascending scan, swap to the end)
+  for (int i = 1; i <= n; ++i) {
+    int isub = i;
+    double smin = d[i - 1];
+    for (int j = i + 1; j <= n; ++j)
+      if (d[j - 1] < smin) { isub = j; smin = d[j - 1]; }
+    if (isub != n + 1 - i) {
+      d[isub - 1] = d[n - i];
+      d[n - i] = smin;
+      dswap(n, &VT[isub - 1], ldvt, &VT[n - i], ldvt);
+      dswap(n, &U[(isub - 1) * ldu], 1, &U[(n - i) * ldu], 1);
+    }
+  }
+  // dbdsdc selection sort into decreasing order
+  for (int ii = 2; ii <= n; ++ii) {
+    const int i = ii - 1;
+    int kk = i;
+    double p = d[i - 1];
+    for (int j = ii; j <= n; ++j)
+      if (d[j - 1] > p) { kk = j; p = d[j - 1]; }
+    if (kk != i) {
+      d[kk - 1] = d[i - 1];
+      d[i - 1] = p;
+      dswap(n, &U[(i - 1) * ldu], 1, &U[(kk - 1) * ldu], 1);
+      dswap(n, &VT[i - 1], ldvt, &VT[kk - 1], ldvt);
+    }
+  }
+  return 0;
+}
+
+// dorm2r('L', 'N', m, n, k, A, lda, tau, C, ldc): C := Q C
+VK_HD void dorm2r_ln(int m, int n, int k, double* A, int lda, const double* tau, double* C, int ldc) {
+  for (int i = k - 1; i >= 0; --i) {
+    const double aii = A[i + i * lda];
+    A[i + i * lda] = 1.0;
+    dlarf(true, m - i, n, &A[i + i * lda], 1, tau[i], &C[i], ldc);
+    A[i + i * lda] = aii;
+  }
+}
+
+// dorml2('R', 'N', m, n, k, A, lda, tau, C, ldc): C := C Q (Q from dgelqf rows)
+VK_HD void dorml2_rn(int m, int n, int k, double* A, int lda, const double* tau, double* C, int ldc) {
+  for (int i = k - 1; i >= 0; --i) {
+    const double aii = A[i + i * lda];
+    A[i + i * lda] = 1.0;
+    dlarf(false, m, n - i, &A[i + i * lda], lda, tau[i], &C[i * ldc], ldc);
+    A[i + i * lda] = aii;
+  }
+}
+
+// numpy.linalg.svd(A, full_matrices=False) for a row-major (M x 3) A, M >= 5.
+// Outputs U row-major (M x 3), s (3), VT row-major (3 x 3).  Returns 0 on
+// success, nonzero if dbdsqr did not converge (numpy raises LinAlgError).
+VK_HD int svd_m3(const double* A_rm, int M, double* U_rm, double* s, double* VT_rm) {
+  const int N = 3;
+  double A[GMAXM * 3];                                   // column-major, lda = M
+  for (int r = 0; r < M; ++r)
+    for (int c = 0; c < N; ++c) A[r + c * M] = A_rm[r * N + c];
+  double tau[3];
+  dgeqr2(M, N, A, M, tau);
+  double R[9];                                           // upper triangle, lda = 3
+  for (int j = 0; j < N; ++j)
+    for (int i = 0; i < N; ++i) R[i + j * N] = (i <= j) ? A[i + j * M] : 0.0;
+  dorg2r(M, N, N, A, M, tau);
+  double d[3], e[3], tauq[3], taup[3];
+  dgebd2(N, N, R, N, d, e, tauq, taup);
+  double Ub[9], VTb[9];
+  const int info = dbdsdc(N, d, e, Ub, N, VTb, N);
+  if (info) return info;
+  dorm2r_ln(N, N, N, R, N, tauq, Ub, N);                 // dormbr('Q','L','N')
+  dorml2_rn(N, N - 1, N - 1, &R[0 + 1 * N], N, taup, &VTb[0 + 1 * N], N);  // dormbr('P','R','T')
+  // dgemm('N','N', M, 3, 3, 1, Q, Ub, 0, U): one FMA chain over k per element
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N; ++j) {
+      double c = mul(A[i + 0 * M], Ub[0 + j * N]);
+      c = fma_(A[i + 1 * M], Ub[1 + j * N], c);
+      c = fma_(A[i + 2 * M], Ub[2 + j * N], c);
+      U_rm[i * N + j] = c;
+    }
+  for (int i = 0; i < N; ++i) {
+    s[i] = d[i];
+    for (int j = 0; j < N; ++j) VT_rm[i * N + j] = VTb[i + j * N];
+  }
+  return 0;
+}
+
+}  // namespace lapack
+}  // namespace vk

@@ -97,6 +97,13 @@ struct vk_plan {
   PairTable* d_tables = nullptr;
   std::vector<PairJob> jobs;          // one per pair class
   PairJob* d_jobs = nullptr;
+  // numpy-exact svar and bin sums (vk_npstats.cu)
+  std::vector<NpSumTree> trees;       // one per pair class
+  NpSumTree* d_trees = nullptr;
+  int max_leaf = 0;
+  int64_t leaf_stride = 0, node_stride = 0;
+  double *d_npleaf = nullptr, *d_npnode = nullptr, *d_mean = nullptr, *d_svar = nullptr;
+  double *d_sq = nullptr, *d_bsum = nullptr;
   bool pairs_ready = false;
   double* h_models = nullptr;        // pinned staging [S][3]
   int kernels = 0;
@@ -325,9 +332,35 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
       VK_TRY(p->alloc(&t.cnt, (size_t)ns));
       VK_TRY(p->alloc(&t.off, (size_t)ns + 1));
       VK_TRY(p->alloc(&t.hbits, (size_t)1));
+      VK_TRY(p->alloc(&t.order, (size_t)d->max_pairs));
+      VK_TRY(p->alloc(&t.boff, (size_t)MAX_BINS + 1));
       p->tables.push_back(t);
+      // numpy's pairwise-summation tree for this class's sample count
+      const NpSumTreeHost th = build_npsum_tree(g.pair_classes[c].m);
+      NpSumTree tr;
+      tr.nleaf = (int32_t)th.leaf_off.size() - 1;
+      tr.nnode = (int32_t)th.node_lr.size() / 2;
+      tr.nlevel = (int32_t)th.level.size() - 1;
+      int32_t *lo = nullptr, *lr = nullptr, *lv = nullptr;
+      VK_TRY(p->put(&lo, th.leaf_off));
+      VK_TRY(p->put(&lr, th.node_lr.empty() ? std::vector<int32_t>{0, 0} : th.node_lr));
+      VK_TRY(p->put(&lv, th.level));
+      tr.leaf_off = lo;
+      tr.node_lr = lr;
+      tr.level = lv;
+      p->trees.push_back(tr);
+      p->max_leaf = std::max(p->max_leaf, tr.nleaf);
+      p->leaf_stride = std::max<int64_t>(p->leaf_stride, tr.nleaf);
+      p->node_stride = std::max<int64_t>(p->node_stride, std::max(1, tr.nnode));
     }
     VK_TRY(p->put(&p->d_tables, p->tables));
+    VK_TRY(p->put(&p->d_trees, p->trees));
+    VK_TRY(p->alloc(&p->d_npleaf, (size_t)S * p->leaf_stride));
+    VK_TRY(p->alloc(&p->d_npnode, (size_t)S * p->node_stride));
+    VK_TRY(p->alloc(&p->d_mean, (size_t)S));
+    VK_TRY(p->alloc(&p->d_svar, (size_t)S));
+    VK_TRY(p->alloc(&p->d_sq, (size_t)S * d->max_pairs));
+    VK_TRY(p->alloc(&p->d_bsum, (size_t)S * d->n_bins));
     {
       const Pcg64 gen = pcg64_from_seed(d->seed);
       int32_t zoff = 0;
@@ -465,7 +498,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   // of the volume is still being reduced
   const int H = chained ? p->head_parts : 0;
   const int kh = H > 0 ? g.parts[H - 1].e + 1 : 0;   // head planes [0, kh)
-  BinsArgs ba;
+  BinSumArgs ba;
   ba.known = known;
   ba.values = nullptr;
   ba.part_base = p->d_part_base;
@@ -473,9 +506,24 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   ba.tables = p->d_tables;
   ba.max_pairs = d.max_pairs;
   ba.n_bins = d.n_bins;
-  ba.nblk = p->nblk;
-  ba.S = S;
-  ba.partial = p->d_partial;
+  ba.sq = p->d_sq;
+  ba.bsum = p->d_bsum;
+  ba.part0 = 0;
+  ba.n_parts = S;
+  NpVarArgs va;
+  va.known = known;
+  va.values = nullptr;
+  va.part_base = p->d_part_base;
+  va.part_m = p->d_part_m;
+  va.part_class = p->d_part_class;
+  va.trees = p->d_trees;
+  va.max_leaf = p->max_leaf;
+  va.leaf_stride = p->leaf_stride;
+  va.node_stride = p->node_stride;
+  va.leaf = p->d_npleaf;
+  va.node = p->d_npnode;
+  va.mean = p->d_mean;
+  va.svar = p->d_svar;
   if (draw || side_bins) {
     VK_CUDA(cudaEventRecord(p->ev_fork, st));
     VK_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
@@ -487,31 +535,45 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     }
     if (trace) cudaEventRecord(t_pre[0], p->side);
     if (side_bins && H > 0) {
-      BinsArgs b1 = ba;
+      BinSumArgs b1 = ba;
       b1.part0 = 0;
       b1.n_parts = H;
-      VK_CUDA(launch_bins(b1, p->side));
+      VK_CUDA(launch_binsums(b1, p->side));
       VK_CUDA(cudaEventRecord(p->ev_hbins, p->side));
       if (trace) cudaEventRecord(t_pre[1], p->side);
       b1.part0 = H;
       b1.n_parts = S - H;
-      VK_CUDA(launch_bins(b1, p->side));
-      kernels += 2;
+      VK_CUDA(launch_binsums(b1, p->side));
+      kernels += 4;
     } else if (side_bins) {
-      VK_CUDA(launch_bins(ba, p->side));
-      ++kernels;
+      VK_CUDA(launch_binsums(ba, p->side));
+      kernels += 2;
     }
     if (trace) cudaEventRecord(t_pre[2], p->side);
     VK_CUDA(cudaEventRecord(p->ev_join, p->side));
   }
   if (H > 0) {
     VK_CUDA(launch_plane_stats(known, 0, kh, P, p->d_stats, p->nchunk, st, p->d_inexact));
-    VK_CUDA(cudaEventRecord(p->ev_hstats, st));
     ++kernels;
+    if (d.fit_variogram) {
+      NpVarArgs v1 = va;
+      v1.part0 = 0;
+      v1.n_parts = H;
+      VK_CUDA(launch_npvar(v1, st));
+      kernels += 4;
+    }
+    VK_CUDA(cudaEventRecord(p->ev_hstats, st));
   }
   if (trace) cudaEventRecord(t_pre[3], st);
   VK_CUDA(launch_plane_stats(known, kh, g.K, P, p->d_stats, p->nchunk, st, p->d_inexact));
   ++kernels;
+  if (d.fit_variogram) {
+    NpVarArgs v1 = va;
+    v1.part0 = H;
+    v1.n_parts = S - H;
+    VK_CUDA(launch_npvar(v1, st));
+    kernels += 4;
+  }
   if (trace) cudaEventRecord(t_pre[4], st);
   if (fast && d.accum == VK_ACCUM_FIXED) {
     VK_CUDA(launch_quant_range(p->d_stats, g.K * p->nchunk, p->d_fxq, st));
@@ -521,8 +583,8 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   if (draw || side_bins) VK_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));   // "pairs" = residual wait
   if (d.fit_variogram && !side_bins) {
     VK_CUDA(mark(2));
-    VK_CUDA(launch_bins(ba, st));
-    ++kernels;
+    VK_CUDA(launch_binsums(ba, st));
+    kernels += 2;
   }
   if (!d.fit_variogram || side_bins) VK_CUDA(mark(2));
   VK_CUDA(mark(3));
@@ -540,6 +602,8 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   fa.part_m = p->d_part_m;
   fa.tables = p->d_tables;
   fa.partial = p->d_partial;
+  fa.svar = p->d_svar;
+  fa.bsum = p->d_bsum;
   fa.models = p->d_models;
   fa.lohi = p->d_lohi;
   fa.status = p->d_part_status;
@@ -1078,9 +1142,28 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   t.cnt = (int32_t*)get((size_t)ns * 4);
   t.off = (int64_t*)get((size_t)(ns + 1) * 8);
   t.hbits = (unsigned long long*)get(8);
+  t.order = (int32_t*)get((size_t)npmax * 4);
+  t.boff = (int32_t*)get((MAX_BINS + 1) * 4);
   PairTable* d_t = (PairTable*)get(sizeof(PairTable));
   ChunkStat* stats = (ChunkStat*)get((size_t)nchunk * sizeof(ChunkStat));
   double* partial = (double*)get((size_t)nblk * n_bins * 8);
+  const NpSumTreeHost th = build_npsum_tree(m);
+  NpSumTree tr;
+  tr.nleaf = (int32_t)th.leaf_off.size() - 1;
+  tr.nnode = (int32_t)th.node_lr.size() / 2;
+  tr.nlevel = (int32_t)th.level.size() - 1;
+  int32_t* t_lo = (int32_t*)get(th.leaf_off.size() * 4);
+  int32_t* t_lr = (int32_t*)get(std::max<size_t>(2, th.node_lr.size()) * 4);
+  int32_t* t_lv = (int32_t*)get(th.level.size() * 4);
+  tr.leaf_off = t_lo;
+  tr.node_lr = t_lr;
+  tr.level = t_lv;
+  NpSumTree* d_tr = (NpSumTree*)get(sizeof(NpSumTree));
+  double* npleaf = (double*)get((size_t)std::max(1, tr.nleaf) * 8);
+  double* npnode = (double*)get((size_t)std::max(1, tr.nnode) * 8);
+  double* npstat = (double*)get(2 * 8);
+  double* sq = (double*)get((size_t)npmax * 8);
+  double* bsum = (double*)get((size_t)n_bins * 8);
   double* models = (double*)get(3 * 8);
   double* lohi = (double*)get(2 * 8);
   int32_t* status = (int32_t*)get(4);
@@ -1091,6 +1174,11 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   for (void* q : mem)
     if (!q) { cleanup(); return set_err(VK_E_CUDA, "cudaMalloc failed"); }
   cudaError_t e = cudaMemcpyAsync(d_t, &t, sizeof(PairTable), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t_lo, th.leaf_off.data(), th.leaf_off.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !th.node_lr.empty())
+    e = cudaMemcpyAsync(t_lr, th.node_lr.data(), th.node_lr.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t_lv, th.level.data(), th.level.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_tr, &tr, sizeof(NpSumTree), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(zero32, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(zero64, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(mm, &m, 8, cudaMemcpyHostToDevice, st);
@@ -1107,7 +1195,24 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_job, &job, sizeof(PairJob), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = launch_pair_tables(d_job, &job, 1, st);
   if (e == cudaSuccess) e = launch_plane_stats_f64(values, m, stats, nchunk, st);
-  BinsArgs ba;
+  NpVarArgs va;
+  va.known = nullptr;
+  va.values = values;
+  va.part_base = zero64;
+  va.part_m = mm;
+  va.part_class = zero32;
+  va.trees = d_tr;
+  va.part0 = 0;
+  va.n_parts = 1;
+  va.max_leaf = tr.nleaf;
+  va.leaf_stride = tr.nleaf;
+  va.node_stride = std::max(1, tr.nnode);
+  va.leaf = npleaf;
+  va.node = npnode;
+  va.mean = npstat;
+  va.svar = npstat + 1;
+  if (e == cudaSuccess) e = launch_npvar(va, st);
+  BinSumArgs ba;
   ba.known = nullptr;
   ba.values = values;
   ba.part_base = zero64;
@@ -1115,10 +1220,11 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   ba.tables = d_t;
   ba.max_pairs = npmax;
   ba.n_bins = n_bins;
-  ba.nblk = nblk;
-  ba.S = 1;
-  ba.partial = partial;
-  if (e == cudaSuccess) e = launch_bins(ba, st);
+  ba.sq = sq;
+  ba.bsum = bsum;
+  ba.part0 = 0;
+  ba.n_parts = 1;
+  if (e == cudaSuccess) e = launch_binsums(ba, st);
   FitArgs fa;
   fa.S = 1;
   fa.n_bins = n_bins;
@@ -1133,6 +1239,8 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   fa.part_m = mm;
   fa.tables = d_t;
   fa.partial = partial;
+  fa.svar = npstat + 1;
+  fa.bsum = bsum;
   fa.models = models;
   fa.lohi = lohi;
   fa.status = status;

@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 #include "vk_common.h"
+#include "npsum.h"
 
 namespace vk {
 
@@ -24,6 +25,9 @@ struct PairTable {                   // one per pair class (device pointers)
   int32_t* cnt;                      // [n_thr]
   int64_t* off;                      // [n_thr + 1]
   unsigned long long* hbits;         // [1]
+  // pairs sorted by bin, stable (launch_pair_order; nullptr: not kept)
+  int32_t* order = nullptr;          // [npairs]
+  int32_t* boff = nullptr;           // [n_bins + 1]
 };
 // number of draw threads (= scratch entries) for a pair class
 int64_t pair_scratch_elems(int64_t m, int64_t max_pairs);
@@ -68,6 +72,48 @@ struct BinsArgs {
 };
 cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st);
 
+// ---- numpy-exact statistics (vk_npstats.cu) ----
+// numpy's pairwise-summation tree for an array of m float64 (leaves of <= 128
+// elements, internal nodes grouped by height)
+struct NpSumTree {                   // device view of one class's tree
+  int32_t nleaf, nnode, nlevel;
+  const int32_t* leaf_off;
+  const int32_t* node_lr;
+  const int32_t* level;
+};
+// svar[s] = values.var() of part s exactly as numpy computes it
+struct NpVarArgs {
+  const float* known;                // structured samples (known planes) or nullptr
+  const double* values;              // explicit samples or nullptr
+  const int64_t* part_base;          // [S]
+  const int64_t* part_m;             // [S]
+  const int32_t* part_class;         // [S]
+  const NpSumTree* trees;            // [n_classes]
+  int part0 = 0, n_parts = 0;
+  int max_leaf = 0;                  // max nleaf over the classes of the launch
+  int64_t leaf_stride = 0, node_stride = 0;
+  double* leaf;                      // [S][leaf_stride]
+  double* node;                      // [S][node_stride]
+  double* mean;                      // [S]
+  double* svar;                      // [S]
+};
+cudaError_t launch_npvar(const NpVarArgs& a, cudaStream_t st);
+// stable sort of each class's pairs by bin (tables with order != nullptr)
+cudaError_t launch_pair_order(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st);
+// bsum[s][b] = np.bincount(which, weights=0.5*(v_i - v_j)^2)[b] of part s
+struct BinSumArgs {
+  const float* known;
+  const double* values;
+  const int64_t* part_base;
+  const int32_t* part_class;
+  const PairTable* tables;
+  int part0 = 0, n_parts = 0, n_bins = 0;
+  int64_t max_pairs = 0;
+  double* sq;                        // [S][max_pairs] scratch
+  double* bsum;                      // [S][n_bins]
+};
+cudaError_t launch_binsums(const BinSumArgs& a, cudaStream_t st);
+
 struct FitArgs {
   int S, n_bins, nblk, kind, fit, nchunk;
   int part0, n_parts;       // parts [part0, part0 + n_parts) of this launch
@@ -78,7 +124,9 @@ struct FitArgs {
   const int32_t* part_class;
   const int64_t* part_m;    // [S]
   const PairTable* tables;
-  const double* partial;    // bins partials
+  const double* partial;    // bins partials (used when bsum == nullptr)
+  const double* svar = nullptr;   // [S] numpy-exact values.var() (else the Chan merge of the stats)
+  const double* bsum = nullptr;   // [S][n_bins] numpy-exact bin sums (else the partials)
   double* models;           // [S][3] in/out
   double* lohi;             // [S][2]
   int32_t* status;          // [S]

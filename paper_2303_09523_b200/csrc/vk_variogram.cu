@@ -13,7 +13,8 @@
 //   bins         : per part, sum of 0.5*(v_i - v_j)^2 per bin; per-thread
 //                  shared-memory accumulators reduced in a fixed order.
 //   fit          : per part, the TRF fit on the non-empty bins: one warp per
-//                  part, lane = residual row (trf_warp.cuh restating trf.h).
+//                  part, residual rows on lanes (trf_warp.cuh, trf.h); svar
+//                  and the bin sums come numpy-exact from vk_npstats.cu.
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cfloat>
@@ -364,7 +365,8 @@ __global__ void __launch_bounds__(256) bins_kernel(BinsArgs a) {
 __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   // One warp per sub-part.  Statistics are merged redundantly by every lane
   // (same order -> same bits); bins are reduced lane-per-bin; the TRF runs
-  // warp-parallel (lane = residual row) when n_bins + 3 <= 32.
+  // redundantly on every lane with residual rows evaluated lane-parallel
+  // (trf_warp.cuh).
   const int s = a.part0 + blockIdx.x, lane = threadIdx.x;
   __shared__ TrfProblem P;
   // Chan merge of the part's chunk statistics: lanes merge strided chunks,
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   if (bad > 0) status = PS_NONFINITE;
   else if (n <= 0) status = PS_FIT_FAILED;
   if (!a.fit) { if (lane == 0) a.status[s] = status; return; }
-  const double svar = m2 / n;
+  const double svar = a.svar ? a.svar[s] : m2 / n;
   const int64_t m = a.part_m[s];
   if (m * (m - 1) / 2 < 30) { if (lane == 0) a.status[s] = PS_INSUFFICIENT; return; }
   const PairTable t = a.tables[a.part_class[s]];
@@ -432,7 +434,9 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   const unsigned nzmask = __ballot_sync(0xffffffffu, cnt > 0);
   if (cnt > 0) {
     double sum = 0.0;
-    for (int blk = 0; blk < a.nblk; ++blk) sum += a.partial[((int64_t)s * a.nblk + blk) * a.n_bins + lane];
+    if (a.bsum) sum = a.bsum[(int64_t)s * a.n_bins + lane];
+    else
+      for (int blk = 0; blk < a.nblk; ++blk) sum += a.partial[((int64_t)s * a.nblk + blk) * a.n_bins + lane];
     const int r = __popc(nzmask & ((1u << lane) - 1u));
     // 0.5 * (edges[:-1] + edges[1:]) without contraction (numpy rounding)
     const double e0 = __dmul_rn((double)lane, step);
@@ -447,17 +451,11 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   const double lb[3] = {0.0, 0.0, 1e-6};
   const double ub[3] = {2.0 * svar + 1e-12, 4.0 * svar + 1e-12, 10.0 * hmax};
   if (!(ub[2] > lb[2])) { if (lane == 0) a.status[s] = PS_FIT_FAILED; return; }
-  if (P.nb + 3 > 32) {                  // residual rows exceed a warp: scalar kernel
-    if (lane == 0) a.status[s] = PS_NEED_SCALAR_FIT;
-    return;
-  }
-  VK_PT(t_f0);
+  __shared__ double rowbuf[3 * MAX_BINS];
   TrfResult r;
-  if (P.kind == KIND_EXPONENTIAL) r = WarpTrf<KIND_EXPONENTIAL>(P, lane).fit(x0, lb, ub);
-  else if (P.kind == KIND_GAUSSIAN) r = WarpTrf<KIND_GAUSSIAN>(P, lane).fit(x0, lb, ub);
-  else r = WarpTrf<KIND_SPHERICAL>(P, lane).fit(x0, lb, ub);
-  VK_PT(t_f1);
-  VK_PACC(5, t_f0, t_f1);
+  if (P.kind == KIND_EXPONENTIAL) r = trf_fit_t(WarpEval<KIND_EXPONENTIAL>(P, rowbuf, lane), x0, lb, ub);
+  else if (P.kind == KIND_GAUSSIAN) r = trf_fit_t(WarpEval<KIND_GAUSSIAN>(P, rowbuf, lane), x0, lb, ub);
+  else r = trf_fit_t(WarpEval<KIND_SPHERICAL>(P, rowbuf, lane), x0, lb, ub);
   if (lane != 0) return;
   if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
   const double nug = pymax(r.x[0], 0.0);
@@ -467,65 +465,8 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   a.status[s] = status;
 }
 
-// Scalar TRF (trf.h) for parts whose non-empty bins exceed 29 (n_bins > 29);
-// re-derives the problem exactly as fit_kernel does.
-__global__ void __launch_bounds__(32) fit_scalar_kernel(FitArgs a) {
-  const int s = a.part0 + blockIdx.x;
-  if (threadIdx.x != 0 || a.status[s] != PS_NEED_SCALAR_FIT) return;
-  double n = 0.0, mean = 0.0, m2 = 0.0;
-  for (int k = a.part_b[s]; k <= a.part_e[s]; ++k)
-    for (int c = 0; c < a.nchunk; ++c) {
-      const ChunkStat cs = a.stats[(int64_t)k * a.nchunk + c];
-      if (cs.n <= 0) continue;
-      const double nn = n + cs.n, d = cs.mean - mean;
-      mean = mean + d * (cs.n / nn);
-      m2 = m2 + cs.m2 + d * d * (n * cs.n / nn);
-      n = nn;
-    }
-  const double svar = m2 / n;
-  const PairTable t = a.tables[a.part_class[s]];
-  const double hmax = t.scal[0];
-  const double step = hmax / (double)a.n_bins;
-  TrfProblem P;
-  P.kind = a.kind;
-  P.nb = 0;
-  for (int b = 0; b < a.n_bins; ++b) {
-    const int64_t cnt = t.counts[b];
-    if (cnt <= 0) continue;
-    double sum = 0.0;
-    for (int blk = 0; blk < a.nblk; ++blk) sum += a.partial[((int64_t)s * a.nblk + blk) * a.n_bins + b];
-    const double e0 = __dmul_rn((double)b, step);
-    const double e1 = (b + 1 == a.n_bins) ? hmax : __dmul_rn((double)(b + 1), step);
-    P.h[P.nb] = __dmul_rn(0.5, __dadd_rn(e0, e1));
-    P.gemp[P.nb] = sum / (double)cnt;
-    P.w[P.nb] = sqrt((double)cnt);
-    P.nb++;
-  }
-  const double x0[3] = {0.0, svar, hmax / 3.0};
-  const double lb[3] = {0.0, 0.0, 1e-6};
-  const double ub[3] = {2.0 * svar + 1e-12, 4.0 * svar + 1e-12, 10.0 * hmax};
-  const TrfResult r = trf_fit(P, x0, lb, ub);
-  if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
-  double* model = a.models + 3 * s;
-  const double nug = pymax(r.x[0], 0.0);
-  model[0] = nug;
-  model[1] = nug + pymax(r.x[1], 0.0);
-  model[2] = pymax(r.x[2], 1e-6);
-  a.status[s] = PS_OK;
-}
-
 }  // namespace
 
-#ifdef VK_FIT_PROFILE
-extern "C" int vk_debug_fit_profile(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, g_fit_prof, sizeof(unsigned long long) * 12);
-  if (reset) {
-    unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(g_fit_prof, z, sizeof(z));
-  }
-  return 0;
-}
-#endif
 
 cudaError_t launch_plane_stats(const float* known, int k0, int k1, int64_t P, ChunkStat* out, int nchunk,
                                cudaStream_t st, int* inexact) {
@@ -727,8 +668,8 @@ __global__ void __launch_bounds__(PT_BLOCK) pair_draw_kernel(const PairJob* jobs
   }
 }
 
-cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st,
-                               int* launches) {
+static cudaError_t launch_pair_draw(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st,
+                                    int* launches) {
   int64_t max_thr = 1, max_pairs = 1, max_m = 1;
   for (int c = 0; c < n_jobs; ++c) {
     max_thr = std::max(max_thr, h_jobs[c].n_thr);
@@ -770,6 +711,18 @@ cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int
   return cudaGetLastError();
 }
 
+// draw, then the stable bin order of the pairs (tables that keep one)
+cudaError_t launch_pair_tables(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st,
+                               int* launches) {
+  cudaError_t e = launch_pair_draw(d_jobs, h_jobs, n_jobs, st, launches);
+  if (e != cudaSuccess) return e;
+  bool order = false;
+  for (int c = 0; c < n_jobs; ++c) order |= h_jobs[c].t.order != nullptr;
+  if (!order) return cudaSuccess;
+  if (launches) *launches += 1;
+  return launch_pair_order(d_jobs, h_jobs, n_jobs, st);
+}
+
 cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
   dim3 grid(a.nblk, a.n_parts > 0 ? a.n_parts : a.S);
   const size_t smem = (size_t)a.n_bins * 256 * sizeof(double);
@@ -793,7 +746,6 @@ cudaError_t launch_fit(const FitArgs& a, cudaStream_t st) {
     }
   }
   fit_kernel<<<a.n_parts, 32, a.reserve_smem, st>>>(a);
-  if (a.fit && a.n_bins + 3 > 32) fit_scalar_kernel<<<a.n_parts, 32, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -129,3 +129,79 @@ int vkh_orbits(int H, int W, int T, const int* known_z, int K, int S, int drift,
 }
 
 }
+
+// ---- TRF pieces exposed for the fit-parity tests --------------------------
+extern "C" {
+
+// svd_aug of an (M x 3) row-major matrix: U (M x 3), s (3), VT (3 x 3) as numpy.linalg.svd returns them
+void vkh_svd_aug(const double* A, int M, double* U, double* s, double* VT) {
+  double V[9];
+  vk::svd_aug(A, M, U, s, V);
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 3; ++k) VT[k * 3 + i] = V[i * 3 + k];
+}
+
+void vkh_np_exp(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) y[i] = vk::np::exp_(x[i]);
+}
+
+}
+extern "C" void vkh_cube(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) y[i] = vk::np::cube(x[i]);
+}
+
+// ---- LAPACK / BLAS restatements of gesdd.h (checked against the shipped OpenBLAS) ----
+#include "gesdd.h"
+extern "C" {
+double vkl_dnrm2(int n, const double* x, int incx) { return vk::lapack::dnrm2(n, x, incx); }
+void vkl_dlarfg(int n, double* alpha, double* x, int incx, double* tau) { vk::lapack::dlarfg(n, alpha, x, incx, tau); }
+void vkl_dlarf(int left, int m, int n, const double* v, int incv, double tau, double* C, int ldc) { vk::lapack::dlarf(left != 0, m, n, v, incv, tau, C, ldc); }
+void vkl_dgeqr2(int m, int n, double* A, int lda, double* tau) { vk::lapack::dgeqr2(m, n, A, lda, tau); }
+void vkl_dorg2r(int m, int n, int k, double* A, int lda, const double* tau) { vk::lapack::dorg2r(m, n, k, A, lda, tau); }
+void vkl_dgebd2(int m, int n, double* A, int lda, double* d, double* e, double* tq, double* tp) { vk::lapack::dgebd2(m, n, A, lda, d, e, tq, tp); }
+void vkl_dlartg(double f, double g, double* c, double* s, double* r) { vk::lapack::dlartg(f, g, c, s, r); }
+void vkl_dlas2(double f, double g, double h, double* a, double* b) { vk::lapack::dlas2(f, g, h, a, b); }
+void vkl_dlasv2(double f, double g, double h, double* o) { vk::lapack::dlasv2(f, g, h, o, o + 1, o + 2, o + 3, o + 4, o + 5); }
+int vkl_dbdsqr(int n, double* d, double* e, double* VT, int ldvt, double* U, int ldu) { return vk::lapack::dbdsqr(n, d, e, VT, ldvt, U, ldu); }
+int vkl_dbdsdc(int n, double* d, double* e, double* U, int ldu, double* VT, int ldvt) { return vk::lapack::dbdsdc(n, d, e, U, ldu, VT, ldvt); }
+int vkl_svd_m3(const double* A, int M, double* U, double* s, double* VT) { return vk::lapack::svd_m3(A, M, U, s, VT); }
+void vkl_drot(int n, double* x, int incx, double* y, int incy, double c, double s) { vk::lapack::drot(n, x, incx, y, incy, c, s); }
+void vkl_dger(int m, int n, double alpha, const double* x, const double* y, int incy, double* A, int lda) { vk::lapack::dger(m, n, alpha, x, y, incy, A, lda); }
+void vkl_dgemv_t(int m, int n, const double* A, int lda, const double* x, double* y) { vk::lapack::dgemv_t(m, n, A, lda, x, y); }
+void vkl_dgemv_n(int m, int n, const double* A, int lda, const double* x, int incx, double* y) { vk::lapack::dgemv_n(m, n, A, lda, x, incx, y); }
+}
+
+// ---- numpy pairwise-summation tree (npsum.h) ----
+#include "npsum.h"
+extern "C" {
+// numpy's sum of a[0:n] evaluated over the host-built tree; returns nleaf
+double vkh_npsum_tree(const double* a, int64_t n, int32_t* nleaf_out) {
+  const vk::NpSumTreeHost t = vk::build_npsum_tree(n);
+  const int nleaf = (int)t.leaf_off.size() - 1;
+  const int nnode = (int)t.node_lr.size() / 2;
+  std::vector<double> v(nleaf + nnode);
+  for (int l = 0; l < nleaf; ++l) {
+    const int64_t o = t.leaf_off[l], m = t.leaf_off[l + 1] - o;
+    const double* x = a + o;
+    double res;
+    if (m < 8) {
+      res = -0.0;
+      for (int64_t i = 0; i < m; ++i) res += x[i];
+    } else {
+      double r[8];
+      for (int k = 0; k < 8; ++k) r[k] = x[k];
+      int64_t i = 8;
+      for (; i < m - m % 8; i += 8)
+        for (int k = 0; k < 8; ++k) r[k] += x[i + k];
+      res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+      for (; i < m; ++i) res += x[i];
+    }
+    v[l] = res;
+  }
+  for (int lev = 0; lev + 1 < (int)t.level.size(); ++lev)
+    for (int j = t.level[lev]; j < t.level[lev + 1]; ++j)
+      v[nleaf + j] = v[t.node_lr[2 * j]] + v[t.node_lr[2 * j + 1]];
+  if (nleaf_out) *nleaf_out = nleaf;
+  return nnode ? v[nleaf + nnode - 1] : v[0];
+}
+}

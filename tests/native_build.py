@@ -16,7 +16,7 @@ CSRC = os.path.join(ROOT, "paper_2303_09523_b200", "csrc")
 
 def build_shim() -> C.CDLL:
     out = os.path.join(tempfile.gettempdir(), f"vk_host_shim_{os.getpid()}.so")
-    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", CSRC,
+    cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-shared", "-fPIC", "-I", CSRC,
            os.path.join(HERE, "native", "host_shim.cpp"),
            os.path.join(CSRC, "vk_geometry.cpp"), "-o", out]
     subprocess.run(cmd, check=True)
