@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import hashlib
 import json
+import multiprocessing
 import os
 from concurrent.futures import ProcessPoolExecutor
 
@@ -39,7 +40,7 @@ def known_slices(name: str) -> np.ndarray:
         return ks(cfg)
     chunks = [zs[i::n] for i in range(n)]
     out = np.empty((len(zs), cfg.height, cfg.width), np.float32)
-    with ProcessPoolExecutor(n) as ex:
+    with ProcessPoolExecutor(n, mp_context=multiprocessing.get_context("spawn")) as ex:
         for i, planes in enumerate(ex.map(_planes, [(name, c) for c in chunks])):
             out[i::n] = planes
     return out
@@ -66,7 +67,7 @@ def oracle_parts(ks: np.ndarray, factor: int, ranges, models, drift="linear", tm
     np.save(path, ks)
     try:
         jobs = [(path, b, e, factor, tuple(models[s]), drift) for s, (b, e) in enumerate(ranges)]
-        with ProcessPoolExecutor(_workers()) as ex:
+        with ProcessPoolExecutor(_workers(), mp_context=multiprocessing.get_context("spawn")) as ex:
             for s, ((b, e), out) in enumerate(zip(ranges, ex.map(_fill_part, jobs))):
                 yield s, b, e, out
     finally:

@@ -11,7 +11,7 @@ from oracle import kriging_oracle as O
 pytestmark = pytest.mark.gpu
 
 TOL64 = 1e-6
-FIT_FUZZ = 5e-5
+FIT_FUZZ = 1e-6     # device fits reproduce the reference's (test_gpu_fit_parity.py)
 
 
 def _stack(seed, K, H, W):

@@ -21,7 +21,7 @@ pytestmark = [pytest.mark.gpu]
 
 TOL64 = 1e-6
 TOL32 = 1e-3
-FIT_FUZZ = 5e-5
+FIT_FUZZ = 1e-6     # device fits reproduce the reference's (test_gpu_fit_parity.py)
 
 
 def _oracle_voxels(ks, b, e, factor, model, drift, zyx):

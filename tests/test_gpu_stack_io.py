@@ -152,7 +152,7 @@ def test_formats_around_the_path(cuda, tmp_path):
     vol, _ = zk.run(st.slices)
     zk.finish()
     ref, _, _ = O.reconstruct_zparts(blob["u8_L/slices"], st.factor, 1)
-    assert np.abs(vol.cpu().numpy().astype(np.float64) - ref).max() <= 5e-5 * 1.0   # normalised range is 1
+    assert np.abs(vol.cpu().numpy().astype(np.float64) - ref).max() <= 1e-6 * 1.0   # normalised range is 1
     path = tmp_path / "out.vkv"
     save_volume(VolumeGrid(vol), path)
     back = load_volume(path)
