@@ -65,50 +65,78 @@ VK_HD int top_bit128(unsigned __int128 v) {
   return hi ? 127 - clz64(hi) : 63 - clz64((uint64_t)v);
 }
 
-// v * 2^e rounded to a 64-bit significand, round to nearest even
-VK_HD Ext ext_round(unsigned __int128 v, int e) {
-  if (v == 0) return Ext{0, 0};
-  const int tb = top_bit128(v);
-  if (tb <= 63) return Ext{(uint64_t)v << (63 - tb), e - (63 - tb)};
-  const int sh = tb - 63;
-  uint64_t m = (uint64_t)(v >> sh);
-  const unsigned __int128 rem = v & ((((unsigned __int128)1) << sh) - 1);
-  const unsigned __int128 half = ((unsigned __int128)1) << (sh - 1);
-  if (rem > half || (rem == half && (m & 1))) {
+VK_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+VK_HD uint64_t dbits(double x) {
+#if defined(__CUDA_ARCH__)
+  return (uint64_t)__double_as_longlong(x);
+#else
+  uint64_t b;
+  __builtin_memcpy(&b, &x, 8);
+  return b;
+#endif
+}
+
+// round-to-nearest-even increment of a 64-bit significand m whose discarded
+// fraction is frac (bit 63 = one half, bit 0 sticky)
+VK_HD Ext ext_round_frac(uint64_t m, uint64_t frac, int e) {
+  const uint64_t half = 1ull << 63;
+  if (frac > half || (frac == half && (m & 1))) {
     m += 1;
-    if (m == 0) return Ext{1ull << 63, e + sh + 1};
+    if (m == 0) return Ext{half, e + 1};
   }
-  return Ext{m, e + sh};
+  return Ext{m, e};
 }
 
 // fmul st(0), st(0) of a double loaded with fldl: x*x in extended precision
 VK_HD Ext ext_sq(double x) {
-  if (x == 0.0) return Ext{0, 0};
-  int ex;
-  const double fr = frexp(fabs(x), &ex);                // fr in [0.5, 1)
-  const uint64_t mx = (uint64_t)ldexp(fr, 53);          // exact 53-bit integer
-  return ext_round((unsigned __int128)mx * mx, 2 * (ex - 53));
+  const uint64_t bits = dbits(x) & 0x7fffffffffffffffull;
+  if (bits == 0) return Ext{0, 0};
+  int ex = (int)(bits >> 52);
+  uint64_t mx = bits & 0xfffffffffffffull;
+  if (ex == 0) {                                        // subnormal: normalise
+    const int sh = clz64(mx) - 11;
+    mx <<= sh;
+    ex = 1 - sh;
+  } else {
+    mx |= 1ull << 52;
+  }
+  // x = mx * 2^(ex - 1075); x^2 = mx^2 * 2^(2ex - 2150), mx^2 in [2^104, 2^106)
+  const uint64_t lo = mx * mx, hi = umulhi64(mx, mx);
+  const int e2 = 2 * ex - 2150;
+  if (hi >> 41) {                                       // top bit 105: drop 42 bits
+    const uint64_t m = (hi << 22) | (lo >> 42);
+    const uint64_t rest = lo << 22;                     // the 42 dropped bits, left-aligned
+    return ext_round_frac(m, rest, e2 + 42);
+  }
+  const uint64_t m = (hi << 23) | (lo >> 41);           // top bit 104: drop 41 bits
+  const uint64_t rest = lo << 23;
+  return ext_round_frac(m, rest, e2 + 41);
 }
 
-// faddp of two non-negative extended values
+// faddp of two non-negative extended values (round to nearest even, 64 bits)
 VK_HD Ext ext_add(Ext a, Ext b) {
   if (a.m == 0) return b;
   if (b.m == 0) return a;
-  if (b.e > a.e) { const Ext t = a; a = b; b = t; }
+  if (b.e > a.e || (b.e == a.e && b.m > a.m)) { const Ext t = a; a = b; b = t; }
   const int d = a.e - b.e;
-  const unsigned __int128 A = ((unsigned __int128)a.m) << 63;
-  unsigned __int128 B = ((unsigned __int128)b.m) << 63;
-  bool sticky = false;
-  if (d >= 127) {
-    sticky = true;
-    B = 0;
-  } else if (d > 0) {
-    sticky = (B & ((((unsigned __int128)1) << d) - 1)) != 0;
-    B >>= d;
-  }
-  unsigned __int128 s = A + B;
-  if (sticky) s |= 1;
-  return ext_round(s, a.e - 63);
+  if (d >= 66) return a;                                // b < a quarter ulp of a: no change
+  uint64_t bh, frac;
+  if (d == 0) { bh = b.m; frac = 0; }
+  else if (d < 64) { bh = b.m >> d; frac = b.m << (64 - d); }
+  else { bh = 0; frac = (b.m >> (d - 64)) | ((b.m << (128 - d)) != 0 ? 1ull : 0ull); }
+  const uint64_t sum = a.m + bh;
+  if (sum >= a.m) return ext_round_frac(sum, frac, a.e);   // no carry
+  // carry: true significand is 2^64 + sum; shift right one (keep sticky)
+  const uint64_t m = (1ull << 63) | (sum >> 1);
+  const uint64_t f2 = ((sum & 1) << 63) | (frac >> 1) | (frac & 1);
+  return ext_round_frac(m, f2, a.e + 1);
 }
 
 // fsqrt (correctly rounded to 64 bits) then fstpl (rounded to double)

@@ -115,6 +115,10 @@ struct TrfScalarEval {
     const FitModel md = fit_model(x);
     for (int r = 0; r < P.nb; ++r) f[r] = fit_residual_kind(P.kind, md, P.h[r], P.gemp[r], P.w[r]);
   }
+  // numpy.linalg.svd of the augmented Jacobian (gesdd.h)
+  VK_HD int svd(const double* A, int M, double* U, double* s, double* VT) const {
+    return lapack::svd_m3(A, M, U, s, VT);
+  }
   VK_HD void jac(const double* x, const double* f0, const double* lb, const double* ub, double* J) const {
     double f1[MAX_BINS];
     for (int i = 0; i < 3; ++i) {
@@ -464,9 +468,26 @@ VK_HD void trf_grad(const double* J, const double* f, int m, double* g) {
   for (int i = 0; i < 3; ++i) g[i] = np::colT(J + i * m, f, m, i);
 }
 
+// optional per-phase cycle counters of the device fit (-DVK_FIT_PROFILE,
+// tools/fit_phase_profile.py): 0 resid, 1 jac+grad, 2 svd, 3 lsq, 4 select,
+// 5 total, 6 iterations, 7 nfev
+#if defined(VK_FIT_PROFILE) && defined(__CUDACC__)
+__device__ unsigned long long g_fit_prof[16];
+#endif
+#if defined(VK_FIT_PROFILE) && defined(__CUDA_ARCH__)
+#define VK_TP(v) const long long v = clock64()
+#define VK_TACC(slot, a) if ((threadIdx.x & 31) == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)(clock64() - (a)))
+#define VK_TADD(slot, n) if ((threadIdx.x & 31) == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)(n))
+#else
+#define VK_TP(v)
+#define VK_TACC(slot, a)
+#define VK_TADD(slot, n)
+#endif
+
 // trf.py trf_bounds with loss='linear', x_scale=1, tr_solver='exact'.
 template <class Eval>
 VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb, const double* ub) {
+  VK_TP(t_all);
   const int m = ev.m();
   const double ftol = 1e-8, xtol = 1e-8, gtol = 1e-8;
   const int max_nfev = 300;
@@ -527,10 +548,12 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
       for (int c = 0; c < 3; ++c) Ja[(m + r) * 3 + c] = (r == c) ? np::sqrt_(diag_h[r]) : 0.0;
     {
       double VT[9];
-      if (M < 5 || lapack::svd_m3(Ja, M, U, sv, VT) != 0) svd_aug(Ja, M, U, sv, V);
+      VK_TP(t_svd);
+      if (M < 5 || ev.svd(Ja, M, U, sv, VT) != 0) svd_aug(Ja, M, U, sv, V);
       else
         for (int i = 0; i < 3; ++i)
           for (int k = 0; k < 3; ++k) V[i * 3 + k] = VT[k * 3 + i];
+      VK_TACC(2, t_svd);
     }
     for (int r = 0; r < M; ++r) fa[r] = r < m ? f[r] : 0.0;
     double uf[3];
@@ -540,10 +563,15 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
     double step_norm = 0.0;
     while (actual_reduction <= 0 && nfev < max_nfev) {
       double p_h[3], p[3];
+      VK_TP(t_lsq);
       lsq_trust_region(m, uf, sv, V, Delta, alpha, p_h, &alpha);
+      VK_TACC(3, t_lsq);
+      VK_TP(t_sel);
       for (int i = 0; i < 3; ++i) p[i] = np::mul(d[i], p_h[i]);
       double step[3], step_h[3], pred;
-      if (!select_step(x, Ja, m, diag_h, g_h, p, p_h, d, Delta, lb, ub, theta, step, step_h, &pred)) {
+      const bool sel_ok = select_step(x, Ja, m, diag_h, g_h, p, p_h, d, Delta, lb, ub, theta, step, step_h, &pred);
+      VK_TACC(4, t_sel);
+      if (!sel_ok) {
         res.status = -1;
         res.nfev = nfev;
         res.iterations = iteration;
@@ -552,7 +580,9 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
       }
       for (int i = 0; i < 3; ++i) x_new[i] = np::add(x[i], step[i]);
       make_strictly_feasible(x_new, lb, ub, 0.0);
+      VK_TP(t_res);
       ev.resid(x_new, f_new);
+      VK_TACC(0, t_res);
       nfev += 1;
       const double step_h_norm = np::norm(step_h, 3);
       bool finite = true;
@@ -583,8 +613,10 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
       for (int i = 0; i < 3; ++i) x[i] = x_new[i];
       for (int r = 0; r < m; ++r) f[r] = f_new[r];
       cost = cost_new;
+      VK_TP(t_jac);
       ev.jac(x, f, lb, ub, J);
       trf_grad(J, f, m, g);
+      VK_TACC(1, t_jac);
     }
     iteration += 1;
   }
@@ -593,6 +625,9 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
   res.status = status;
   res.nfev = nfev;
   res.iterations = iteration;
+  VK_TACC(5, t_all);
+  VK_TADD(6, iteration);
+  VK_TADD(7, nfev);
   return res;
 }
 

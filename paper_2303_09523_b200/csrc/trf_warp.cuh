@@ -3,11 +3,13 @@
 // redundantly on all 32 lanes -- every lane holds the same iterate, bit for
 // bit, so lanes never diverge -- while the residual rows (one bin per lane)
 // and the three finite-difference columns of the Jacobian are evaluated
-// lane-parallel and shared through a per-warp shared-memory row buffer.
+// lane-parallel and shared through a per-warp shared-memory row buffer, and
+// the SVD's row work is spread over the lanes (gesdd_warp.cuh).
 // The residual is the only part of an iteration whose cost grows with the
 // bins, and its SVML exp is the most expensive scalar operation of the fit.
 #pragma once
 #include "trf.h"
+#include "gesdd_warp.cuh"
 
 namespace vk {
 
@@ -15,10 +17,16 @@ template <int KIND>
 struct WarpEval {
   const TrfProblem& P;      // shared memory
   double* row;              // shared memory, >= 3 * MAX_BINS doubles
+  lapack::SvdWarpSmem& sv;  // shared memory
   int lane;
 
-  __device__ WarpEval(const TrfProblem& p, double* buf, int l) : P(p), row(buf), lane(l) {}
+  __device__ WarpEval(const TrfProblem& p, double* buf, lapack::SvdWarpSmem& s, int l)
+      : P(p), row(buf), sv(s), lane(l) {}
   __device__ int m() const { return P.nb; }
+
+  __device__ int svd(const double* A, int M, double* U, double* s, double* VT) const {
+    return lapack::svd_m3_warp(A, M, U, s, VT, sv, lane);
+  }
 
   __device__ void resid(const double* x, double* f) const {
     const FitModel md = fit_model(x);

@@ -105,7 +105,13 @@ struct vk_plan {
   double *d_npleaf = nullptr, *d_npnode = nullptr, *d_mean = nullptr, *d_svar = nullptr;
   double *d_sq = nullptr, *d_bsum = nullptr;
   bool pairs_ready = false;
-  double* h_models = nullptr;        // pinned staging [S][3]
+  // pinned staging of caller models ([S][3] each): a ring, so an execute
+  // queued behind another on a busy stream never overwrites models whose
+  // host-to-device copy has not run yet (each slot's copy is fenced by an event)
+  static constexpr int NMODEL_RING = 4;
+  double* h_models[NMODEL_RING] = {};
+  cudaEvent_t ev_models[NMODEL_RING] = {};
+  int models_slot = 0;
   int kernels = 0;
   cudaStream_t side = nullptr;        // pair draw runs here, concurrent with stats
   cudaStream_t io = nullptr;          // vk_plan_download: host-side known planes
@@ -163,7 +169,10 @@ struct vk_plan {
       if (pchain[i]) cudaStreamDestroy(pchain[i]);
     }
     for (void* p : allocs) cudaFree(p);
-    if (h_models) cudaFreeHost(h_models);
+    for (int i = 0; i < NMODEL_RING; ++i) {
+      if (h_models[i]) cudaFreeHost(h_models[i]);
+      if (ev_models[i]) cudaEventDestroy(ev_models[i]);
+    }
   }
 };
 
@@ -318,7 +327,10 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
     VK_TRY(p->alloc(&p->d_fxc, fxc_floats(S, std::max(1, p->NK))));
     VK_TRY(p->alloc(&p->d_fxq, (size_t)8));
   }
-  VK_TRY(cudaMallocHost((void**)&p->h_models, (size_t)S * 3 * sizeof(double)));
+  for (int i = 0; i < vk_plan::NMODEL_RING; ++i) {
+    VK_TRY(cudaMallocHost((void**)&p->h_models[i], (size_t)S * 3 * sizeof(double)));
+    VK_TRY(cudaEventCreateWithFlags(&p->ev_models[i], cudaEventDisableTiming));
+  }
   if (d->fit_variogram) {
     VK_TRY(p->alloc(&p->d_partial, (size_t)S * p->nblk * d->n_bins));
     for (size_t c = 0; c < g.pair_classes.size(); ++c) {
@@ -479,9 +491,13 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   }
   if (!d.fit_variogram) {
     if (!models) return set_err(VK_E_INVALID_ARGUMENT, "models required when fit_variogram == 0");
-    std::memcpy(p->h_models, models, (size_t)S * 3 * sizeof(double));
-    VK_CUDA(cudaMemcpyAsync(p->d_models, p->h_models, (size_t)S * 3 * sizeof(double),
+    const int slot = p->models_slot;
+    p->models_slot = (slot + 1) % vk_plan::NMODEL_RING;
+    VK_CUDA(cudaEventSynchronize(p->ev_models[slot]));     // that slot's earlier copy has run
+    std::memcpy(p->h_models[slot], models, (size_t)S * 3 * sizeof(double));
+    VK_CUDA(cudaMemcpyAsync(p->d_models, p->h_models[slot], (size_t)S * 3 * sizeof(double),
                             cudaMemcpyHostToDevice, st));
+    VK_CUDA(cudaEventRecord(p->ev_models[slot], st));
   }
   // the pair draw depends only on geometry and seed: fork it onto the side
   // stream so it overlaps the plane statistics

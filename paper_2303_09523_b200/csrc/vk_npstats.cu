@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(256) npsum_leaf_kernel(NpVarArgs a) {
     n8 = n - n % 8;
     if (n >= 8) {
       r = npv<MODE>(a.known, a.values, base + o + k, mean);
+#pragma unroll 4
       for (int64_t i = 8; i < n8; i += 8) r = __dadd_rn(r, npv<MODE>(a.known, a.values, base + o + i + k, mean));
     }
   }
@@ -177,24 +178,57 @@ __global__ void __launch_bounds__(256) binsq_kernel(BinSumArgs a) {
   }
 }
 
-// bin sums in pair order, one lane per bin (np.bincount: out[b] += w in order)
+// bin sums in pair order (np.bincount: out[b] += w in order): one warp per
+// (part, bin).  The warp streams the bin's slots in coalesced chunks of 256
+// into registers, parks them in shared memory, and lane 0 adds them in order
+// while the next chunk's loads are in flight.
 __global__ void __launch_bounds__(32) binsum_kernel(BinSumArgs a) {
-  const int s = a.part0 + blockIdx.x, lane = threadIdx.x;
-  if (lane >= a.n_bins) return;
+  const int s = a.part0 + blockIdx.y, b = blockIdx.x, lane = threadIdx.x;
   const PairTable t = a.tables[a.part_class[s]];
-  const int q0 = t.boff[lane], q1 = t.boff[lane + 1];
+  const int q0 = t.boff[b], q1 = t.boff[b + 1];
   const double* x = a.sq + (int64_t)s * a.max_pairs;
+  __shared__ double buf[2][256];
+  double v[8];
+  auto fetch = [&](int q) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = q + lane + 32 * u;
+      v[u] = i < q1 ? x[i] : 0.0;
+    }
+  };
+  auto park = [&](int slot) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) buf[slot][lane + 32 * u] = v[u];
+  };
   double sum = 0.0;
-  int q = q0;
-  for (; q + 8 <= q1; q += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = x[q + u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, v[u]);
+  int cur = 0;
+  if (q0 < q1) {
+    fetch(q0);
+    park(0);
   }
-  for (; q < q1; ++q) sum = __dadd_rn(sum, x[q]);
-  a.bsum[(int64_t)s * a.n_bins + lane] = sum;
+  __syncwarp();
+  for (int q = q0; q < q1; q += 256) {
+    const bool more = q + 256 < q1;
+    if (more) fetch(q + 256);                 // in flight while lane 0 adds
+    if (lane == 0) {
+      const int n = min(256, q1 - q);
+      const double* c = buf[cur];
+      int k = 0;
+      for (; k + 8 <= n; k += 8) {
+        double w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = c[k + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, w[u]);
+      }
+      for (; k < n; ++k) sum = __dadd_rn(sum, c[k]);
+    }
+    __syncwarp();
+    if (more) park(cur ^ 1);
+    __syncwarp();
+    cur ^= 1;
+  }
+  if (lane == 0) a.bsum[(int64_t)s * a.n_bins + b] = sum;
 }
 
 }  // namespace
@@ -230,7 +264,7 @@ cudaError_t launch_binsums(const BinSumArgs& a, cudaStream_t st) {
   if (a.n_parts <= 0) return cudaSuccess;
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (a.max_pairs + 1023) / 1024));
   binsq_kernel<<<dim3(gx, a.n_parts), 256, 0, st>>>(a);
-  binsum_kernel<<<a.n_parts, 32, 0, st>>>(a);
+  binsum_kernel<<<dim3(a.n_bins, a.n_parts), 32, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -452,10 +452,11 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   const double ub[3] = {2.0 * svar + 1e-12, 4.0 * svar + 1e-12, 10.0 * hmax};
   if (!(ub[2] > lb[2])) { if (lane == 0) a.status[s] = PS_FIT_FAILED; return; }
   __shared__ double rowbuf[3 * MAX_BINS];
+  __shared__ lapack::SvdWarpSmem svsm;
   TrfResult r;
-  if (P.kind == KIND_EXPONENTIAL) r = trf_fit_t(WarpEval<KIND_EXPONENTIAL>(P, rowbuf, lane), x0, lb, ub);
-  else if (P.kind == KIND_GAUSSIAN) r = trf_fit_t(WarpEval<KIND_GAUSSIAN>(P, rowbuf, lane), x0, lb, ub);
-  else r = trf_fit_t(WarpEval<KIND_SPHERICAL>(P, rowbuf, lane), x0, lb, ub);
+  if (P.kind == KIND_EXPONENTIAL) r = trf_fit_t(WarpEval<KIND_EXPONENTIAL>(P, rowbuf, svsm, lane), x0, lb, ub);
+  else if (P.kind == KIND_GAUSSIAN) r = trf_fit_t(WarpEval<KIND_GAUSSIAN>(P, rowbuf, svsm, lane), x0, lb, ub);
+  else r = trf_fit_t(WarpEval<KIND_SPHERICAL>(P, rowbuf, svsm, lane), x0, lb, ub);
   if (lane != 0) return;
   if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
   const double nug = pymax(r.x[0], 0.0);
@@ -733,6 +734,17 @@ cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st) {
   bins_kernel<<<grid, 256, smem, st>>>(a);
   return cudaGetLastError();
 }
+
+#ifdef VK_FIT_PROFILE
+extern "C" int vk_debug_fit_profile(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, vk::g_fit_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(vk::g_fit_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 cudaError_t launch_fit(const FitArgs& a, cudaStream_t st) {
   if (a.n_parts <= 0) return cudaSuccess;

@@ -82,6 +82,52 @@ def _stream_handle(stream) -> int:
     return int(s.cuda_stream)
 
 
+def _model_params(model):
+    """(kind, [nugget, sill, range_len]) of any object with the reference
+    VariogramModel's attributes (kriging.py:44-57) -- ours or volkrig's."""
+    kind = model.kind
+    if kind not in VARIOGRAM_KINDS:
+        raise ValueError(f"kind must be one of {VARIOGRAM_KINDS}")
+    return kind, np.array([float(model.nugget), float(model.sill), float(model.range_len)],
+                          dtype=np.float64)
+
+
+def _is_cuda_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch") and bool(x.is_cuda)
+
+
+def _grid_parts(grid):
+    """(data, mask, origin_offset, on_device) of any object with the reference
+    VolumeGrid's attributes (model.py:71-92): ``.data`` [z, y, x],
+    ``.missing_mask`` (None -> NaN sentinel), ``.origin_offset``."""
+    data = grid.data
+    mask = getattr(grid, "missing_mask", None)
+    origin = tuple(getattr(grid, "origin_offset", (0, 0, 0)))
+    on_dev = _is_cuda_tensor(data)
+    if on_dev:
+        torch = _torch()
+        data = data.to(torch.float32).contiguous()
+        mask = (torch.isnan(data) if mask is None else mask.to(torch.bool)).contiguous()
+    else:
+        data = np.ascontiguousarray(data, dtype=np.float32)
+        mask = np.ascontiguousarray(np.isnan(data) if mask is None else mask, dtype=bool)
+    if tuple(mask.shape) != tuple(data.shape) or len(data.shape) != 3:
+        raise ValueError("volume data must be 3D with a mask of the same shape")
+    return data, mask, origin, on_dev
+
+
+def _like_grid(grid, data, mask, origin):
+    """A result grid of the caller's grid type (the reference's VolumeGrid for
+    a reference grid), falling back to ours for device data."""
+    cls = type(grid)
+    if cls is not VolumeGrid:
+        try:
+            return cls(data, mask, origin)
+        except Exception:
+            pass
+    return VolumeGrid(data, mask, origin)
+
+
 class KrigingPlan:
     """A device plan: geometry tables, stencil systems and workspace for one
     grid layout (``vk_plan``).  ``execute`` is stream-ordered and async;
@@ -316,9 +362,9 @@ def solve_systems(rels, model: VariogramModel, drift="linear"):
                              np.zeros((0, 3), np.int16)).cuda()
     w_d = torch.empty(int(off[-1]), dtype=torch.float64, device="cuda")
     v_d = torch.empty(len(arrs), dtype=torch.float64, device="cuda")
-    m = np.ascontiguousarray(model.as_array(), dtype=np.float64)
+    kind, m = _model_params(model)
     raise_for_status(_lib.load().vk_solve_systems(
-        rel_d.data_ptr(), off.ctypes.data, len(arrs), _lib.KIND_IDS[model.kind],
+        rel_d.data_ptr(), off.ctypes.data, len(arrs), _lib.KIND_IDS[kind],
         _lib.DRIFT_IDS[drift], m.ctypes.data, w_d.data_ptr(), v_d.data_ptr(), None,
         _stream_handle(None)))
     w = w_d.cpu().numpy()
@@ -333,8 +379,9 @@ def interpolate_voxel(grid: VolumeGrid, target, model: VariogramModel, drift="li
     window gather is index arithmetic on the mask; the system is solved on
     the device (``solve_systems``)."""
     x, y, z = (int(v) for v in target)
-    data = grid.data.cpu().numpy() if grid.on_device else grid.data
-    mask = grid.missing_mask.cpu().numpy() if grid.on_device else grid.missing_mask
+    data, mask, _, on_dev = _grid_parts(grid)
+    if on_dev:
+        data, mask = data.cpu().numpy(), mask.cpu().numpy()
     if not mask[z, y, x]:
         return float(data[z, y, x])
     dz, dy, dx = data.shape
@@ -356,7 +403,7 @@ def interpolate_voxel(grid: VolumeGrid, target, model: VariogramModel, drift="li
     return float(np.clip(pred, clamp_range[0], clamp_range[1]))
 
 
-def _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev):
+def _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev, origin):
     """Non-plane masks on the device: ``vk_fill_generic`` (window schedule,
     distinct-pattern solves, per-voxel prediction; kriging.py:408-431)."""
     torch = _torch()
@@ -367,18 +414,28 @@ def _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev):
     out_d = torch.empty_like(data_d)
     var_d = (torch.empty(data_d.shape, dtype=torch.float64, device=data_d.device)
              if return_variance else None)
-    m = np.ascontiguousarray(model.as_array(), dtype=np.float64)
+    kind, m = _model_params(model)
     info = np.zeros(3, np.int64)
     raise_for_status(lib.vk_fill_generic(
-        data_d.data_ptr(), mask_d.data_ptr(), T, H, W, _lib.KIND_IDS[model.kind],
+        data_d.data_ptr(), mask_d.data_ptr(), T, H, W, _lib.KIND_IDS[kind],
         _lib.DRIFT_IDS[drift], m.ctypes.data, lo, hi, out_d.data_ptr(),
         var_d.data_ptr() if var_d is not None else None, info.ctypes.data,
         _stream_handle(None)))
+    return _result(grid, out_d, var_d, on_dev, origin, return_variance)
+
+
+def _result(grid, out_d, var_d, on_dev, origin, return_variance):
+    """kriging.py:492-496: new grid, all-false mask, same origin_offset;
+    numpy in -> numpy out, CUDA in -> CUDA out."""
+    torch = _torch()
     if on_dev:
-        out_grid = VolumeGrid(out_d, torch.zeros_like(grid.missing_mask), grid.origin_offset)
+        out_grid = _like_grid(grid, out_d, torch.zeros(out_d.shape, dtype=torch.bool,
+                                                       device=out_d.device), origin)
         return (out_grid, var_d) if return_variance else out_grid
-    out_grid = VolumeGrid(out_d.cpu().numpy(), np.zeros_like(grid.missing_mask), grid.origin_offset)
-    return (out_grid, var_d.cpu().numpy()) if return_variance else out_grid
+    out_grid = _like_grid(grid, out_d.cpu().numpy(), np.zeros(tuple(out_d.shape), dtype=bool), origin)
+    if return_variance:
+        return out_grid, var_d.cpu().numpy()
+    return out_grid
 
 
 def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
@@ -394,13 +451,13 @@ def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
     torch = _torch()
     if callable(drift):
         raise DeviceUnsupported("a callable drift cannot cross the C ABI")
-    on_dev = grid.on_device
-    data = grid.data
+    kind, mparams = _model_params(model)
+    data, mask, origin, on_dev = _grid_parts(grid)
     if on_dev:
-        data_d, mask_d = data, grid.missing_mask.view(torch.uint8)
+        data_d, mask_d = data, mask.view(torch.uint8)
     else:
         data_d = torch.from_numpy(data).cuda()
-        mask_d = torch.from_numpy(grid.missing_mask.view(np.uint8)).cuda()
+        mask_d = torch.from_numpy(mask.view(np.uint8)).cuda()
     T, H, W = data_d.shape
     counts = _scan_grid(data_d, mask_d)
     if counts[:, 2].any():
@@ -409,10 +466,11 @@ def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
         raise ValueError("known voxels must be finite")
     n_missing = counts[:, 0].astype(np.int64)
     if n_missing.sum() == 0:                                 # kriging.py:469-473
-        out = grid.copy()
+        out = grid.copy() if hasattr(grid, "copy") else _like_grid(grid, data.clone() if on_dev
+                                                                    else data.copy(), mask, origin)
         if return_variance:
             zeros = (torch.zeros(data_d.shape, dtype=torch.float64, device=data_d.device)
-                     if on_dev else np.zeros(data.shape, dtype=np.float64))
+                     if on_dev else np.zeros(tuple(data.shape), dtype=np.float64))
             return out, zeros
         return out
     P = H * W
@@ -423,9 +481,15 @@ def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
         raise ValueError(f"unknown drift {drift!r}")
     if not np.all((n_missing == 0) | (n_missing == P)):
         # arbitrary mask: the per-voxel window path (kriging.py:488-490, 408-431)
-        return _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev)
-    plan = cached_plan(height=H, width=W, depth=T, known_z=known_z.tolist(), n_subparts=1,
-                       kind=model.kind, drift=drift, accum=accum, fit=False)
+        return _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev, origin)
+    try:
+        plan = cached_plan(height=H, width=W, depth=T, known_z=known_z.tolist(), n_subparts=1,
+                           kind=kind, drift=drift, accum=accum, fit=False)
+    except DeviceUnsupported:
+        # a missing plane whose z window reaches more than NPMAX known planes:
+        # the per-voxel path selects the same windows (in-plane 4, z extent
+        # 4 -> 8 -> 16 until bracketed) with no plane limit
+        return _fill_generic(grid, data_d, mask_d, model, drift, return_variance, on_dev, origin)
     lib = _lib.load()
     known_d = torch.empty((len(known_z), H, W), dtype=torch.float32, device=data_d.device)
     raise_for_status(lib.vk_gather_planes(data_d.data_ptr(), known_z.ctypes.data,
@@ -434,13 +498,6 @@ def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
     out_d = torch.empty((T, H, W), dtype=torch.float32, device=data_d.device)
     var_d = (torch.empty((T, H, W), dtype=torch.float64, device=data_d.device)
              if return_variance else None)
-    plan.execute(known_d, out_d, var_d, models=model.as_array()[None, :])
+    plan.execute(known_d, out_d, var_d, models=mparams[None, :])
     plan.finish()
-    if on_dev:
-        out_grid = VolumeGrid(out_d, torch.zeros_like(grid.missing_mask), grid.origin_offset)
-        return (out_grid, var_d) if return_variance else out_grid
-    out_grid = VolumeGrid(out_d.cpu().numpy(), np.zeros_like(grid.missing_mask),
-                          grid.origin_offset)
-    if return_variance:
-        return out_grid, var_d.cpu().numpy()
-    return out_grid
+    return _result(grid, out_d, var_d, on_dev, origin, return_variance)
