@@ -78,6 +78,22 @@ int nccl_err(const char* what, ncclResult_t r) {
     if (r_ != ncclSuccess) return nccl_err(#call, r_);       \
   } while (0)
 
+// inside ncclGroupStart/End: keep the first failure, carry on to group_end
+// (an open group would capture the process's later NCCL calls, torch's too)
+#define VK_NCCL_G(first, call)                               \
+  do {                                                       \
+    const ncclResult_t r_ = (call);                          \
+    if (r_ != ncclSuccess && first.r == ncclSuccess) {       \
+      first.r = r_;                                          \
+      first.what = #call;                                    \
+    }                                                        \
+  } while (0)
+
+struct GroupErr {
+  ncclResult_t r = ncclSuccess;
+  const char* what = "";
+};
+
 int need_nccl() {
   if (!nccl().ok) return vk::comm_set_err(VK_E_UNSUPPORTED, nccl().why);
   return VK_OK;
@@ -125,10 +141,12 @@ int vk_halo_exchange(void* comm, const float* first_plane, float* halo, int64_t 
   if ((rank > 0 && !first_plane) || (rank < world - 1 && !halo))
     return vk::comm_set_err(VK_E_INVALID_ARGUMENT, "vk_halo_exchange: null plane");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  GroupErr ge;
   VK_NCCL(nccl().group_start());
-  if (rank > 0) VK_NCCL(nccl().send(first_plane, (size_t)n, ncclFloat32, rank - 1, c, st));
-  if (rank < world - 1) VK_NCCL(nccl().recv(halo, (size_t)n, ncclFloat32, rank + 1, c, st));
+  if (rank > 0) VK_NCCL_G(ge, nccl().send(first_plane, (size_t)n, ncclFloat32, rank - 1, c, st));
+  if (rank < world - 1) VK_NCCL_G(ge, nccl().recv(halo, (size_t)n, ncclFloat32, rank + 1, c, st));
   VK_NCCL(nccl().group_end());
+  if (ge.r != ncclSuccess) return nccl_err(ge.what, ge.r);
   return VK_OK;
 }
 
@@ -148,12 +166,14 @@ int vk_gather_core(void* comm, const float* core, const int64_t* counts, float* 
       if (ce != cudaSuccess) return vk::comm_set_err(VK_E_CUDA, cudaGetErrorString(ce));
     }
     int64_t off = counts[0];
+    GroupErr ge;
     VK_NCCL(nccl().group_start());
     for (int r = 1; r < world; ++r) {
-      if (counts[r] > 0) VK_NCCL(nccl().recv(out + off, (size_t)counts[r], ncclFloat32, r, c, st));
+      if (counts[r] > 0) VK_NCCL_G(ge, nccl().recv(out + off, (size_t)counts[r], ncclFloat32, r, c, st));
       off += counts[r];
     }
     VK_NCCL(nccl().group_end());
+    if (ge.r != ncclSuccess) return nccl_err(ge.what, ge.r);
   } else if (counts[rank] > 0) {
     if (!core) return vk::comm_set_err(VK_E_INVALID_ARGUMENT, "vk_gather_core: core");
     VK_NCCL(nccl().send(core, (size_t)counts[rank], ncclFloat32, 0, c, st));

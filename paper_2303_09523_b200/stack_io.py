@@ -185,10 +185,11 @@ def _decode_all(files, workers):
     return out, shape
 
 
-def load_stack(manifest_path, device: bool = True, workers: int | None = None) -> SliceStack:
-    """io.py:128-143: parse, decode, stack and normalise.  The result's
-    ``slices`` is a CUDA float32 tensor ([n, h, w], the known slices the
-    kriging path consumes); ``device=False`` copies it back to numpy."""
+def load_stack(manifest_path, device: bool = False, workers: int | None = None) -> SliceStack:
+    """io.py:128-143: parse, decode, stack and normalise (on the device).  The
+    result's ``slices`` is a numpy float32 [n, h, w] array like the
+    reference's; ``device=True`` keeps it as the CUDA tensor the kriging path
+    consumes."""
     manifest = parse_manifest(manifest_path)
     decoded, (h, w) = _decode_all(manifest.slice_files, workers)
     n = len(decoded)

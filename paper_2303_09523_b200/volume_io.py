@@ -12,7 +12,8 @@ mask, and a trailing CRC-32 of everything before it.
 * ``load_volume`` checks size, magic, version and length on the host in the
   reference's order (io.py:170-186, ``CorruptHeader``), uploads the body once
   and verifies the CRC on the device (``ChecksumMismatch``), then unpacks the
-  mask there.  ``device=False`` returns numpy arrays like the reference.
+  mask there.  The default returns numpy arrays like the reference;
+  ``device=True`` keeps the grid on the GPU.
 """
 
 from __future__ import annotations
@@ -109,7 +110,7 @@ def parse_header(blob: bytes, path="<bytes>"):
     return (dx, dy, dz), (ox, oy, oz)
 
 
-def load_volume(path, device: bool = True) -> VolumeGrid:
+def load_volume(path, device: bool = False) -> VolumeGrid:
     """io.py:170-200; the CRC check and mask unpacking run on the GPU."""
     try:
         blob = Path(path).read_bytes()

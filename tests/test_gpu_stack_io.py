@@ -28,7 +28,7 @@ def test_load_stack_matches_reference(cuda):
     with open(os.path.join(GOLD, "reference_stack.json")) as f:
         meta = json.load(f)
     for s in meta["stacks"]:
-        st = load_stack(os.path.join(GOLD, s["manifest"]))
+        st = load_stack(os.path.join(GOLD, s["manifest"]), device=True)
         assert st.on_device and st.slices.is_cuda
         assert _bits_equal(st.slices.cpu().numpy(), blob[f"{s['name']}/slices"]), s["name"]
         host = load_stack(os.path.join(GOLD, s["manifest"]), device=False)
@@ -146,7 +146,7 @@ def test_formats_around_the_path(cuda, tmp_path):
     from oracle import kriging_oracle as O
     from paper_2303_09523_b200 import VolumeGrid, ZPartKriging, load_stack, load_volume, save_volume
     blob = np.load(os.path.join(GOLD, "reference_stack.npz"))
-    st = load_stack(os.path.join(GOLD, "stack", "u8_L", "stack.manifest"))
+    st = load_stack(os.path.join(GOLD, "stack", "u8_L", "stack.manifest"), device=True)
     assert st.factor == 3 and st.output_depth() == 10
     zk = ZPartKriging(st.n, st.height, st.width, st.factor, 1)
     vol, _ = zk.run(st.slices)
@@ -155,5 +155,5 @@ def test_formats_around_the_path(cuda, tmp_path):
     assert np.abs(vol.cpu().numpy().astype(np.float64) - ref).max() <= 1e-6 * 1.0   # normalised range is 1
     path = tmp_path / "out.vkv"
     save_volume(VolumeGrid(vol), path)
-    back = load_volume(path)
+    back = load_volume(path, device=True)
     assert _bits_equal(back.data.cpu().numpy(), vol.cpu().numpy()) and not bool(back.missing_mask.any())

@@ -78,7 +78,7 @@ def test_crc_corruption_detected(cuda, tmp_path):
         p = tmp_path / f"bad{pos}.vkv"
         p.write_bytes(bytes(c))
         with pytest.raises(ChecksumMismatch):
-            load_volume(p)
+            load_volume(p, device=True)
 
 
 def test_large_round_trip(cuda, tmp_path):
@@ -93,7 +93,7 @@ def test_large_round_trip(cuda, tmp_path):
     save_volume(VolumeGrid(torch.from_numpy(d).cuda(), torch.from_numpy(m).cuda(), (3, 2, 1)), p)
     raw = p.read_bytes()
     assert zlib.crc32(raw[:-4]) == int.from_bytes(raw[-4:], "little")
-    v = load_volume(p)
+    v = load_volume(p, device=True)
     assert torch.equal(v.missing_mask.cpu(), torch.from_numpy(m))
     assert np.array_equal(v.data.cpu().numpy(), d, equal_nan=True)
 
