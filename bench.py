@@ -143,12 +143,12 @@ def _cpu_worker(args):
     os.environ["OMP_NUM_THREADS"] = "1"
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle import kriging_oracle as O
-    slices, b, e, factor = args
-    out, _, _ = O.reconstruct_zpart(slices, b, e, factor)
+    slices, b, e, factor, drift = args
+    out, _, _ = O.reconstruct_zpart(slices, b, e, factor, drift=drift)
     return out.shape[0]
 
 
-def cpu_reference_sample(ks, factor, n_parts, cores, pool=None, n_sample=None):
+def cpu_reference_sample(ks, factor, n_parts, cores, pool=None, n_sample=None, drift="linear"):
     """Run the reference algorithm on a bounded sample of sub-parts with a
     process pool; returns (voxels, seconds, sample description)."""
     from oracle import kriging_oracle as O
@@ -157,7 +157,7 @@ def cpu_reference_sample(ks, factor, n_parts, cores, pool=None, n_sample=None):
     sel = ranges[:n_sample]
     H, W = ks.shape[1:]
     vox = sum((e - b) * (factor - 1) * H * W for b, e in sel)
-    jobs = [(ks[b:e + 1].copy(), 0, e - b, factor) for b, e in sel]
+    jobs = [(ks[b:e + 1].copy(), 0, e - b, factor, drift) for b, e in sel]
     t0 = time.perf_counter()
     if pool is None:
         for j in jobs:
@@ -184,12 +184,14 @@ def run_reference(args, cfg, ks):
     cores = _host_cores()
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        pool.map(_cpu_worker, [(ks[:2].copy(), 0, 1, cfg.factor)] * cores)   # warm
+        pool.map(_cpu_worker, [(ks[:2].copy(), 0, 1, cfg.factor, args.drift)] * cores)   # warm
         for _ in range(args.warmup):
-            cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool, n_sample=min(cores, 4))
+            cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool, n_sample=min(cores, 4),
+                                 drift=args.drift)
         times, vox = [], 0
         for _ in range(args.steps):
-            v, dt, sample = cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool)
+            v, dt, sample = cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool,
+                                                 drift=args.drift)
             times.append(dt)
             vox = v
     ms = 1e3 * float(np.median(times))
@@ -222,13 +224,19 @@ def _l2_desc(cfg):
 
 
 def _config(cfg, args, world):
+    values = ("normalised to [0, 1] (non-integer floats: the 16-tap fp64 stencil path)"
+              if args.values == "normalized" else
+              f"{cfg.quantise} grey levels as float32 (integer-valued: the x<->y symmetric fp64 rows)"
+              if cfg.quantise in ("u8", "u12") else "float32 in [0, 1]")
     return {"workload": f"{cfg.name} {cfg.height}x{cfg.width}, K={cfg.n_known} known slices/GPU, "
                         f"factor {cfg.factor}, {cfg.n_subparts} Z sub-parts/GPU",
-            "kind": "exponential", "drift": "linear", "accum": args.accum,
+            "kind": "exponential", "drift": args.drift, "accum": args.accum,
             "return_variance": bool(args.variance), "max_pairs": 100000, "seed": 0,
+            "input_values": values,
             "parallelism": f"zparts x {world} GPU (weak, 1-slice NCCL halo)",
             "l2": _l2_desc(cfg),
-            "pair_draws": "redrawn every step"}
+            "pair_draws": "redrawn every step",
+            "fit": "device TRF reproducing scipy's fit bit for bit (tests/test_gpu_fit_parity.py)"}
 
 
 # --------------------------------------------------------------------------
@@ -247,6 +255,9 @@ def run_gpu(args, cfg, ks):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        # communicator set-up lines on stderr (nranks / transport per rank)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -254,13 +265,14 @@ def run_gpu(args, cfg, ks):
     has_halo = rank < world - 1
     K_loc = cfg.n_known + int(has_halo)
     H, W, f = cfg.height, cfg.width, cfg.factor
-    zk = ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, redraw_pairs=not os.environ.get("VK_DIAG_NO_REDRAW"),
+    zk = ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, drift=args.drift,
+                      redraw_pairs=not os.environ.get("VK_DIAG_NO_REDRAW"),
                       part_len=cfg.n_known // cfg.n_subparts, overlap=not args.serial)
     # per-stage / per-kernel times come from the serial schedule (one launch
     # per stage on one stream); the default chained schedule interleaves them
     zs = zk if args.serial else ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum,
-                                             redraw_pairs=True, part_len=cfg.n_known // cfg.n_subparts,
-                                             overlap=False)
+                                             drift=args.drift, redraw_pairs=True,
+                                             part_len=cfg.n_known // cfg.n_subparts, overlap=False)
     zs.plan.set_timing(max(1, args.steps))
     stack = torch.empty((K_loc, H, W), dtype=torch.float32, device=dev)
     stack[:cfg.n_known].copy_(owned)
@@ -362,32 +374,127 @@ def run_gpu(args, cfg, ks):
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, ks, stream, rank, world, dev)
 
+    # strong scaling: ONE volume (the base config's K slices) split over the
+    # ranks by Z sub-parts, halo over the C-ABI NCCL communicator inside the
+    # step; the gather of the core planes to rank 0 timed separately
+    strong = None
+    if world > 1 or args.scaling == "strong":
+        strong = run_strong(args, rank, world, dev, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing as mp
         cores = _host_cores()
         with mp.get_context("fork").Pool(cores) as pool:
-            pool.map(_cpu_worker, [(ks[:2].copy(), 0, 1, cfg.factor)] * cores)
-            v, dt, sample = cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool)
+            pool.map(_cpu_worker, [(ks[:2].copy(), 0, 1, cfg.factor, args.drift)] * cores)
+            v, dt, sample = cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool,
+                                                 drift=args.drift)
         cpu = {"value": v / dt, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
 
+    scaling = "weak"
+    if args.scaling == "strong":
+        scaling, value, ms_step = "strong", strong["value"], strong["ms_per_step"]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": DTYPES[args.accum],
             "data": _data_desc(cfg),
             "config": _config(cfg, args, world),
             "schedule": "serial" if args.serial else "per-part fit->solve->predict chains",
             "roofline": roof, "stage_ms_serial": stages, "cpu_baseline": cpu, "e2e": e2e,
-            "pipelined": pipelined,
+            "pipelined": pipelined, "strong": strong,
             "gpu_launches": kpe * args.steps, "clocks": clk.summary(),
         }
+        if scaling == "strong":
+            line["config"]["parallelism"] = (f"one {cfg.n_known}-slice volume split over {world} GPU by Z "
+                                             f"sub-parts (strong, 1-slice NCCL halo)")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_strong(args, rank, world, dev, stream):
+    """Strong scaling of the same metric: the base config's stack split by Z
+    sub-parts (zshard.strong_shard: rank r owns parts [r S/N, (r+1) S/N) and
+    receives the next rank's first slice), the halo exchanged on the plan's
+    stream through the C ABI's NCCL communicator (vk_halo_exchange) inside
+    every timed step.  Device time per step, max over ranks; the gather of
+    every rank's core planes to rank 0 (vk_gather_core) is timed on its own."""
+    import torch
+    import torch.distributed as dist
+    from paper_2303_09523_b200 import ZPartKriging
+    from paper_2303_09523_b200.phantoms import CONFIGS, phantom_planes
+    from paper_2303_09523_b200.zshard import NativeComm, core_planes, strong_shard
+    base = CONFIGS[args.config]
+    K, H, W, f, S = base.n_known, base.height, base.width, base.factor, base.n_subparts
+    sh = strong_shard(K, S, rank, world)
+    own = sh.k1 - sh.k0 + 1
+    stack = torch.empty((sh.n_local, H, W), dtype=torch.float32, device=dev)
+    stack[:own].copy_(torch.from_numpy(_values(args, base, phantom_planes(base, base.known_z[sh.k0:sh.k1 + 1]))))
+    comm = NativeComm(rank, world) if world > 1 else None
+    zk = ZPartKriging(sh.n_local, H, W, f, sh.n_parts, accum=args.accum, drift=args.drift,
+                      redraw_pairs=True, part_len=sh.part_len)
+    out, var = zk.allocate(bool(args.variance))
+
+    def step():
+        if comm is not None:
+            comm.halo(stack[0], out=stack[own] if sh.has_halo else None, stream=stream)
+        zk.run(stack, out, var)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    zk.finish()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    zk.finish()
+    ms = e0.elapsed_time(e1) / args.steps
+    core = core_planes(out, f, sh.has_halo).reshape(-1)
+    gather_ms = None
+    if comm is not None:
+        counts = [None] * world
+        dist.all_gather_object(counts, int(core.numel()))
+        comm.gather(core, counts, stream=stream)               # warm
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        comm.gather(core, counts, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = e0.elapsed_time(e1)
+        t = torch.tensor([ms, gather_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, gather_ms = float(t[0].item()), float(t[1].item())
+        comm.close()
+    vox = (K - 1) * (f - 1) * H * W
+    res = {"value": vox / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": args.steps,
+           "volume": f"{base.name}: K={K}, {S} sub-parts in total, {sh.n_parts} per GPU",
+           "halo": "vk_halo_exchange (C-ABI NCCL send/recv) inside the step"}
+    if gather_ms is not None:
+        res.update({"gather_ms": gather_ms, "gather_to_rank0_gbs": (((K - 1) * f + 1) * H * W * 4
+                                                                    - int(core.numel()) * 4) / (gather_ms / 1e3) / 1e9,
+                    "gather": "vk_gather_core: every rank's core planes into rank 0's volume (timed alone)"})
+    return res
+
+
+def _values(args, cfg, planes):
+    """--values normalized: the stack rescaled to [0, 1] floats (as the
+    reference pipeline's normalize_stack would feed it), which takes the
+    16-tap fp64 stencil rows instead of the integer-only symmetric rows."""
+    if args.values != "normalized":
+        return planes
+    hi = {"u8": 255.0, "u12": 4095.0}.get(cfg.quantise, 1.0)
+    return (planes / np.float32(hi)).astype(np.float32)
 
 
 def run_pipelined(args, cfg, stack, K_loc, rank, world, dev, stream):
@@ -399,8 +506,8 @@ def run_pipelined(args, cfg, stack, K_loc, rank, world, dev, stream):
     from paper_2303_09523_b200 import ZPartKriging
     H, W, f = cfg.height, cfg.width, cfg.factor
     streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
-    plans = [ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, redraw_pairs=True,
-                          part_len=cfg.n_known // cfg.n_subparts) for _ in range(2)]
+    plans = [ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, drift=args.drift,
+                          redraw_pairs=True, part_len=cfg.n_known // cfg.n_subparts) for _ in range(2)]
     stacks = [stack.clone() for _ in range(2)]
     outs = [p.allocate(bool(args.variance)) for p in plans]
     ev_start = torch.cuda.Event()
@@ -466,7 +573,7 @@ def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):
     host_in = [torch.empty((K_loc, H, W), dtype=torch.float32).pin_memory() for _ in range(2)]
     for h in host_in:
         h[:K].copy_(torch.from_numpy(ks))
-    zk1 = ZPartKriging(K_loc, H, W, cfg.factor, cfg.n_subparts, accum=args.accum,
+    zk1 = ZPartKriging(K_loc, H, W, cfg.factor, cfg.n_subparts, accum=args.accum, drift=args.drift,
                        redraw_pairs=True, part_len=K // cfg.n_subparts)
     dev_in = [torch.empty((K_loc, H, W), dtype=torch.float32, device=dev or "cuda") for _ in range(2)]
     bufs = [zk1.allocate(bool(args.variance)) for _ in range(2)]
@@ -567,6 +674,12 @@ def main(argv=None):
     ap.add_argument("--config", default="C4")
     ap.add_argument("--accum", default="fp64", choices=["fp64", "fp32", "fixed"])
     ap.add_argument("--variance", action="store_true")
+    ap.add_argument("--drift", default="linear", choices=["linear", "constant"])
+    ap.add_argument("--values", default="native", choices=["native", "normalized"],
+                    help="normalized: the stack rescaled to [0, 1] (non-integer input)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak (default): every GPU owns a C4-sized stack; strong: one stack split "
+                         "over the GPUs (also reported beside the weak value when N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipelined", action="store_true")
@@ -575,6 +688,8 @@ def main(argv=None):
                          "default per-part chains")
     args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        return _launch_ranks(args, sys.argv[1:] if argv is None else list(argv))
 
     from paper_2303_09523_b200.phantoms import CONFIGS, known_slices
     import dataclasses
@@ -584,8 +699,26 @@ def main(argv=None):
     if args.impl == "reference":
         if rank != 0:
             return 0
-        return run_reference(args, base, known_slices(base))
-    return run_gpu(args, cfg, known_slices(cfg))
+        return run_reference(args, base, _values(args, base, known_slices(base)))
+    return run_gpu(args, cfg, _values(args, cfg, known_slices(cfg)))
+
+
+def _launch_ranks(args, argv):
+    """``--gpus N`` outside torchrun: launch the N ranks here (one process per
+    GPU, torch.distributed.run on 127.0.0.1), failing loudly when fewer GPUs
+    are visible."""
+    import socket
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but only {n} GPU(s) visible"}), flush=True)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

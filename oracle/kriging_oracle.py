@@ -337,6 +337,7 @@ def fill_missing(data, mask, model: Model, drift="linear",
     dz, dy, dx = data.shape
     known_z = np.nonzero(~flags)[0]
     cache: dict[bytes, tuple] = {}
+    border_cache: dict[tuple, tuple] = {}
 
     def weights(rel):
         key = rel.astype(np.int16).tobytes()
@@ -365,24 +366,33 @@ def fill_missing(data, mask, model: Model, drift="linear",
             out[z, 1:dy - 2, 1:dx - 2] = acc
             if var is not None:
                 var[z, 1:dy - 2, 1:dx - 2] = v
-        # border voxels, clamped windows -- kriging.py:531-557
-        for y in range(dy):
+            border = [(y, x) for y in range(dy) for x in range(dx)
+                      if not (1 <= y <= dy - 3 and 1 <= x <= dx - 3)]
+        else:
+            border = [(y, x) for y in range(dy) for x in range(dx)]
+        # border voxels, clamped windows -- kriging.py:531-557: the solved
+        # stencil of each (plane offsets, clamped window) is looked up by that
+        # key, as the reference's border_cache does (the same weights as a
+        # rebuilt offset list: the key determines the list)
+        dz_key = tuple(offs)
+        for (y, x) in border:
+            xlo, xhi = window(x, 4, dx)
             ylo, yhi = window(y, 4, dy)
-            inner_row = interior and 1 <= y <= dy - 3
-            for x in range(dx):
-                if inner_row and 1 <= x <= dx - 3:
-                    continue
-                xlo, xhi = window(x, 4, dx)
+            key = (dz_key, xlo - x, xhi - x, ylo - y, yhi - y)
+            hit = border_cache.get(key)
+            if hit is None:
                 rel = np.array([(ox - x, oy - y, oz) for oz in offs
                                 for oy in range(ylo, yhi)
                                 for ox in range(xlo, xhi)], dtype=np.int64)
-                w, v = weights(rel)
-                vals = np.concatenate([data[z + oz, ylo:yhi, xlo:xhi].ravel()
-                                       for oz in offs])
-                pred = float(w @ vals)
-                out[z, y, x] = min(max(pred, lo), hi)
-                if var is not None:
-                    var[z, y, x] = v
+                hit = weights(rel)
+                border_cache[key] = hit
+            w, v = hit
+            vals = np.concatenate([data[z + oz, ylo:yhi, xlo:xhi].ravel()
+                                   for oz in offs])
+            pred = float(w @ vals)
+            out[z, y, x] = min(max(pred, lo), hi)
+            if var is not None:
+                var[z, y, x] = v
     return out, var
 
 
