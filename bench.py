@@ -498,26 +498,30 @@ def _values(args, cfg, planes):
 
 
 def run_pipelined(args, cfg, stack, K_loc, rank, world, dev, stream):
-    """Device throughput with consecutive steps overlapped: two plans (each
-    with its own workspace, output volume and input copy) alternate on two
-    streams.  Device time over K steps, max over ranks."""
+    """Device throughput with consecutive steps overlapped: ``--depth`` plans
+    (each with its own workspace, output volume and input copy) take steps in
+    turn on their own streams, so a step's statistics, fits and solves run
+    while earlier steps stream their predictions.  Device time over K steps,
+    max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2303_09523_b200 import ZPartKriging
     H, W, f = cfg.height, cfg.width, cfg.factor
-    streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    depth = max(1, args.depth)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(depth)]
     plans = [ZPartKriging(K_loc, H, W, f, cfg.n_subparts, accum=args.accum, drift=args.drift,
-                          redraw_pairs=True, part_len=cfg.n_known // cfg.n_subparts) for _ in range(2)]
-    stacks = [stack.clone() for _ in range(2)]
+                          redraw_pairs=True, part_len=cfg.n_known // cfg.n_subparts,
+                          overlap=args.pipe_chains) for _ in range(depth)]
+    stacks = [stack.clone() for _ in range(depth)]
     outs = [p.allocate(bool(args.variance)) for p in plans]
     ev_start = torch.cuda.Event()
 
     def step(i):
-        b = i % 2
+        b = i % depth
         with torch.cuda.stream(streams[b]):
             plans[b].run(stacks[b], *outs[b])
 
-    for i in range(4):
+    for i in range(2 * depth):
         step(i)
     torch.cuda.synchronize()
     for p in plans:
@@ -548,8 +552,10 @@ def run_pipelined(args, cfg, stack, K_loc, rank, world, dev, stream):
         ms = float(t.item())
     vox = float(plans[0].interpolated_voxels) * world
     return {"value": vox / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": args.steps,
-            "scheme": "2 plans x 2 streams: step i+1's stats/pairs/bins/fits/solves overlap step i's "
-                      "prediction; every step runs the whole path (no halo exchange in this loop)"}
+            "depth": depth, "plan_schedule": "per-part chains" if args.pipe_chains else "stage order",
+            "scheme": f"{depth} plans x {depth} streams in turn: a step's stats/pairs/bins/fits/solves "
+                      "overlap earlier steps' predictions; every step runs the whole path "
+                      "(no halo exchange in this loop)"}
 
 
 def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):
@@ -683,6 +689,10 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipelined", action="store_true")
+    ap.add_argument("--depth", type=int, default=4, help="plans in flight for the pipelined figure")
+    ap.add_argument("--pipe-chains", action="store_true",
+                    help="pipelined figure with the per-part chain schedule inside each plan "
+                         "(default: each plan's stages in launch order on its own stream)")
     ap.add_argument("--serial", action="store_true",
                     help="time the serial schedule (one launch per stage) instead of the "
                          "default per-part chains")

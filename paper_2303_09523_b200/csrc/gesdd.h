@@ -139,8 +139,10 @@ VK_HD Ext ext_add(Ext a, Ext b) {
   return ext_round_frac(m, f2, a.e + 1);
 }
 
-// fsqrt (correctly rounded to 64 bits) then fstpl (rounded to double)
-VK_HD double ext_sqrt_to_double(Ext a) {
+// fsqrt (correctly rounded to 64 bits) then fstpl (rounded to double), by
+// exact integer square root -- the reference form, and the fallback of
+// ext_sqrt_to_double near a rounding boundary
+VK_HD double ext_sqrt_exact(Ext a) {
   if (a.m == 0) return 0.0;
   unsigned __int128 M;
   int re;
@@ -176,6 +178,42 @@ VK_HD double ext_sqrt_to_double(Ext a) {
   const uint64_t rem = r & 0x7ff;
   if (rem > 0x400 || (rem == 0x400 && (q & 1))) q += 1;
   return ldexp((double)q, re + 11);
+}
+
+// fsqrt then fstpl, fast form: S = F 2^E with F in [1, 4) (E even) as an
+// exact double pair Fh + Fl; y = sqrt(Fh) rounded, one Newton correction
+// d = (Fh - y^2 + Fl) / 2y (Fh - y^2 exact by FMA) gives sqrt(S) to ~2^-103
+// absolute, i.e. the offset t = d / 2^-63 from y on the 64-bit grid to ~2^-40;
+// t rounds to the 64-bit result unless it lies within 2^-30 of a half (then
+// the exact integer form decides), and the 64-bit result rounds to 53 bits by
+// integer arithmetic on t (ties to even).
+VK_HD double ext_sqrt_to_double(Ext a) {
+  if (a.m == 0) return 0.0;
+  int E = a.e + 63;
+  double Fh = (double)(a.m & ~0x7ffull) * 0x1p-63;       // exact: 53 significant bits
+  double Fl = (double)(a.m & 0x7ffull) * 0x1p-63;        // exact: 11 bits
+  if (E & 1) { Fh *= 2.0; Fl *= 2.0; E -= 1; }
+  const double y = sqrt_(Fh);                            // in [1, 2]
+  if (!(y < 2.0)) return ext_sqrt_exact(a);
+  const double e1 = fma_(-y, y, Fh);                     // exact residual
+  const double R = add(e1, Fl);
+#if defined(__CUDA_ARCH__)
+  const double half_inv = 0.5 * __drcp_rn(y);
+#else
+  const double half_inv = 0.5 / y;
+#endif
+  const double t = mul(R, half_inv) * 0x1p63;             // offset in units of 2^-63
+  const double n = rint(t);
+  if (fabs(fabs(t - n) - 0.5) < 0x1p-30) return ext_sqrt_exact(a);
+  // 53-bit rounding of y + n 2^-63: y's ulp is 2^-52 = 2^11 units
+  const long long ni = (long long)n;
+  long long q0 = ni >> 11;                               // floor(n / 2048)
+  const long long r = ni - (q0 << 11);                   // 0 .. 2047
+  const long long ymant = (long long)(dbits(y) & 0xfffffffffffffull);
+  long long q = q0;
+  if (r > 1024 || (r == 1024 && ((ymant + q0) & 1))) q = q0 + 1;
+  const double res = y + (double)q * 0x1p-52;            // exact: a few ulps of y
+  return scalbn(res, E / 2);
 }
 
 // OpenBLAS dnrm2 (interface: n == 1 -> |x|; kernel dnrm2_k SKYLAKEX, x87)

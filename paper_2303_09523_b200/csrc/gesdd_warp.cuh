@@ -64,7 +64,9 @@ __device__ void dscal_warp(int n, double a, double* x, int lane) {
 // dlarfg(n, alpha, x, 1, tau) with alpha and x in shared memory
 __device__ void dlarfg_warp(int n, double* alpha, double* x, double* tau, SvdWarpSmem& sm, int lane) {
   if (n <= 1) { *tau = 0.0; return; }
+  VK_TP(tn);
   double xnorm = dnrm2_warp(n - 1, x, sm, lane);
+  VK_TACC(14, tn);
   if (xnorm == 0.0) { *tau = 0.0; return; }
   double a = *alpha;
   double beta = -fsign(dlapy2(a, xnorm), a);
@@ -171,7 +173,9 @@ __device__ int svd_m3_warp(const double* A_rm, int M, double* U_rm, double* s, d
       __syncwarp();
       if (lane == 0) A[i + i * M] = 1.0;
       __syncwarp();
+      VK_TP(tl);
       dlarf_left_warp(M - i, N - i - 1, &A[i + i * M], tau[i], &A[i + (i + 1) * M], M, lane);
+      VK_TACC(15, tl);
       if (lane == 0) A[i + i * M] = aii;
       __syncwarp();
     }

@@ -20,6 +20,7 @@ tot = buf[5]
 for i, n in enumerate(names):
     if i < 6: print(f"{n:10s} {buf[i]/1e6:10.2f} Mcycles ({100*buf[i]/tot:5.1f}%)")
     else: print(f"{n:10s} {buf[i]}")
-for i, n in zip(range(8, 14), ["svd dgeqr2", "svd dorg2r", "svd dormbr x2", "svd dgemm+out", "svd dgebd2", "svd dbdsdc"]):
+for i, n in zip(range(8, 16), ["svd dgeqr2", "svd dorg2r", "svd dormbr x2", "svd dgemm+out", "svd dgebd2", "svd dbdsdc",
+                               "  dnrm2 (warp)", "  dgeqr2 dlarf"]):
     print(f"{n:14s} {buf[i]/1e6:10.2f} Mcycles ({100*buf[i]/tot:5.1f}%)")
 print(f"cycles per iteration {tot/buf[6]:.0f} (summed over {cfg.n_subparts} parts)")
