@@ -33,8 +33,8 @@ VK_HD double mul(double a, double b) { return __dmul_rn(a, b); }
 VK_HD double add(double a, double b) { return __dadd_rn(a, b); }
 VK_HD double sub(double a, double b) { return __dsub_rn(a, b); }
 VK_HD double div(double a, double b) { return __ddiv_rn(a, b); }
-VK_HD double fma_(double a, double b, double c) { return __fma_rn(a, b, c); }
 VK_HD double sqrt_(double a) { return __dsqrt_rn(a); }
+VK_HD double fma_(double a, double b, double c) { return __fma_rn(a, b, c); }
 #else
 VK_HD double mul(double a, double b) { return a * b; }
 VK_HD double add(double a, double b) { return a + b; }

@@ -346,6 +346,7 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
       VK_TRY(p->alloc(&t.hbits, (size_t)1));
       VK_TRY(p->alloc(&t.order, (size_t)d->max_pairs));
       VK_TRY(p->alloc(&t.boff, (size_t)MAX_BINS + 1));
+      VK_TRY(p->alloc(&t.ocnt, (size_t)order_chunks(d->max_pairs) * MAX_BINS));
       p->tables.push_back(t);
       // numpy's pairwise-summation tree for this class's sample count
       const NpSumTreeHost th = build_npsum_tree(g.pair_classes[c].m);
@@ -1160,6 +1161,7 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   t.hbits = (unsigned long long*)get(8);
   t.order = (int32_t*)get((size_t)npmax * 4);
   t.boff = (int32_t*)get((MAX_BINS + 1) * 4);
+  t.ocnt = (int32_t*)get((size_t)order_chunks(npmax) * MAX_BINS * 4);
   PairTable* d_t = (PairTable*)get(sizeof(PairTable));
   ChunkStat* stats = (ChunkStat*)get((size_t)nchunk * sizeof(ChunkStat));
   double* partial = (double*)get((size_t)nblk * n_bins * 8);

@@ -28,6 +28,7 @@ struct PairTable {                   // one per pair class (device pointers)
   // pairs sorted by bin, stable (launch_pair_order; nullptr: not kept)
   int32_t* order = nullptr;          // [npairs]
   int32_t* boff = nullptr;           // [n_bins + 1]
+  int32_t* ocnt = nullptr;           // [order_chunks(npairs) * MAX_BINS] scratch of the sort
 };
 // number of draw threads (= scratch entries) for a pair class
 int64_t pair_scratch_elems(int64_t m, int64_t max_pairs);
@@ -99,6 +100,7 @@ struct NpVarArgs {
 };
 cudaError_t launch_npvar(const NpVarArgs& a, cudaStream_t st);
 // stable sort of each class's pairs by bin (tables with order != nullptr)
+inline int64_t order_chunks(int64_t npairs) { return (npairs + 2047) / 2048; }
 cudaError_t launch_pair_order(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st);
 // bsum[s][b] = np.bincount(which, weights=0.5*(v_i - v_j)^2)[b] of part s
 struct BinSumArgs {

@@ -41,45 +41,73 @@ __device__ __forceinline__ double npv(const float* __restrict__ known, const dou
   return __dmul_rn(t, t);
 }
 
-// eight lanes per leaf (lane k holds numpy's accumulator r[k]), four leaves
-// per warp
+// A CTA sums LEAF_CTA consecutive leaves (<= 128 elements each): their
+// contiguous element range is staged in shared memory with 128-bit loads (all
+// independent, so the loads of a CTA are in flight together), then eight
+// lanes per leaf (lane k holds numpy's accumulator r[k]) add it in numpy's
+// order.
+constexpr int LEAF_CTA = 64;
+
 template <int MODE>
 __global__ void __launch_bounds__(256) npsum_leaf_kernel(NpVarArgs a) {
   const int s = a.part0 + blockIdx.y;
   const NpSumTree T = a.trees[a.part_class[s]];
-  const int leaf = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-  const int k = threadIdx.x & 7;
-  const bool act = leaf < T.nleaf;
+  const int l0 = blockIdx.x * LEAF_CTA;
+  if (l0 >= T.nleaf) return;
+  const int l1 = min(T.nleaf, l0 + LEAF_CTA);
   const int64_t base = a.part_base[s];
-  const double mean = MODE ? a.mean[s] : 0.0;
-  double r = 0.0;
-  int64_t o = 0, n = 0, n8 = 0;
-  if (act) {
-    o = T.leaf_off[leaf];
-    n = T.leaf_off[leaf + 1] - o;
-    n8 = n - n % 8;
-    if (n >= 8) {
-      r = npv<MODE>(a.known, a.values, base + o + k, mean);
-#pragma unroll 4
-      for (int64_t i = 8; i < n8; i += 8) r = __dadd_rn(r, npv<MODE>(a.known, a.values, base + o + i + k, mean));
-    }
+  const int64_t e0 = T.leaf_off[l0], e1 = T.leaf_off[l1];
+  __shared__ __align__(16) float stage[LEAF_CTA * 128 + 4];
+  // stage elements [e0, e1) of the part (absolute index base + e)
+  const int64_t g0 = base + e0, g1 = base + e1;
+  const bool vec = ((uintptr_t)a.known & 15) == 0;
+  const int64_t a0 = vec ? (g0 & ~(int64_t)3) : g0;     // 16-byte aligned start
+  if (!a.values) {                                      // explicit float64 samples are read directly
+    const int n = (int)(g1 - a0);
+    const int n4 = vec ? n >> 2 : 0;
+    const float4* src = reinterpret_cast<const float4*>(a.known + a0);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<float4*>(stage)[i] = __ldg(src + i);
+    for (int i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) stage[i] = __ldg(a.known + a0 + i);
   }
-  // res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
-  const unsigned full = 0xffffffffu;
-  double t = __shfl_down_sync(full, r, 1);
-  r = __dadd_rn(r, t);
-  t = __shfl_down_sync(full, r, 2);
-  r = __dadd_rn(r, t);
-  t = __shfl_down_sync(full, r, 4);
-  r = __dadd_rn(r, t);
-  if (act && k == 0) {
-    double res = r;
-    if (n < 8) {                                    // whole array below 8 (not reached: m >= 9)
-      res = -0.0;
-      n8 = 0;
+  __syncthreads();
+  const int shift = (int)(g0 - a0);                     // stage[j + shift] = element e0 + j
+  const double mean = MODE ? a.mean[s] : 0.0;
+  auto val = [&](int64_t e) -> double {                 // element e of the part (e0 <= e < e1)
+    const double v = a.values ? a.values[base + e] : (double)stage[(int)(e - e0) + shift];
+    if (MODE == 0) return v;
+    const double t = __dsub_rn(v, mean);
+    return __dmul_rn(t, t);
+  };
+  const int k = threadIdx.x & 7;
+  for (int leaf = l0 + (threadIdx.x >> 3); leaf < l0 + LEAF_CTA; leaf += blockDim.x >> 3) {
+    const bool act = leaf < l1;
+    double r = 0.0;
+    int64_t o = 0, n = 0, n8 = 0;
+    if (act) {
+      o = T.leaf_off[leaf];
+      n = T.leaf_off[leaf + 1] - o;
+      n8 = n - n % 8;
+      if (n >= 8) {
+        r = val(o + k);
+        for (int64_t i = 8; i < n8; i += 8) r = __dadd_rn(r, val(o + i + k));
+      }
     }
-    for (int64_t i = n8; i < n; ++i) res = __dadd_rn(res, npv<MODE>(a.known, a.values, base + o + i, mean));
-    a.leaf[(int64_t)s * a.leaf_stride + leaf] = res;
+    // res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
+    double t = __shfl_down_sync(0xffffffffu, r, 1);
+    r = __dadd_rn(r, t);
+    t = __shfl_down_sync(0xffffffffu, r, 2);
+    r = __dadd_rn(r, t);
+    t = __shfl_down_sync(0xffffffffu, r, 4);
+    r = __dadd_rn(r, t);
+    if (act && k == 0) {
+      double res = r;
+      if (n < 8) {                                  // whole array below 8 (not reached: m >= 9)
+        res = -0.0;
+        n8 = 0;
+      }
+      for (int64_t i = n8; i < n; ++i) res = __dadd_rn(res, val(o + i));
+      a.leaf[(int64_t)s * a.leaf_stride + leaf] = res;
+    }
   }
 }
 
@@ -108,55 +136,72 @@ __global__ void __launch_bounds__(1024) npsum_tree_kernel(NpVarArgs a) {
 }
 
 // ---- bins -------------------------------------------------------------------
-// stable counting sort of a class's pairs by bin: order[boff[b] + rank] = k
-__global__ void __launch_bounds__(1024) pair_order_kernel(const PairJob* jobs) {
-  const PairJob& J = jobs[blockIdx.x];
+// stable counting sort of a class's pairs by bin: order[boff[b] + rank] = k.
+// Chunks of ORD_CHUNK consecutive pairs per CTA: pass 1 counts each chunk's
+// bins, pass 2 offsets every chunk by boff (from the draw's bin counts) plus
+// the earlier chunks' counts and ranks its pairs in order -- inside a warp
+// with __match_any_sync, across the chunk's warps and rounds by running
+// per-bin counters.
+constexpr int ORD_CHUNK = 2048;
+
+__global__ void __launch_bounds__(256) pair_order_count_kernel(const PairJob* jobs) {
+  const PairJob& J = jobs[blockIdx.y];
   if (!J.t.order) return;
-  extern __shared__ int cnt[];                      // [n_bins][1024]
-  __shared__ int tot[MAX_BINS + 1];
+  const int64_t c0 = (int64_t)blockIdx.x * ORD_CHUNK;
+  if (c0 >= J.npairs) return;
+  __shared__ int cnt[MAX_BINS];
+  if (threadIdx.x < MAX_BINS) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t c1 = min(J.npairs, c0 + ORD_CHUNK);
+  for (int64_t k = c0 + threadIdx.x; k < c1; k += blockDim.x) {
+    const int bb = J.t.bin[k];
+    if (bb != 255) atomicAdd(&cnt[bb], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < J.n_bins) J.t.ocnt[blockIdx.x * MAX_BINS + threadIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(256) pair_order_kernel(const PairJob* jobs) {
+  const PairJob& J = jobs[blockIdx.y];
+  if (!J.t.order) return;
+  const int64_t c0 = (int64_t)blockIdx.x * ORD_CHUNK;
+  if (c0 >= J.npairs) return;
+  __shared__ int base[MAX_BINS];
+  __shared__ int wcnt[8][MAX_BINS + 1];
   const int nb = J.n_bins, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t np_ = J.npairs;
-  const int64_t per = (np_ + 1023) / 1024;
-  const int64_t b0 = min(np_, (int64_t)tid * per), b1 = min(np_, b0 + per);
-  for (int b = 0; b < nb; ++b) cnt[b * 1024 + tid] = 0;
-  for (int64_t k = b0; k < b1; ++k) {
-    const int bb = J.t.bin[k];
-    if (bb != 255) cnt[bb * 1024 + tid] += 1;
-  }
-  __syncthreads();
-  // per-bin exclusive scan over the 1024 threads: warp w scans bin w
-  for (int b = warp; b < nb; b += 32) {
-    int run = 0;
-    for (int c = 0; c < 1024; c += 32) {
-      const int v = cnt[b * 1024 + c + lane];
-      int incl = v;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-      }
-      cnt[b * 1024 + c + lane] = run + incl - v;
-      run += __shfl_sync(0xffffffffu, incl, 31);
+  if (tid < nb) {
+    int acc = 0;                                          // boff[tid] + earlier chunks
+    for (int b = 0; b < tid; ++b) acc += (int)J.t.counts[b];
+    for (int c = 0; c < (int)blockIdx.x; ++c) acc += J.t.ocnt[c * MAX_BINS + tid];
+    base[tid] = acc;
+    if (blockIdx.x == 0) {
+      J.t.boff[tid] = acc;
+      if (tid == nb - 1) J.t.boff[nb] = acc + (int)J.t.counts[tid];
     }
-    if (lane == 0) tot[b] = run;
   }
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int b = 0; b < nb; ++b) {
-      J.t.boff[b] = acc;
-      const int t = tot[b];
-      tot[b] = acc;
-      acc += t;
+  const int64_t c1 = min(J.npairs, c0 + ORD_CHUNK);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t r0 = c0; r0 < c1; r0 += 256) {
+    if (tid < 8 * (MAX_BINS + 1)) (&wcnt[0][0])[tid] = 0;
+    __syncthreads();
+    const int64_t k = r0 + tid;
+    const int bb = k < c1 ? (int)J.t.bin[k] : 255;
+    const unsigned same = __match_any_sync(0xffffffffu, bb);
+    const int wrank = __popc(same & lt);
+    if (bb != 255 && wrank == 0) wcnt[warp][bb] = __popc(same);
+    __syncthreads();
+    if (bb != 255) {
+      int before = base[bb] + wrank;
+      for (int w = 0; w < warp; ++w) before += wcnt[w][bb];
+      J.t.order[before] = (int32_t)k;
     }
-    J.t.boff[nb] = acc;
-  }
-  __syncthreads();
-  for (int64_t k = b0; k < b1; ++k) {
-    const int bb = J.t.bin[k];
-    if (bb == 255) continue;
-    const int slot = tot[bb] + cnt[bb * 1024 + tid];
-    cnt[bb * 1024 + tid] += 1;
-    J.t.order[slot] = (int32_t)k;
+    __syncthreads();
+    if (tid < nb) {
+      int c = 0;
+      for (int w = 0; w < 8; ++w) c += wcnt[w][tid];
+      base[tid] += c;
+    }
+    __syncthreads();
   }
 }
 
@@ -187,6 +232,31 @@ __global__ void __launch_bounds__(32) binsum_kernel(BinSumArgs a) {
   const PairTable t = a.tables[a.part_class[s]];
   const int q0 = t.boff[b], q1 = t.boff[b + 1];
   const double* x = a.sq + (int64_t)s * a.max_pairs;
+  // integer-valued data: every weight is a half-integer, and while the total
+  // stays below 2^51 every partial sum in any order is exact -- the
+  // lane-parallel sum then equals the sequential one bit for bit
+  {
+    double ps = 0.0;
+    bool ok = true;
+    for (int c = q0; c < q1 && ok; c += 256) {       // chunks of 8 per lane; float data stops early
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = c + lane + 32 * u;
+        const double v = q < q1 ? x[q] : 0.0;
+        const double t = 2.0 * v;
+        ok &= (t == rint(t));
+        ps += v;
+      }
+      ok = __all_sync(0xffffffffu, ok);
+    }
+    if (ok) {
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      if (ps < 0x1p51) {
+        if (lane == 0) a.bsum[(int64_t)s * a.n_bins + b] = ps;
+        return;
+      }
+    }
+  }
   __shared__ double buf[2][256];
   double v[8];
   auto fetch = [&](int q) {
@@ -235,7 +305,7 @@ __global__ void __launch_bounds__(32) binsum_kernel(BinSumArgs a) {
 
 cudaError_t launch_npvar(const NpVarArgs& a, cudaStream_t st) {
   if (a.n_parts <= 0) return cudaSuccess;
-  const dim3 lgrid((unsigned)((a.max_leaf * 8 + 255) / 256), (unsigned)a.n_parts);
+  const dim3 lgrid((unsigned)((a.max_leaf + LEAF_CTA - 1) / LEAF_CTA), (unsigned)a.n_parts);
   npsum_leaf_kernel<0><<<lgrid, 256, 0, st>>>(a);
   npsum_tree_kernel<0><<<a.n_parts, 1024, 0, st>>>(a);
   npsum_leaf_kernel<1><<<lgrid, 256, 0, st>>>(a);
@@ -244,19 +314,16 @@ cudaError_t launch_npvar(const NpVarArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_pair_order(const PairJob* d_jobs, const PairJob* h_jobs, int n_jobs, cudaStream_t st) {
-  int nb = 1;
   bool any = false;
+  int64_t mp = 1;
   for (int c = 0; c < n_jobs; ++c) {
-    nb = std::max(nb, h_jobs[c].n_bins);
     any |= h_jobs[c].t.order != nullptr;
+    mp = std::max(mp, h_jobs[c].npairs);
   }
   if (!any) return cudaSuccess;
-  const size_t smem = (size_t)nb * 1024 * sizeof(int);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(pair_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  pair_order_kernel<<<n_jobs, 1024, smem, st>>>(d_jobs);
+  const dim3 grid((unsigned)((mp + ORD_CHUNK - 1) / ORD_CHUNK), (unsigned)n_jobs);
+  pair_order_count_kernel<<<grid, 256, 0, st>>>(d_jobs);
+  pair_order_kernel<<<grid, 256, 0, st>>>(d_jobs);
   return cudaGetLastError();
 }
 
