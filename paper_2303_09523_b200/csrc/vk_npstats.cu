@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) pair_order_kernel(const PairJob* jobs) {
   const int64_t c1 = min(J.npairs, c0 + ORD_CHUNK);
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t r0 = c0; r0 < c1; r0 += 256) {
-    if (tid < 8 * (MAX_BINS + 1)) (&wcnt[0][0])[tid] = 0;
+    for (int t = tid; t < 8 * (MAX_BINS + 1); t += 256) (&wcnt[0][0])[t] = 0;
     __syncthreads();
     const int64_t k = r0 + tid;
     const int bb = k < c1 ? (int)J.t.bin[k] : 255;

@@ -160,6 +160,16 @@ __device__ __forceinline__ void st_cs_f1_if(float* p, float x, bool c) {
                ::"l"(p), "f"(x), "r"((unsigned)c) : "memory");
 }
 
+// predicated 128-bit streaming stores of two doubles (the variance volume)
+__device__ __forceinline__ void st_cs_d2_if(double* p, double x, double y, bool c) {
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %3, 0; @q st.global.cs.v2.f64 [%0], {%1, %2};}"
+               ::"l"(p), "d"(x), "d"(y), "r"((unsigned)c) : "memory");
+}
+__device__ __forceinline__ void st_cs_d1_if(double* p, double x, bool c) {
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.cs.f64 [%0], %1;}"
+               ::"l"(p), "d"(x), "r"((unsigned)c) : "memory");
+}
+
 template <int COLS>
 __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
   if constexpr (COLS == 4) {
@@ -410,9 +420,20 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
         st_cs_cols<COLS>(a.out + zk * P + pix, selfA);
         if (copy_b) st_cs_cols<COLS>(a.out + (zk + G + 1) * P + pix, selfB);
         if (VAR) {
-          for (int c = 0; c < COLS; ++c) a.var[zk * P + pix + c] = 0.0;
-          if (copy_b)
-            for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
+          // known planes: zero variance, 128-bit streaming stores (32-byte
+          // aligned: gx % 4 == 0 and W % 4 == 0 on the streaming path)
+          if constexpr (COLS == 4) {
+            double* v0 = a.var + zk * P + pix;
+            st_cs_d2_if(v0, 0.0, 0.0, true);
+            st_cs_d2_if(v0 + 2, 0.0, 0.0, true);
+            double* v1 = a.var + (zk + G + 1) * P + pix;
+            st_cs_d2_if(v1, 0.0, 0.0, copy_b);
+            st_cs_d2_if(v1 + 2, 0.0, 0.0, copy_b);
+          } else {
+            for (int c = 0; c < COLS; ++c) a.var[zk * P + pix + c] = 0.0;
+            if (copy_b)
+              for (int c = 0; c < COLS; ++c) a.var[(zk + G + 1) * P + pix + c] = 0.0;
+          }
         }
         float* dst = a.out + (zk + 1) * P + pix;
 #pragma unroll
@@ -420,7 +441,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           float o[COLS];
 #pragma unroll
           for (int c = 0; c < COLS; ++c) o[c] = fminf(fmaxf(out_of(j, c), lo), hi);
-          if constexpr (COLS == 4 && !VAR) {
+          if constexpr (COLS == 4) {
             // border columns (x = 0, W-2, W-1) belong to the border pass:
             // predicated stores, no divergent branch (groups at x = 0 and
             // x = W-4 hold them; W % 4 == 0 on the streaming path)
@@ -428,6 +449,14 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
             st_cs_f1_if(dst + 1, o[1], xb0);
             st_cs_f2_if(dst + 2, o[2], o[3], xb0);
             st_cs_f2_if(dst, o[0], o[1], xb1 && !xb0);
+            if constexpr (VAR) {
+              const double vj = a.svar[((int64_t)s * a.NP + a.gap_pattern[k * G + j]) * a.NK +
+                                       a.kmap[NKIND1 + kyr] * a.nkx + kint];
+              double* vdst = a.var + (zk + 1 + j) * P + pix;
+              st_cs_d2_if(vdst, vj, vj, !xb0);                 // columns 0, 1 (not at x = 0)
+              st_cs_d2_if(vdst + 2, vj, vj, !xb1);             // columns 2, 3 (not at x = W-2)
+              st_cs_d1_if(vdst + 1, vj, xb0);                  // x = 1 of the first group
+            }
           } else {
             double* vdst = VAR ? a.var + (zk + 1 + j) * P + pix : nullptr;
             const double vj =

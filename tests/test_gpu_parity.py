@@ -186,8 +186,9 @@ def test_chained_schedule_matches_serial(cuda, accum):
 
 @pytest.mark.parametrize("n_bins", [3, 29, 30, 32])
 def test_fit_variogram_bin_counts(cuda, n_bins):
-    """n_bins + 3 residual rows above a warp (30, 32) take the scalar TRF
-    kernel (fit_scalar_kernel); 29 is the largest warp-parallel case."""
+    """Bin counts up to MAX_BINS = 32: one residual row per lane, up to 35
+    augmented-Jacobian rows in the warp SVD, and pair ranking whose per-warp
+    bin counters (8 x 33) outnumber the 256 threads that clear them."""
     from paper_2303_09523_b200 import fit_variogram
     r = np.random.default_rng(n_bins)
     c = r.integers(0, 60, size=(4000, 3)).astype(float)
