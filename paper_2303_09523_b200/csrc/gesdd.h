@@ -142,7 +142,7 @@ VK_HD Ext ext_add(Ext a, Ext b) {
 // fsqrt (correctly rounded to 64 bits) then fstpl (rounded to double), by
 // exact integer square root -- the reference form, and the fallback of
 // ext_sqrt_to_double near a rounding boundary
-VK_HD double ext_sqrt_exact(Ext a) {
+VK_HDC double ext_sqrt_exact(Ext a) {
   if (a.m == 0) return 0.0;
   unsigned __int128 M;
   int re;
@@ -216,10 +216,53 @@ VK_HD double ext_sqrt_to_double(Ext a) {
   return scalbn(res, E / 2);
 }
 
+// (h, l) += (bh, bl) for non-negative double-doubles: two-sum of the high
+// parts, low parts added to its error, renormalised
+VK_HD void dd_add(double& h, double& l, double bh, double bl) {
+  const double s = add(h, bh), bb = sub(s, h);
+  const double e = add(add(sub(h, sub(s, bb)), sub(bh, bb)), add(l, bl));
+  h = add(s, e);
+  l = sub(e, sub(h, s));
+}
+
+// Fast decision of the x87 dnrm2 from the exact sum of squares S = h + l (a
+// double-double, relative error < 2^-100).  The x87 chain rounds each square
+// and each partial sum to 64 bits: n <= 32 terms give |X - S| <= n 2^-64 S,
+// so round64(sqrt X) lies within 2^-59 y of y = sqrt(S).  If y is farther
+// than that from every midpoint between two doubles, round53(round64(sqrt X))
+// = round53(y) = yh (the correctly rounded sqrt(h), corrected by yl < ulp/2).
+// Returns false (the caller runs the exact emulation) near a midpoint (about
+// 1 % of inputs), when yh is a power of two, or outside [2^-900, 2^900].
+VK_HD bool dnrm2_decide(double h, double l, double* res) {
+  if (!(h > 0x1p-900 && h < 0x1p+900)) return false;
+  const double yh = sqrt_(h);
+  const double r = add(fma_(-yh, yh, h), l);             // S - yh^2 (first term exact)
+  const double yl = mul(r, div(0.5, yh));
+  const uint64_t b = dbits(yh);
+  if ((b & 0xfffffffffffffull) == 0) return false;
+  const double ulp = np::from_bits(((b >> 52) - 52) << 52);
+  if (!(fabs(yl) < sub(mul(0.5, ulp), mul(yh, 0x1p-58)))) return false;
+  *res = yh;
+  return true;
+}
+
+// double-double accumulation of squares (error-free products, two-sum; every
+// operation rounded separately -- no contraction)
+VK_HD void dd_add_sq(double v, double& h, double& l) {
+  const double p = mul(v, v);
+  const double pe = fma_(v, v, -p);
+  dd_add(h, l, p, pe);
+}
+
 // OpenBLAS dnrm2 (interface: n == 1 -> |x|; kernel dnrm2_k SKYLAKEX, x87)
-VK_HD double dnrm2(int n, const double* x, int incx) {
+VK_HDN double dnrm2(int n, const double* x, int incx) {
   if (n <= 0) return 0.0;
   if (n == 1) return fabs(x[0]);
+  if (n <= 32) {
+    double h = 0.0, l = 0.0, r;
+    for (int i = 0; i < n; ++i) dd_add_sq(x[i * incx], h, l);
+    if (dnrm2_decide(h, l, &r)) return r;
+  }
   Ext acc[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
   int i = 0;
   const int n8 = n & ~7;
@@ -317,7 +360,7 @@ VK_HD void dswap(int n, double* x, int incx, double* y, int incy) {
 }
 
 // ------------------------------------------------------------------- LAPACK
-VK_HD double dlapy2(double x, double y) {
+VK_HDN double dlapy2(double x, double y) {
   if (x != x) return x;
   if (y != y) return y;
   const double xa = fabs(x), ya = fabs(y);
@@ -328,7 +371,7 @@ VK_HD double dlapy2(double x, double y) {
 }
 
 // dlarfg(n, alpha, x, incx, tau)
-VK_HD void dlarfg(int n, double* alpha, double* x, int incx, double* tau) {
+VK_HDN void dlarfg(int n, double* alpha, double* x, int incx, double* tau) {
   if (n <= 1) { *tau = 0.0; return; }
   double xnorm = dnrm2(n - 1, x, incx);
   if (xnorm == 0.0) { *tau = 0.0; return; }
@@ -353,7 +396,7 @@ VK_HD void dlarfg(int n, double* alpha, double* x, int incx, double* tau) {
 }
 
 // dlarf(side, m, n, v, incv, tau, C, ldc)
-VK_HD void dlarf(bool left, int m, int n, const double* v, int incv, double tau, double* C, int ldc) {
+VK_HDN void dlarf(bool left, int m, int n, const double* v, int incv, double tau, double* C, int ldc) {
   int lastv = 0, lastc = 0;
   if (tau != 0.0) {
     lastv = left ? m : n;
@@ -393,7 +436,7 @@ VK_HD void dlarf(bool left, int m, int n, const double* v, int incv, double tau,
 }
 
 // dgeqr2(m, n, A, lda, tau), n = 3
-VK_HD void dgeqr2(int m, int n, double* A, int lda, double* tau) {
+VK_HDN void dgeqr2(int m, int n, double* A, int lda, double* tau) {
   const int k = m < n ? m : n;
   for (int i = 0; i < k; ++i) {
     dlarfg(m - i, &A[i + i * lda], &A[(i + 1 < m ? i + 1 : m - 1) + i * lda], 1, &tau[i]);
@@ -407,7 +450,7 @@ VK_HD void dgeqr2(int m, int n, double* A, int lda, double* tau) {
 }
 
 // dorg2r(m, n, k, A, lda, tau), k = n
-VK_HD void dorg2r(int m, int n, int k, double* A, int lda, const double* tau) {
+VK_HDN void dorg2r(int m, int n, int k, double* A, int lda, const double* tau) {
   for (int i = k - 1; i >= 0; --i) {
     if (i < n - 1) {
       A[i + i * lda] = 1.0;
@@ -420,7 +463,7 @@ VK_HD void dorg2r(int m, int n, int k, double* A, int lda, const double* tau) {
 }
 
 // dgebd2(m, n, A, lda, d, e, tauq, taup), m >= n
-VK_HD void dgebd2(int m, int n, double* A, int lda, double* d, double* e, double* tauq, double* taup) {
+VK_HDN void dgebd2(int m, int n, double* A, int lda, double* d, double* e, double* tauq, double* taup) {
   for (int i = 0; i < n; ++i) {
     dlarfg(m - i, &A[i + i * lda], &A[(i + 1 < m ? i + 1 : m - 1) + i * lda], 1, &tauq[i]);
     d[i] = A[i + i * lda];
@@ -440,7 +483,7 @@ VK_HD void dgebd2(int m, int n, double* A, int lda, double* d, double* e, double
 }
 
 // dlartg (LAPACK 3.10+ form)
-VK_HD void dlartg(double f, double g, double* c, double* s, double* r) {
+VK_HDN void dlartg(double f, double g, double* c, double* s, double* r) {
   const double safmin = 2.2250738585072014e-308;         // 2^-1022
   const double safmax = 4.49423283715579e+307;           // 2^1022
   const double rtmin = 1.4916681462400413e-154;          // sqrt(safmin)
@@ -467,7 +510,7 @@ VK_HD void dlartg(double f, double g, double* c, double* s, double* r) {
 }
 
 // dlas2: singular values of [[f, g], [0, h]]
-VK_HD void dlas2(double f, double g, double h, double* ssmin, double* ssmax) {
+VK_HDN void dlas2(double f, double g, double h, double* ssmin, double* ssmax) {
   const double fa = fabs(f), ga = fabs(g), ha = fabs(h);
   const double fhmn = fmin(fa, ha), fhmx = fmax(fa, ha);
   if (fhmn == 0.0) {
@@ -507,7 +550,7 @@ VK_HD void dlas2(double f, double g, double h, double* ssmin, double* ssmax) {
 }
 
 // dlasv2: SVD of [[f, g], [0, h]]
-VK_HD void dlasv2(double f, double g, double h, double* ssmin, double* ssmax, double* snr,
+VK_HDN void dlasv2(double f, double g, double h, double* ssmin, double* ssmax, double* snr,
                   double* csr, double* snl, double* csl) {
   double ft = f, fa = fabs(ft), ht = h, ha = fabs(h);
   int pmax = 1;
@@ -572,7 +615,7 @@ VK_HD void dlasv2(double f, double g, double h, double* ssmin, double* ssmax, do
 }
 
 // dlasr(side, 'V', direct, m, n, c, s, A, lda)
-VK_HD void dlasr(bool left, bool forward, int m, int n, const double* c, const double* s, double* A, int lda) {
+VK_HDN void dlasr(bool left, bool forward, int m, int n, const double* c, const double* s, double* A, int lda) {
   if (left) {
     for (int jj = 0; jj < m - 1; ++jj) {
       const int j = forward ? jj : m - 2 - jj;
@@ -602,7 +645,7 @@ VK_HD void dlasr(bool left, bool forward, int m, int n, const double* c, const d
 
 // dbdsqr('U', n, ncvt = n, nru = n, ncc = 0, d, e, VT, ldvt, U, ldu); n <= 3.
 // Returns info (0 on convergence).
-VK_HD int dbdsqr(int n, double* d, double* e, double* VT, int ldvt, double* U, int ldu) {
+VK_HDN int dbdsqr(int n, double* d, double* e, double* VT, int ldvt, double* U, int ldu) {
   const int ncvt = n, nru = n;
   const double eps = DL_EPS, unfl = DL_SFMIN;
   const int maxitr = 6;
@@ -842,7 +885,7 @@ VK_HD int dbdsqr(int n, double* d, double* e, double* VT, int ldvt, double* U, i
 // dbdsdc('U', 'I', n): identity U, VT, then dlasdq -> dbdsqr, then the
 // selection sort of dlasdq / dbdsdc (no-ops on dbdsqr's sorted output unless
 // values tie, which the same code then resolves identically).
-VK_HD int dbdsdc(int n, double* d, double* e, double* U, int ldu, double* VT, int ldvt) {
+VK_HDN int dbdsdc(int n, double* d, double* e, double* U, int ldu, double* VT, int ldvt) {
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) {
       U[i + j * ldu] = (i == j) ? 1.0 : 0.0;
@@ -881,7 +924,7 @@ VK_HD int dbdsdc(int n, double* d, double* e, double* U, int ldu, double* VT, in
 }
 
 // dorm2r('L', 'N', m, n, k, A, lda, tau, C, ldc): C := Q C
-VK_HD void dorm2r_ln(int m, int n, int k, double* A, int lda, const double* tau, double* C, int ldc) {
+VK_HDN void dorm2r_ln(int m, int n, int k, double* A, int lda, const double* tau, double* C, int ldc) {
   for (int i = k - 1; i >= 0; --i) {
     const double aii = A[i + i * lda];
     A[i + i * lda] = 1.0;
@@ -891,7 +934,7 @@ VK_HD void dorm2r_ln(int m, int n, int k, double* A, int lda, const double* tau,
 }
 
 // dorml2('R', 'N', m, n, k, A, lda, tau, C, ldc): C := C Q (Q from dgelqf rows)
-VK_HD void dorml2_rn(int m, int n, int k, double* A, int lda, const double* tau, double* C, int ldc) {
+VK_HDN void dorml2_rn(int m, int n, int k, double* A, int lda, const double* tau, double* C, int ldc) {
   for (int i = k - 1; i >= 0; --i) {
     const double aii = A[i + i * lda];
     A[i + i * lda] = 1.0;
@@ -903,7 +946,7 @@ VK_HD void dorml2_rn(int m, int n, int k, double* A, int lda, const double* tau,
 // numpy.linalg.svd(A, full_matrices=False) for a row-major (M x 3) A, M >= 5.
 // Outputs U row-major (M x 3), s (3), VT row-major (3 x 3).  Returns 0 on
 // success, nonzero if dbdsqr did not converge (numpy raises LinAlgError).
-VK_HD int svd_m3(const double* A_rm, int M, double* U_rm, double* s, double* VT_rm) {
+VK_HDN int svd_m3(const double* A_rm, int M, double* U_rm, double* s, double* VT_rm) {
   const int N = 3;
   double A[GMAXM * 3];                                   // column-major, lda = M
   for (int r = 0; r < M; ++r)

@@ -34,10 +34,35 @@ __device__ __forceinline__ Ext shfl_ext(Ext v, int src) {
   return r;
 }
 
+// Fast form of the x87 dnrm2 below (see dnrm2_decide): the exact sum of
+// squares as a double-double over a warp tree; about 1 % of the calls fall
+// back to the exact emulation.  Lanes may associate the tree differently, so
+// the fallback is taken warp-uniformly (__any_sync); a lane's fast result,
+// when taken, is provably the x87 result.
+__device__ __forceinline__ bool dnrm2_fast(int n, const double* x, int lane, double* res) {
+  double h = 0.0, l = 0.0;
+  if (lane < n) {
+    const double v = x[lane];
+    h = mul(v, v);
+    l = fma_(v, v, -h);                        // exact square h + l
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double bh = __shfl_xor_sync(0xffffffffu, h, o), bl = __shfl_xor_sync(0xffffffffu, l, o);
+    dd_add(h, l, bh, bl);
+  }
+  const bool ok = dnrm2_decide(h, l, res);
+  return !__any_sync(0xffffffffu, !ok);
+}
+
 // dnrm2(n, x, 1), x in shared memory; every lane returns the same value
-__device__ double dnrm2_warp(int n, const double* x, SvdWarpSmem& sm, int lane) {
+VK_DN double dnrm2_warp(int n, const double* x, SvdWarpSmem& sm, int lane) {
   if (n <= 0) return 0.0;
   if (n == 1) return fabs(x[0]);
+  if (n <= 32) {
+    double r;
+    if (dnrm2_fast(n, x, lane, &r)) return r;
+  }
   for (int j = lane; j < n; j += 32) {
     const Ext q = ext_sq(x[j]);
     sm.em[j] = q.m;
@@ -62,7 +87,7 @@ __device__ void dscal_warp(int n, double a, double* x, int lane) {
 }
 
 // dlarfg(n, alpha, x, 1, tau) with alpha and x in shared memory
-__device__ void dlarfg_warp(int n, double* alpha, double* x, double* tau, SvdWarpSmem& sm, int lane) {
+VK_DN void dlarfg_warp(int n, double* alpha, double* x, double* tau, SvdWarpSmem& sm, int lane) {
   if (n <= 1) { *tau = 0.0; return; }
   VK_TP(tn);
   double xnorm = dnrm2_warp(n - 1, x, sm, lane);
@@ -91,7 +116,7 @@ __device__ void dlarfg_warp(int n, double* alpha, double* x, double* tau, SvdWar
 }
 
 // dlarf('L', m, n, v, 1, tau, C, ldc) with n <= 2 columns, v and C in shared memory
-__device__ void dlarf_left_warp(int m, int n, const double* v, double tau, double* C, int ldc, int lane) {
+VK_DN void dlarf_left_warp(int m, int n, const double* v, double tau, double* C, int ldc, int lane) {
   int lastv = 0, lastc = 0;
   if (tau != 0.0) {
     lastv = m;
@@ -154,7 +179,7 @@ __device__ void dlarf_left_warp(int m, int n, const double* v, double tau, doubl
 
 // numpy.linalg.svd(A, full_matrices=False) of the row-major (M x 3) A (the
 // same on every lane); outputs on every lane as svd_m3.
-__device__ int svd_m3_warp(const double* A_rm, int M, double* U_rm, double* s, double* VT_rm,
+VK_DN int svd_m3_warp(const double* A_rm, int M, double* U_rm, double* s, double* VT_rm,
                            SvdWarpSmem& sm, int lane) {
   const int N = 3;
   double* A = sm.A;

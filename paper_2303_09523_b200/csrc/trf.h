@@ -45,6 +45,17 @@ struct TrfResult {
 constexpr double TRF_EPS = 2.220446049250313e-16;   // np.finfo(float).eps
 constexpr int TRF_MAXM = MAX_BINS + 3;              // rows of the augmented Jacobian
 
+// The TRF's row-length arrays.  The evaluator owns them: the host evaluator
+// as a member, the device warp in shared memory -- every lane stores the same
+// bits, so each lane reads back its own store or an identical one, and the
+// 32 lanes share one copy instead of 32 copies of local memory (~100 KB per
+// warp, more than the L1 left beside a fit's shared-memory reservation).
+struct TrfWork {
+  double f[MAX_BINS], J[MAX_BINS * 3], Ja[TRF_MAXM * 3], U[TRF_MAXM * 3];
+  double f_new[MAX_BINS], fa[TRF_MAXM];
+  double q1[MAX_BINS], q2[MAX_BINS];   // evaluate_quadratic / build_quadratic_1d rows
+};
+
 VK_HD bool finite_d(double v) { return v - v == 0.0; }
 
 VK_HD double pymax(double a, double b) { return (b > a) ? b : a; }  // Python max(a, b)
@@ -109,7 +120,9 @@ VK_HD double fd_step(const double* x, const double* lb, const double* ub, int i)
 // J_transposed.T, an F-contiguous (m, 3) array.
 struct TrfScalarEval {
   const TrfProblem& P;
+  mutable TrfWork wk;
   VK_HD explicit TrfScalarEval(const TrfProblem& p) : P(p) {}
+  VK_HD TrfWork& work() const { return wk; }
   VK_HD int m() const { return P.nb; }
   VK_HD void resid(const double* x, double* f) const {
     const FitModel md = fit_model(x);
@@ -136,7 +149,7 @@ struct TrfScalarEval {
 // s descending, U (M x 3, row-major), V (3 x 3, row-major: V[i*3+k] = V_ik).
 // One-sided Jacobi on the columns of A (rotations until every pair is
 // orthogonal to working precision), then normalised columns.
-VK_HD void svd_aug(const double* A, int M, double* U, double* s, double* V) {
+VK_HDC void svd_aug(const double* A, int M, double* U, double* s, double* V) {
   double B[TRF_MAXM * 3];
   for (int i = 0; i < M * 3; ++i) B[i] = A[i];
   for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0 : 0.0;
@@ -196,7 +209,7 @@ VK_HD void v_dot(const double* V, const double* x, double* y) {
 }
 
 // common.py solve_lsq_trust_region (More's method on one SVD).
-VK_HD void lsq_trust_region(int m, const double* uf, const double* s, const double* V,
+VK_HDN void lsq_trust_region(int m, const double* uf, const double* s, const double* V,
                             double Delta, double initial_alpha, double* p, double* alpha_out) {
   const int n = 3;
   double suf[3];
@@ -263,7 +276,7 @@ VK_HD bool in_bounds3(const double* x, const double* lb, const double* ub) {
 }
 
 // common.py step_size_to_bound
-VK_HD double step_to_bound(const double* x, const double* s, const double* lb,
+VK_HDN double step_to_bound(const double* x, const double* s, const double* lb,
                            const double* ub, int* hits) {
   double steps[3];
   double mn = INFINITY;
@@ -282,7 +295,7 @@ VK_HD double step_to_bound(const double* x, const double* s, const double* lb,
 }
 
 // common.py intersect_trust_region: roots t of ||x + s t|| = Delta
-VK_HD bool intersect_tr(const double* x, const double* s, double Delta, double* t_neg, double* t_pos) {
+VK_HDN bool intersect_tr(const double* x, const double* s, double Delta, double* t_neg, double* t_pos) {
   const double a = np::dot(s, s, 3);
   if (a == 0.0) return false;
   const double b = np::dot(x, s, 3);
@@ -301,8 +314,8 @@ VK_HD void jh_dot(const double* Jh, int m, const double* s, double* out) {
 }
 
 // common.py evaluate_quadratic (1-D s)
-VK_HD double eval_quad(const double* Jh, int m, const double* g, const double* s, const double* diag) {
-  double Js[MAX_BINS];
+VK_HDN double eval_quad(const double* Jh, int m, const double* g, const double* s, const double* diag,
+                        double* Js) {
   jh_dot(Jh, m, s, Js);
   double q = np::dot(Js, Js, m);
   double sd[3];
@@ -313,9 +326,9 @@ VK_HD double eval_quad(const double* Jh, int m, const double* g, const double* s
 }
 
 // common.py build_quadratic_1d (with s0 when given)
-VK_HD void build_quad_1d(const double* Jh, int m, const double* g, const double* s,
-                         const double* diag, const double* s0, double* a, double* b, double* c) {
-  double v[MAX_BINS];
+VK_HDN void build_quad_1d(const double* Jh, int m, const double* g, const double* s,
+                         const double* diag, const double* s0, double* a, double* b, double* c,
+                         double* v, double* u) {
   jh_dot(Jh, m, s, v);
   double aa = np::dot(v, v, m);
   double sd[3];
@@ -325,7 +338,6 @@ VK_HD void build_quad_1d(const double* Jh, int m, const double* g, const double*
   double bb = np::dot(g, s, 3);
   double cc = 0.0;
   if (s0) {
-    double u[MAX_BINS];
     jh_dot(Jh, m, s0, u);
     bb = np::add(bb, np::dot(u, v, m));
     cc = np::add(np::mul(0.5, np::dot(u, u, m)), np::dot(g, s0, 3));
@@ -357,14 +369,14 @@ VK_HD void min_quad_1d(double a, double b, double lb, double ub, double c, doubl
 }
 
 // trf.py select_step.  step/step_h out; returns predicted reduction; false on error.
-VK_HD bool select_step(const double* x, const double* Jh, int m, const double* diag_h,
+VK_HDN bool select_step(const double* x, const double* Jh, int m, const double* diag_h,
                        const double* g_h, double* p, double* p_h, const double* d,
                        double Delta, const double* lb, const double* ub, double theta,
-                       double* step, double* step_h, double* pred) {
+                       double* step, double* step_h, double* pred, TrfWork& w) {
   double xp[3];
   for (int i = 0; i < 3; ++i) xp[i] = np::add(x[i], p[i]);
   if (in_bounds3(xp, lb, ub)) {
-    const double pv = eval_quad(Jh, m, g_h, p_h, diag_h);
+    const double pv = eval_quad(Jh, m, g_h, p_h, diag_h, w.q1);
     for (int i = 0; i < 3; ++i) { step[i] = p[i]; step_h[i] = p_h[i]; }
     *pred = -pv;
     return true;
@@ -397,7 +409,7 @@ VK_HD bool select_step(const double* x, const double* Jh, int m, const double* d
   double r_value;
   if (r_stride_l <= r_stride_u) {
     double a, b, c;
-    build_quad_1d(Jh, m, g_h, r_h, diag_h, p_h, &a, &b, &c);
+    build_quad_1d(Jh, m, g_h, r_h, diag_h, p_h, &a, &b, &c, w.q1, w.q2);
     min_quad_1d(a, b, r_stride_l, r_stride_u, c, &r_stride, &r_value);
     for (int i = 0; i < 3; ++i) {
       r_h[i] = np::mul(r_h[i], r_stride);
@@ -408,7 +420,7 @@ VK_HD bool select_step(const double* x, const double* Jh, int m, const double* d
     r_value = INFINITY;
   }
   for (int i = 0; i < 3; ++i) { p[i] = np::mul(p[i], theta); p_h[i] = np::mul(p_h[i], theta); }
-  const double p_value = eval_quad(Jh, m, g_h, p_h, diag_h);
+  const double p_value = eval_quad(Jh, m, g_h, p_h, diag_h, w.q1);
   double ag_h[3], ag[3];
   for (int i = 0; i < 3; ++i) { ag_h[i] = -g_h[i]; ag[i] = np::mul(d[i], ag_h[i]); }
   const double to_tr2 = np::div(Delta, np::norm(ag_h, 3));
@@ -416,7 +428,7 @@ VK_HD bool select_step(const double* x, const double* Jh, int m, const double* d
   const double to_bound2 = step_to_bound(x, ag, lb, ub, hits3);
   double ag_stride = (to_bound2 < to_tr2) ? np::mul(theta, to_bound2) : to_tr2;
   double a2, b2, c2;
-  build_quad_1d(Jh, m, g_h, ag_h, diag_h, nullptr, &a2, &b2, &c2);
+  build_quad_1d(Jh, m, g_h, ag_h, diag_h, nullptr, &a2, &b2, &c2, w.q1, w.q2);
   double ag_value;
   min_quad_1d(a2, b2, 0.0, ag_stride, 0.0, &ag_stride, &ag_value);
   for (int i = 0; i < 3; ++i) { ag_h[i] = np::mul(ag_h[i], ag_stride); ag[i] = np::mul(ag[i], ag_stride); }
@@ -443,7 +455,7 @@ VK_HD double next_toward(double from, double to) {
 
 // common.py make_strictly_feasible (rstep > 0 uses the relative rule,
 // rstep == 0 uses nextafter).
-VK_HD void make_strictly_feasible(double* x, const double* lb, const double* ub, double rstep) {
+VK_HDN void make_strictly_feasible(double* x, const double* lb, const double* ub, double rstep) {
   for (int i = 0; i < 3; ++i) {
     int active = 0;
     if (rstep == 0.0) {
@@ -464,7 +476,7 @@ VK_HD void make_strictly_feasible(double* x, const double* lb, const double* ub,
 }
 
 // compute_grad: J.T.dot(f) for the F-contiguous (m, 3) J (column-major here)
-VK_HD void trf_grad(const double* J, const double* f, int m, double* g) {
+VK_HDN void trf_grad(const double* J, const double* f, int m, double* g) {
   for (int i = 0; i < 3; ++i) g[i] = np::colT(J + i * m, f, m, i);
 }
 
@@ -494,7 +506,9 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
   TrfResult res;
   double x[3] = {x0_in[0], x0_in[1], x0_in[2]};
   make_strictly_feasible(x, lb, ub, 1e-10);      // least_squares.py: x0 strictly feasible
-  double f[MAX_BINS], J[MAX_BINS * 3];
+  TrfWork& w = ev.work();
+  double* const f = w.f;
+  double* const J = w.J;
   ev.resid(x, f);
   ev.jac(x, f, lb, ub, J);
   int nfev = 1;
@@ -520,8 +534,12 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
   double alpha = 0.0;
   int status = -100;       // None
   int iteration = 0;
-  double Ja[TRF_MAXM * 3], U[TRF_MAXM * 3], sv[3], V[9];
-  double x_new[3], f_new[MAX_BINS], fa[TRF_MAXM];
+  double* const Ja = w.Ja;
+  double* const U = w.U;
+  double* const f_new = w.f_new;
+  double* const fa = w.fa;
+  double sv[3], V[9];
+  double x_new[3];
   double cost_new = 0.0;
   double g_norm = 0.0;
   const int M = m + 3;
@@ -569,7 +587,7 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
       VK_TP(t_sel);
       for (int i = 0; i < 3; ++i) p[i] = np::mul(d[i], p_h[i]);
       double step[3], step_h[3], pred;
-      const bool sel_ok = select_step(x, Ja, m, diag_h, g_h, p, p_h, d, Delta, lb, ub, theta, step, step_h, &pred);
+      const bool sel_ok = select_step(x, Ja, m, diag_h, g_h, p, p_h, d, Delta, lb, ub, theta, step, step_h, &pred, w);
       VK_TACC(4, t_sel);
       if (!sel_ok) {
         res.status = -1;

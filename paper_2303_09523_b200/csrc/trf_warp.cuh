@@ -13,16 +13,17 @@
 
 namespace vk {
 
-template <int KIND>
 struct WarpEval {
   const TrfProblem& P;      // shared memory
   double* row;              // shared memory, >= 3 * MAX_BINS doubles
   lapack::SvdWarpSmem& sv;  // shared memory
+  TrfWork& wk;              // shared memory (identical stores from every lane)
   int lane;
 
-  __device__ WarpEval(const TrfProblem& p, double* buf, lapack::SvdWarpSmem& s, int l)
-      : P(p), row(buf), sv(s), lane(l) {}
+  __device__ WarpEval(const TrfProblem& p, double* buf, lapack::SvdWarpSmem& s, TrfWork& w, int l)
+      : P(p), row(buf), sv(s), wk(w), lane(l) {}
   __device__ int m() const { return P.nb; }
+  __device__ TrfWork& work() const { return wk; }
 
   __device__ int svd(const double* A, int M, double* U, double* s, double* VT) const {
     return lapack::svd_m3_warp(A, M, U, s, VT, sv, lane);
@@ -30,7 +31,7 @@ struct WarpEval {
 
   __device__ void resid(const double* x, double* f) const {
     const FitModel md = fit_model(x);
-    if (lane < P.nb) row[lane] = fit_residual<KIND>(md, P.h[lane], P.gemp[lane], P.w[lane]);
+    if (lane < P.nb) row[lane] = fit_residual_kind(P.kind, md, P.h[lane], P.gemp[lane], P.w[lane]);
     __syncwarp();
     for (int r = 0; r < P.nb; ++r) f[r] = row[r];
     __syncwarp();
@@ -47,7 +48,7 @@ struct WarpEval {
         double x1[3] = {x[0], x[1], x[2]};
         x1[i] = np::add(x[i], h);
         const FitModel md = fit_model(x1);
-        const double f1 = fit_residual<KIND>(md, P.h[lane], P.gemp[lane], P.w[lane]);
+        const double f1 = fit_residual_kind(P.kind, md, P.h[lane], P.gemp[lane], P.w[lane]);
         const double dx = np::sub(np::add(x[i], h), x[i]);
         row[i * m + lane] = np::div(np::sub(f1, fr), dx);
       }

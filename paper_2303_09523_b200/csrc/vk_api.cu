@@ -541,6 +541,11 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   va.node = p->d_npnode;
   va.mean = p->d_mean;
   va.svar = p->d_svar;
+  va.stats = p->d_stats;
+  va.inexact = p->d_inexact;
+  va.part_b = p->d_part_b;
+  va.part_e = p->d_part_e;
+  va.nchunk = p->nchunk;
   if (draw || side_bins) {
     VK_CUDA(cudaEventRecord(p->ev_fork, st));
     VK_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));

@@ -12,6 +12,7 @@ namespace vk {
 // Per-chunk plane statistics (count, mean, M2, min, max, non-finite).
 struct ChunkStat {
   double n, mean, m2, mn, mx, bad;
+  double sum;                        // raw sum: exact when the chunk is integer-valued (< 2^23)
 };
 constexpr int STATS_CHUNK = 32768;   // elements per stats block
 
@@ -97,6 +98,13 @@ struct NpVarArgs {
   double* node;                      // [S][node_stride]
   double* mean;                      // [S]
   double* svar;                      // [S]
+  // integer-valued parts: the mean's pairwise sum is the exact sum, read from
+  // the statistics pass's chunk sums (nullptr: always the pairwise pass)
+  const ChunkStat* stats = nullptr;  // [K][nchunk]
+  const int* inexact = nullptr;      // [K] per known plane
+  const int32_t* part_b = nullptr;   // [S] first / last known plane of the part
+  const int32_t* part_e = nullptr;
+  int nchunk = 0;
 };
 cudaError_t launch_npvar(const NpVarArgs& a, cudaStream_t st);
 // stable sort of each class's pairs by bin (tables with order != nullptr)

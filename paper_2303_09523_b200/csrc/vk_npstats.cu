@@ -48,9 +48,20 @@ __device__ __forceinline__ double npv(const float* __restrict__ known, const dou
 // order.
 constexpr int LEAF_CTA = 64;
 
+// part s is integer-valued (every known plane flagged exact by the
+// statistics pass, |v| < 2^23, m < 2^30): each pairwise partial sum of the
+// values is an exact integer below 2^53, so numpy's sum equals the exact sum
+__device__ __forceinline__ bool int_part(const NpVarArgs& a, int s) {
+  if (!a.inexact || !a.stats || a.values || a.part_m[s] >= (int64_t(1) << 30)) return false;
+  for (int k = a.part_b[s]; k <= a.part_e[s]; ++k)
+    if (__ldg(a.inexact + k)) return false;
+  return true;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) npsum_leaf_kernel(NpVarArgs a) {
   const int s = a.part0 + blockIdx.y;
+  if (MODE == 0 && int_part(a, s)) return;              // the mean comes from the chunk sums
   const NpSumTree T = a.trees[a.part_class[s]];
   const int l0 = blockIdx.x * LEAF_CTA;
   if (l0 >= T.nleaf) return;
@@ -115,6 +126,16 @@ __global__ void __launch_bounds__(256) npsum_leaf_kernel(NpVarArgs a) {
 template <int MODE>
 __global__ void __launch_bounds__(1024) npsum_tree_kernel(NpVarArgs a) {
   const int s = a.part0 + blockIdx.x;
+  if (MODE == 0 && int_part(a, s)) {
+    // exact sum of the part's chunk sums (any order), one warp
+    if (threadIdx.x >= 32) return;
+    const int64_t i0 = (int64_t)a.part_b[s] * a.nchunk, i1 = (int64_t)(a.part_e[s] + 1) * a.nchunk;
+    double t = 0.0;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += 32) t += a.stats[i].sum;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) a.mean[s] = __ddiv_rn(t, (double)a.part_m[s]);
+    return;
+  }
   const NpSumTree T = a.trees[a.part_class[s]];
   const double* leaf = a.leaf + (int64_t)s * a.leaf_stride;
   double* node = a.node + (int64_t)s * a.node_stride;

@@ -134,6 +134,9 @@ __device__ __forceinline__ void stats_chunk(const T* __restrict__ data, int64_t 
     cs.mean = cs.n > 0 ? shift + a1 / cs.n : 0.0;
     cs.m2 = cs.n > 0 ? fmax(a2 - a1 * a1 / cs.n, 0.0) : 0.0;
     cs.mn = amn; cs.mx = amx; cs.bad = ab;
+    // integer-valued chunk: every partial of a1 is an exact integer, and so
+    // is shift * n (< 2^38), hence the raw sum is exact
+    cs.sum = a1 + shift * (double)(end - beg);
     out[(int64_t)k * nchunk + c] = cs;
   }
 }
@@ -453,10 +456,9 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
   if (!(ub[2] > lb[2])) { if (lane == 0) a.status[s] = PS_FIT_FAILED; return; }
   __shared__ double rowbuf[3 * MAX_BINS];
   __shared__ lapack::SvdWarpSmem svsm;
+  __shared__ TrfWork wk;
   TrfResult r;
-  if (P.kind == KIND_EXPONENTIAL) r = trf_fit_t(WarpEval<KIND_EXPONENTIAL>(P, rowbuf, svsm, lane), x0, lb, ub);
-  else if (P.kind == KIND_GAUSSIAN) r = trf_fit_t(WarpEval<KIND_GAUSSIAN>(P, rowbuf, svsm, lane), x0, lb, ub);
-  else r = trf_fit_t(WarpEval<KIND_SPHERICAL>(P, rowbuf, svsm, lane), x0, lb, ub);
+  r = trf_fit_t(WarpEval(P, rowbuf, svsm, wk, lane), x0, lb, ub);
   if (lane != 0) return;
   if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
   const double nug = pymax(r.x[0], 0.0);

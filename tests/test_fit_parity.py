@@ -200,3 +200,28 @@ def test_host_trf_reproduces_reference_fits(shim):
             assert info[1] == p["nfev"] and info[0] == p["status"], (name, p["part"])
     print(f"\nhost TRF: {exact}/{total} parts bit-identical, worst gate ratio {worst:.3g}")
     assert worst <= 0.05
+
+
+def test_dnrm2_fast_decision_is_x87(shim, openblas):
+    """dnrm2's double-double fast path (gesdd.h dnrm2_decide) against the
+    shipped x87 kernel on many vectors: random magnitudes, integer vectors
+    (exact sums, often near-exact square roots), repeated values and zeros."""
+    L = openblas
+    I = C.c_int64
+    rng = np.random.default_rng(11)
+    n_vec = 60000
+    for t in range(n_vec):
+        n = int(rng.integers(2, 19))
+        kind = t % 4
+        if kind == 0:
+            x = _rv(rng, n, 8)
+        elif kind == 1:
+            x = rng.integers(-4096, 4096, n).astype(np.float64)
+        elif kind == 2:
+            x = np.full(n, _rv(rng, 1, 4)[0])
+        else:
+            x = _rv(rng, n, 2)
+            x[rng.random(n) < 0.4] = 0.0
+        got = shim.vkl_dnrm2(n, x.ctypes.data_as(D), 1)
+        ref = L.scipy_dnrm2_64_(C.byref(I(n)), x.ctypes.data_as(D), C.byref(I(1)))
+        assert got == ref, (t, n, x.tolist(), got, ref)
