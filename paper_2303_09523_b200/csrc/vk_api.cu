@@ -349,18 +349,27 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
       VK_TRY(p->alloc(&t.ocnt, (size_t)order_chunks(d->max_pairs) * MAX_BINS));
       p->tables.push_back(t);
       // numpy's pairwise-summation tree for this class's sample count
-      const NpSumTreeHost th = build_npsum_tree(g.pair_classes[c].m);
+      const NpSumWarpHost wh = build_npsum_warp(g.pair_classes[c].m);
+      const NpSumTreeHost& th = wh.top;
       NpSumTree tr;
-      tr.nleaf = (int32_t)th.leaf_off.size() - 1;
+      tr.nleaf = (int32_t)wh.wr_leaf.size() - 1;
       tr.nnode = (int32_t)th.node_lr.size() / 2;
       tr.nlevel = (int32_t)th.level.size() - 1;
-      int32_t *lo = nullptr, *lr = nullptr, *lv = nullptr;
-      VK_TRY(p->put(&lo, th.leaf_off));
+      int32_t *lo = nullptr, *lr = nullptr, *lv = nullptr, *wl = nullptr;
+      int16_t* wp = nullptr;
+      int8_t* wn = nullptr;
+      VK_TRY(p->put(&lo, wh.leaf_off));
       VK_TRY(p->put(&lr, th.node_lr.empty() ? std::vector<int32_t>{0, 0} : th.node_lr));
       VK_TRY(p->put(&lv, th.level));
+      VK_TRY(p->put(&wl, wh.wr_leaf));
+      VK_TRY(p->put(&wp, wh.prog));
+      VK_TRY(p->put(&wn, wh.nint));
       tr.leaf_off = lo;
       tr.node_lr = lr;
       tr.level = lv;
+      tr.wr_leaf = wl;
+      tr.wr_prog = wp;
+      tr.wr_nint = wn;
       p->trees.push_back(tr);
       p->max_leaf = std::max(p->max_leaf, tr.nleaf);
       p->leaf_stride = std::max<int64_t>(p->leaf_stride, tr.nleaf);
@@ -1170,17 +1179,24 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   PairTable* d_t = (PairTable*)get(sizeof(PairTable));
   ChunkStat* stats = (ChunkStat*)get((size_t)nchunk * sizeof(ChunkStat));
   double* partial = (double*)get((size_t)nblk * n_bins * 8);
-  const NpSumTreeHost th = build_npsum_tree(m);
+  const NpSumWarpHost wh = build_npsum_warp(m);
+  const NpSumTreeHost& th = wh.top;
   NpSumTree tr;
-  tr.nleaf = (int32_t)th.leaf_off.size() - 1;
+  tr.nleaf = (int32_t)wh.wr_leaf.size() - 1;
   tr.nnode = (int32_t)th.node_lr.size() / 2;
   tr.nlevel = (int32_t)th.level.size() - 1;
-  int32_t* t_lo = (int32_t*)get(th.leaf_off.size() * 4);
+  int32_t* t_lo = (int32_t*)get(wh.leaf_off.size() * 4);
   int32_t* t_lr = (int32_t*)get(std::max<size_t>(2, th.node_lr.size()) * 4);
   int32_t* t_lv = (int32_t*)get(th.level.size() * 4);
+  int32_t* t_wl = (int32_t*)get(wh.wr_leaf.size() * 4);
+  int16_t* t_wp = (int16_t*)get(wh.prog.size() * 2);
+  int8_t* t_wn = (int8_t*)get(wh.nint.size());
   tr.leaf_off = t_lo;
   tr.node_lr = t_lr;
   tr.level = t_lv;
+  tr.wr_leaf = t_wl;
+  tr.wr_prog = t_wp;
+  tr.wr_nint = t_wn;
   NpSumTree* d_tr = (NpSumTree*)get(sizeof(NpSumTree));
   double* npleaf = (double*)get((size_t)std::max(1, tr.nleaf) * 8);
   double* npnode = (double*)get((size_t)std::max(1, tr.nnode) * 8);
@@ -1197,7 +1213,10 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   for (void* q : mem)
     if (!q) { cleanup(); return set_err(VK_E_CUDA, "cudaMalloc failed"); }
   cudaError_t e = cudaMemcpyAsync(d_t, &t, sizeof(PairTable), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(t_lo, th.leaf_off.data(), th.leaf_off.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t_lo, wh.leaf_off.data(), wh.leaf_off.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t_wl, wh.wr_leaf.data(), wh.wr_leaf.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t_wp, wh.prog.data(), wh.prog.size() * 2, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t_wn, wh.nint.data(), wh.nint.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && !th.node_lr.empty())
     e = cudaMemcpyAsync(t_lr, th.node_lr.data(), th.node_lr.size() * 4, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(t_lv, th.level.data(), th.level.size() * 4, cudaMemcpyHostToDevice, st);

@@ -77,11 +77,14 @@ cudaError_t launch_bins(const BinsArgs& a, cudaStream_t st);
 // ---- numpy-exact statistics (vk_npstats.cu) ----
 // numpy's pairwise-summation tree for an array of m float64 (leaves of <= 128
 // elements, internal nodes grouped by height)
-struct NpSumTree {                   // device view of one class's tree
-  int32_t nleaf, nnode, nlevel;
-  const int32_t* leaf_off;
+struct NpSumTree {                   // device view of one class's tree (npsum.h build_npsum_warp)
+  int32_t nleaf, nnode, nlevel;      // the tree above the warp roots: leaf i = warp root i
+  const int32_t* leaf_off;           // [n true leaves + 1] element offsets
   const int32_t* node_lr;
   const int32_t* level;
+  const int32_t* wr_leaf;            // [nleaf + 1] first true leaf of each warp root
+  const int16_t* wr_prog;            // [nleaf][31] children of the root's internal nodes
+  const int8_t* wr_nint;             // [nleaf] internal nodes per warp root
 };
 // svar[s] = values.var() of part s exactly as numpy computes it
 struct NpVarArgs {

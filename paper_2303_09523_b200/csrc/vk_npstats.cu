@@ -9,9 +9,9 @@
 //            leaves of <= 128 elements with eight strided accumulators, split
 //            at n/2 rounded down to a multiple of 8).  The tree depends only on
 //            the sample count m, so the host builds it once per pair class
-//            (build_npsum_tree); the device sums every leaf in parallel
-//            (eight lanes per leaf, numpy's combination order) and then adds
-//            the internal nodes level by level in one CTA per part.  Two
+//            (build_npsum_warp); the device sums every subtree of <= 32
+//            leaves with one warp (a lane per leaf, numpy's combination order)
+//            and then adds the nodes above level by level in one CTA per part.  Two
 //            rounds: mean = sum(v) / m, then svar = sum((v - mean)^2) / m.
 //   bins   : np.bincount accumulates each bin's weights sequentially in pair
 //            order.  pair_order_kernel sorts the pairs of a class by bin
@@ -41,13 +41,6 @@ __device__ __forceinline__ double npv(const float* __restrict__ known, const dou
   return __dmul_rn(t, t);
 }
 
-// A CTA sums LEAF_CTA consecutive leaves (<= 128 elements each): their
-// contiguous element range is staged in shared memory with 128-bit loads (all
-// independent, so the loads of a CTA are in flight together), then eight
-// lanes per leaf (lane k holds numpy's accumulator r[k]) add it in numpy's
-// order.
-constexpr int LEAF_CTA = 64;
-
 // part s is integer-valued (every known plane flagged exact by the
 // statistics pass, |v| < 2^23, m < 2^30): each pairwise partial sum of the
 // values is an exact integer below 2^53, so numpy's sum equals the exact sum
@@ -58,67 +51,85 @@ __device__ __forceinline__ bool int_part(const NpVarArgs& a, int s) {
   return true;
 }
 
+// numpy's leaf sum of n <= 128 elements starting at absolute sample g: eight
+// strided accumulators r[k] (initialised with the first eight values), combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail in order
 template <int MODE>
-__global__ void __launch_bounds__(256) npsum_leaf_kernel(NpVarArgs a) {
-  const int s = a.part0 + blockIdx.y;
-  if (MODE == 0 && int_part(a, s)) return;              // the mean comes from the chunk sums
-  const NpSumTree T = a.trees[a.part_class[s]];
-  const int l0 = blockIdx.x * LEAF_CTA;
-  if (l0 >= T.nleaf) return;
-  const int l1 = min(T.nleaf, l0 + LEAF_CTA);
-  const int64_t base = a.part_base[s];
-  const int64_t e0 = T.leaf_off[l0], e1 = T.leaf_off[l1];
-  __shared__ __align__(16) float stage[LEAF_CTA * 128 + 4];
-  // stage elements [e0, e1) of the part (absolute index base + e)
-  const int64_t g0 = base + e0, g1 = base + e1;
-  const bool vec = ((uintptr_t)a.known & 15) == 0;
-  const int64_t a0 = vec ? (g0 & ~(int64_t)3) : g0;     // 16-byte aligned start
-  if (!a.values) {                                      // explicit float64 samples are read directly
-    const int n = (int)(g1 - a0);
-    const int n4 = vec ? n >> 2 : 0;
-    const float4* src = reinterpret_cast<const float4*>(a.known + a0);
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) reinterpret_cast<float4*>(stage)[i] = __ldg(src + i);
-    for (int i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) stage[i] = __ldg(a.known + a0 + i);
-  }
-  __syncthreads();
-  const int shift = (int)(g0 - a0);                     // stage[j + shift] = element e0 + j
-  const double mean = MODE ? a.mean[s] : 0.0;
-  auto val = [&](int64_t e) -> double {                 // element e of the part (e0 <= e < e1)
-    const double v = a.values ? a.values[base + e] : (double)stage[(int)(e - e0) + shift];
+__device__ __forceinline__ double np_leaf_sum(const NpVarArgs& a, int64_t g, int n, double mean) {
+  auto f = [&](double v) -> double {
     if (MODE == 0) return v;
     const double t = __dsub_rn(v, mean);
     return __dmul_rn(t, t);
   };
-  const int k = threadIdx.x & 7;
-  for (int leaf = l0 + (threadIdx.x >> 3); leaf < l0 + LEAF_CTA; leaf += blockDim.x >> 3) {
-    const bool act = leaf < l1;
-    double r = 0.0;
-    int64_t o = 0, n = 0, n8 = 0;
-    if (act) {
-      o = T.leaf_off[leaf];
-      n = T.leaf_off[leaf + 1] - o;
-      n8 = n - n % 8;
-      if (n >= 8) {
-        r = val(o + k);
-        for (int64_t i = 8; i < n8; i += 8) r = __dadd_rn(r, val(o + i + k));
-      }
+  auto at = [&](int i) -> double { return f(a.values ? a.values[g + i] : (double)__ldg(a.known + g + i)); };
+  if (n < 8) {
+    double res = -0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, at(i));
+    return res;
+  }
+  const int n8 = n - n % 8;
+  double r[8];
+  if (!a.values && ((g & 3) == 0)) {
+    const float4* p = reinterpret_cast<const float4*>(a.known + g);
+    {
+      const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
+      r[0] = f(x0.x); r[1] = f(x0.y); r[2] = f(x0.z); r[3] = f(x0.w);
+      r[4] = f(x1.x); r[5] = f(x1.y); r[6] = f(x1.z); r[7] = f(x1.w);
     }
-    // res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
-    double t = __shfl_down_sync(0xffffffffu, r, 1);
-    r = __dadd_rn(r, t);
-    t = __shfl_down_sync(0xffffffffu, r, 2);
-    r = __dadd_rn(r, t);
-    t = __shfl_down_sync(0xffffffffu, r, 4);
-    r = __dadd_rn(r, t);
-    if (act && k == 0) {
-      double res = r;
-      if (n < 8) {                                  // whole array below 8 (not reached: m >= 9)
-        res = -0.0;
-        n8 = 0;
-      }
-      for (int64_t i = n8; i < n; ++i) res = __dadd_rn(res, val(o + i));
-      a.leaf[(int64_t)s * a.leaf_stride + leaf] = res;
+#pragma unroll 4
+    for (int q = 2; q < n8 / 4; q += 2) {
+      const float4 x0 = __ldg(p + q), x1 = __ldg(p + q + 1);
+      r[0] = __dadd_rn(r[0], f(x0.x)); r[1] = __dadd_rn(r[1], f(x0.y));
+      r[2] = __dadd_rn(r[2], f(x0.z)); r[3] = __dadd_rn(r[3], f(x0.w));
+      r[4] = __dadd_rn(r[4], f(x1.x)); r[5] = __dadd_rn(r[5], f(x1.y));
+      r[6] = __dadd_rn(r[6], f(x1.z)); r[7] = __dadd_rn(r[7], f(x1.w));
     }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = at(k);
+    for (int i = 8; i < n8; i += 8)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], at(i + k));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (int i = n8; i < n; ++i) res = __dadd_rn(res, at(i));
+  return res;
+}
+
+// One warp per warp root (a subtree of <= 32 leaves, npsum.h): lane i sums
+// leaf i straight from global memory (16-byte loads, each lane walking its own
+// leaf), then lane 0 adds the subtree's internal nodes in height order from
+// shared memory; the root's value goes to a.leaf for the top-tree kernel.
+constexpr int NPW_WARPS = 8;
+
+template <int MODE>
+__global__ void __launch_bounds__(32 * NPW_WARPS) npsum_warp_kernel(NpVarArgs a) {
+  const int s = a.part0 + blockIdx.y;
+  if (MODE == 0 && int_part(a, s)) return;              // the mean comes from the chunk sums
+  const NpSumTree T = a.trees[a.part_class[s]];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * NPW_WARPS + warp;
+  if (r >= T.nleaf) return;
+  const int l0 = T.wr_leaf[r], nl = T.wr_leaf[r + 1] - l0;
+  const double mean = MODE ? a.mean[s] : 0.0;
+  double v = 0.0;
+  if (lane < nl) {
+    const int o = T.leaf_off[l0 + lane];
+    v = np_leaf_sum<MODE>(a, a.part_base[s] + o, T.leaf_off[l0 + lane + 1] - o, mean);
+  }
+  __shared__ double val[NPW_WARPS][64];
+  val[warp][lane] = v;
+  __syncwarp();
+  if (lane == 0) {
+    const int ni = T.wr_nint[r];
+    const int16_t* prog = T.wr_prog + (int64_t)r * 31;
+    double* vv = val[warp];
+    for (int j = 0; j < ni; ++j) {
+      const int code = (uint16_t)prog[j];
+      vv[32 + j] = __dadd_rn(vv[code & 0xff], vv[code >> 8]);
+    }
+    a.leaf[(int64_t)s * a.leaf_stride + r] = ni ? vv[32 + ni - 1] : vv[0];
   }
 }
 
@@ -326,10 +337,11 @@ __global__ void __launch_bounds__(32) binsum_kernel(BinSumArgs a) {
 
 cudaError_t launch_npvar(const NpVarArgs& a, cudaStream_t st) {
   if (a.n_parts <= 0) return cudaSuccess;
-  const dim3 lgrid((unsigned)((a.max_leaf + LEAF_CTA - 1) / LEAF_CTA), (unsigned)a.n_parts);
-  npsum_leaf_kernel<0><<<lgrid, 256, 0, st>>>(a);
+  // a.max_leaf: most warp roots of a class in the launch
+  const dim3 lgrid((unsigned)((a.max_leaf + NPW_WARPS - 1) / NPW_WARPS), (unsigned)a.n_parts);
+  npsum_warp_kernel<0><<<lgrid, 32 * NPW_WARPS, 0, st>>>(a);
   npsum_tree_kernel<0><<<a.n_parts, 1024, 0, st>>>(a);
-  npsum_leaf_kernel<1><<<lgrid, 256, 0, st>>>(a);
+  npsum_warp_kernel<1><<<lgrid, 32 * NPW_WARPS, 0, st>>>(a);
   npsum_tree_kernel<1><<<a.n_parts, 1024, 0, st>>>(a);
   return cudaGetLastError();
 }

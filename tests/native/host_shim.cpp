@@ -204,4 +204,50 @@ double vkh_npsum_tree(const double* a, int64_t n, int32_t* nleaf_out) {
   if (nleaf_out) *nleaf_out = nleaf;
   return nnode ? v[nleaf + nnode - 1] : v[0];
 }
+// the device's warp decomposition (build_npsum_warp) evaluated on the host:
+// true leaves, then each warp root's program, then the top tree; returns the
+// number of warp roots in *nwr_out
+static double npsum_leaf(const double* x, int64_t m) {
+  if (m < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < m; ++i) res += x[i];
+    return res;
+  }
+  double r[8];
+  for (int k = 0; k < 8; ++k) r[k] = x[k];
+  int64_t i = 8;
+  for (; i < m - m % 8; i += 8)
+    for (int k = 0; k < 8; ++k) r[k] += x[i + k];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < m; ++i) res += x[i];
+  return res;
+}
+double vkh_npsum_warp(const double* a, int64_t n, int32_t* nwr_out) {
+  const vk::NpSumWarpHost w = vk::build_npsum_warp(n);
+  const int nwr = (int)w.wr_leaf.size() - 1;
+  std::vector<double> root(nwr);
+  for (int r = 0; r < nwr; ++r) {
+    double val[64];
+    const int l0 = w.wr_leaf[r], nl = w.wr_leaf[r + 1] - l0;
+    if (nl > 32 || w.nint[r] != nl - 1) return NAN;
+    for (int i = 0; i < nl; ++i) {
+      const int64_t o = w.leaf_off[l0 + i];
+      val[i] = npsum_leaf(a + o, w.leaf_off[l0 + i + 1] - o);
+    }
+    for (int j = 0; j < w.nint[r]; ++j) {
+      const int code = (uint16_t)w.prog[(size_t)r * 31 + j];
+      val[32 + j] = val[code & 0xff] + val[code >> 8];
+    }
+    root[r] = w.nint[r] ? val[32 + w.nint[r] - 1] : val[0];
+  }
+  const vk::NpSumTreeHost& t = w.top;
+  const int nnode = (int)t.node_lr.size() / 2;
+  std::vector<double> v(nwr + nnode);
+  for (int r = 0; r < nwr; ++r) v[r] = root[r];
+  for (int lev = 0; lev + 1 < (int)t.level.size(); ++lev)
+    for (int j = t.level[lev]; j < t.level[lev + 1]; ++j)
+      v[nwr + j] = v[t.node_lr[2 * j]] + v[t.node_lr[2 * j + 1]];
+  if (nwr_out) *nwr_out = nwr;
+  return nnode ? v[nwr + nnode - 1] : v[0];
+}
 }

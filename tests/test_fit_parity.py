@@ -159,6 +159,24 @@ def test_pairwise_sum_tree_is_numpys(shim):
         assert shim.vkh_npsum_tree(t.ctypes.data_as(D), C.c_int64(len(t)), C.byref(nl)) / len(a) == a.var(), n
 
 
+def test_pairwise_sum_warp_decomposition_is_numpys(shim):
+    """npsum.h build_npsum_warp (the device's warp subtrees + top tree) gives
+    np.sum / np.var bit for bit, including sizes whose root is a leaf and the
+    C1-C5 part sizes."""
+    shim.vkh_npsum_warp.restype = C.c_double
+    rng = np.random.default_rng(5)
+    sizes = list(rng.integers(9, 5000, 60)) + [9, 100, 128, 129, 4095, 4096, 4097, 8191, 81920,
+                                                 9 * 128 * 128, 5 * 256 * 256, 5 * 512 * 512,
+                                                 9 * 512 * 512, 327680, 2359296]
+    for n in sizes:
+        a = rng.standard_normal(int(n)) * 1e3 + rng.uniform(0, 50)
+        nw = C.c_int32(0)
+        assert shim.vkh_npsum_warp(a.ctypes.data_as(D), C.c_int64(len(a)), C.byref(nw)) == a.sum(), n
+        t = (a - a.mean()) ** 2
+        assert shim.vkh_npsum_warp(t.ctypes.data_as(D), C.c_int64(len(t)), C.byref(nw)) / len(a) == a.var(), n
+        assert 1 <= nw.value <= max(1, n // 128 + 1)
+
+
 def _host_fit(shim, p):
     counts = np.array(p["counts"])
     sums = np.array([float.fromhex(s) for s in p["sums"]])
