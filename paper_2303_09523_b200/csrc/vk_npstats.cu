@@ -105,7 +105,9 @@ constexpr int NPW_WARPS = 8;
 
 template <int MODE>
 __global__ void __launch_bounds__(32 * NPW_WARPS) npsum_warp_kernel(NpVarArgs a) {
-  const int s = a.part0 + blockIdx.y;
+  // the second pass walks the parts last to first: the statistics pass (and
+  // the first pass) ended on the last parts' planes, which are still in L2
+  const int s = a.part0 + (MODE == 1 ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y);
   if (MODE == 0 && int_part(a, s)) return;              // the mean comes from the chunk sums
   const NpSumTree T = a.trees[a.part_class[s]];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -255,39 +257,59 @@ __global__ void __launch_bounds__(256) binsq_kernel(BinSumArgs a) {
   }
 }
 
-// bin sums in pair order (np.bincount: out[b] += w in order): one warp per
-// (part, bin).  The warp streams the bin's slots in coalesced chunks of 256
-// into registers, parks them in shared memory, and lane 0 adds them in order
-// while the next chunk's loads are in flight.
-__global__ void __launch_bounds__(32) binsum_kernel(BinSumArgs a) {
-  const int s = a.part0 + blockIdx.y, b = blockIdx.x, lane = threadIdx.x;
+// bin sums in pair order (np.bincount: out[b] += w in order): one CTA per
+// (part, bin).  Integer-valued data first: all eight warps test and sum the
+// bin's weights in any order (exact, see below); otherwise warp 0 streams the
+// bin's slots in coalesced chunks of 256 into registers, parks them in shared
+// memory, and lane 0 adds them in order while the next chunk's loads are in
+// flight.
+constexpr int BINSUM_THREADS = 256;
+
+__global__ void __launch_bounds__(BINSUM_THREADS) binsum_kernel(BinSumArgs a) {
+  const int s = a.part0 + blockIdx.y, b = blockIdx.x, lane = threadIdx.x & 31;
   const PairTable t = a.tables[a.part_class[s]];
   const int q0 = t.boff[b], q1 = t.boff[b + 1];
   const double* x = a.sq + (int64_t)s * a.max_pairs;
   // integer-valued data: every weight is a half-integer, and while the total
   // stays below 2^51 every partial sum in any order is exact -- the
-  // lane-parallel sum then equals the sequential one bit for bit
+  // CTA-parallel sum then equals the sequential one bit for bit
   {
     double ps = 0.0;
     bool ok = true;
-    for (int c = q0; c < q1 && ok; c += 256) {       // chunks of 8 per lane; float data stops early
+    for (int c = q0 + (int)threadIdx.x; c < q1; c += 4 * BINSUM_THREADS) {
+      double v[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int q = c + lane + 32 * u;
-        const double v = q < q1 ? x[q] : 0.0;
-        const double t = 2.0 * v;
-        ok &= (t == rint(t));
-        ps += v;
+      for (int u = 0; u < 4; ++u) {
+        const int q = c + u * BINSUM_THREADS;
+        v[u] = q < q1 ? x[q] : 0.0;
       }
-      ok = __all_sync(0xffffffffu, ok);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double t2 = 2.0 * v[u];
+        ok &= (t2 == rint(t2));
+        ps += v[u];
+      }
     }
+    ok = __syncthreads_and(ok);
     if (ok) {
+      __shared__ double red[BINSUM_THREADS / 32];
       for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-      if (ps < 0x1p51) {
-        if (lane == 0) a.bsum[(int64_t)s * a.n_bins + b] = ps;
-        return;
+      if (lane == 0) red[threadIdx.x >> 5] = ps;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < BINSUM_THREADS / 32; ++w) tot += red[w];
+        if (tot < 0x1p51) {
+          a.bsum[(int64_t)s * a.n_bins + b] = tot;
+          red[0] = -1.0;                              // done
+        } else {
+          red[0] = 0.0;
+        }
       }
+      __syncthreads();
+      if (red[0] < 0.0) return;
     }
+    if (threadIdx.x >= 32) return;                    // the ordered sum is one warp's
   }
   __shared__ double buf[2][256];
   double v[8];
@@ -364,7 +386,7 @@ cudaError_t launch_binsums(const BinSumArgs& a, cudaStream_t st) {
   if (a.n_parts <= 0) return cudaSuccess;
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (a.max_pairs + 1023) / 1024));
   binsq_kernel<<<dim3(gx, a.n_parts), 256, 0, st>>>(a);
-  binsum_kernel<<<dim3(a.n_bins, a.n_parts), 32, 0, st>>>(a);
+  binsum_kernel<<<dim3(a.n_bins, a.n_parts), BINSUM_THREADS, 0, st>>>(a);
   return cudaGetLastError();
 }
 
