@@ -22,6 +22,7 @@
 #pragma once
 #include <cstdint>
 #include <cmath>
+#include <type_traits>
 #include "vk_common.h"
 #include "npref.h"
 
@@ -885,7 +886,402 @@ VK_HDN int dbdsqr(int n, double* d, double* e, double* VT, int ldvt, double* U, 
 // dbdsdc('U', 'I', n): identity U, VT, then dlasdq -> dbdsqr, then the
 // selection sort of dlasdq / dbdsdc (no-ops on dbdsqr's sorted output unless
 // values tie, which the same code then resolves identically).
+// ---- n = 3, every array in registers ---------------------------------------
+// dbdsqr / dbdsdc above specialised for the fit's 3 x 3 bidiagonal: for n = 3
+// the only QR sweep is over the whole matrix (ll = 1, M = 3 -- a 2 x 2 block
+// goes to dlasv2), so every index is a compile-time constant and d, e, U, VT
+// stay in registers instead of local memory.  Same operations in the same
+// order as the generic code (tests/test_fit_parity.py checks both against
+// OpenBLAS).  U, VT column-major, ld = 3.
+
+// dlasr('L', 'V', direct, 3, 3, c, s, A, 3): rotations j = 0, 1 on rows (j, j+1)
+template <bool FORWARD>
+VK_HD void dlasr3_left(const double* c, const double* s, double* A) {
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj) {
+    const int j = FORWARD ? jj : 1 - jj;
+    const double ct = c[j], st = s[j];
+    if (ct != 1.0 || st != 0.0) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double temp = A[(j + 1) + i * 3];
+        A[(j + 1) + i * 3] = sub(mul(ct, temp), mul(st, A[j + i * 3]));
+        A[j + i * 3] = add(mul(st, temp), mul(ct, A[j + i * 3]));
+      }
+    }
+  }
+}
+
+// dlasr('R', 'V', direct, 3, 3, c, s, A, 3): rotations j = 0, 1 on columns (j, j+1)
+template <bool FORWARD>
+VK_HD void dlasr3_right(const double* c, const double* s, double* A) {
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj) {
+    const int j = FORWARD ? jj : 1 - jj;
+    const double ct = c[j], st = s[j];
+    if (ct != 1.0 || st != 0.0) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double temp = A[i + (j + 1) * 3];
+        A[i + (j + 1) * 3] = sub(mul(ct, temp), mul(st, A[i + j * 3]));
+        A[i + j * 3] = add(mul(st, temp), mul(ct, A[i + j * 3]));
+      }
+    }
+  }
+}
+
+// rows a, b of VT (drot over the 3 columns) and columns a, b of U
+template <int A_, int B_>
+VK_HD void rot3_rows(double* VT, double c, double s) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double xi = VT[A_ + i * 3], yi = VT[B_ + i * 3];
+    VT[A_ + i * 3] = fma_(c, xi, mul(s, yi));
+    VT[B_ + i * 3] = fma_(c, yi, -mul(s, xi));
+  }
+}
+template <int A_, int B_>
+VK_HD void rot3_cols(double* U, double c, double s) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double xi = U[i + A_ * 3], yi = U[i + B_ * 3];
+    U[i + A_ * 3] = fma_(c, xi, mul(s, yi));
+    U[i + B_ * 3] = fma_(c, yi, -mul(s, xi));
+  }
+}
+template <int A_, int B_>
+VK_HD void swap3_rows(double* VT) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) { const double t = VT[A_ + i * 3]; VT[A_ + i * 3] = VT[B_ + i * 3]; VT[B_ + i * 3] = t; }
+}
+template <int A_, int B_>
+VK_HD void swap3_cols(double* U) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) { const double t = U[i + A_ * 3]; U[i + A_ * 3] = U[i + B_ * 3]; U[i + B_ * 3] = t; }
+}
+
+// swap d[a], d[b] (a < b), rows a, b of VT and columns a, b of U; a, b runtime
+// in {0, 1, 2}, dispatched to constant indices
+VK_HD void sv3_swap(int a, int b, double* d, double* VT, double* U, bool vt_first) {
+  auto sw = [&](auto ca, auto cb) {
+    constexpr int A_ = decltype(ca)::value, B_ = decltype(cb)::value;
+    if (vt_first) { swap3_rows<A_, B_>(VT); swap3_cols<A_, B_>(U); }
+    else { swap3_cols<A_, B_>(U); swap3_rows<A_, B_>(VT); }
+  };
+  if (a == 0 && b == 1) sw(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{});
+  else if (a == 0 && b == 2) sw(std::integral_constant<int, 0>{}, std::integral_constant<int, 2>{});
+  else sw(std::integral_constant<int, 1>{}, std::integral_constant<int, 2>{});
+  (void)d;
+}
+
+VK_HD double sel3(const double* d, int i) { return i == 0 ? d[0] : (i == 1 ? d[1] : d[2]); }
+VK_HD void put3(double* d, int i, double v) {
+  if (i == 0) d[0] = v;
+  else if (i == 1) d[1] = v;
+  else d[2] = v;
+}
+
+VK_HD int dbdsdc3(double* dio, double* eio, double* Uo, double* VTo) {
+  double d[3] = {dio[0], dio[1], dio[2]};
+  double e[2] = {eio[0], eio[1]};
+  double U[9], VT[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) { U[i] = (i % 4 == 0) ? 1.0 : 0.0; VT[i] = U[i]; }
+  const int n = 3;
+  const double eps = DL_EPS, unfl = DL_SFMIN;
+  const int maxitr = 6;
+  const double tolmul = 0x1.8ace5422aa0dbp+6;
+  const double tol = mul(tolmul, eps);
+  double smax = 0.0;
+  for (int i = 0; i < 3; ++i) smax = fmax(smax, fabs(d[i]));
+  for (int i = 0; i < 2; ++i) smax = fmax(smax, fabs(e[i]));
+  double smin = 0.0, thresh;
+  {
+    double sminoa = fabs(d[0]);
+    if (sminoa != 0.0) {
+      double mu = sminoa;
+#pragma unroll
+      for (int i = 1; i < 3; ++i) {
+        mu = mul(fabs(d[i]), div(mu, add(mu, fabs(e[i - 1]))));
+        sminoa = fmin(sminoa, mu);
+        if (sminoa == 0.0) break;
+      }
+    }
+    sminoa = div(sminoa, sqrt_((double)n));
+    thresh = fmax(mul(tol, sminoa), mul((double)maxitr, mul((double)n, mul((double)n, unfl))));
+  }
+  const int maxitdivn = maxitr * n;
+  int iterdivn = 0, iter = -1, oldll = -1, oldm = -1, idir = 0;
+  int M = 3;
+  while (true) {
+    if (M <= 1) break;
+    if (iter >= n) {
+      iter -= n;
+      ++iterdivn;
+      if (iterdivn >= maxitdivn) return 1;
+    }
+    // find the diagonal block: M in {2, 3}
+    int ll = 0;
+    bool split = false;
+    if (M == 3) {
+      smax = fabs(d[2]);
+      if (fabs(e[1]) <= thresh) { ll = 2; split = true; }
+      else {
+        smax = fmax(smax, fmax(fabs(d[1]), fabs(e[1])));
+        if (fabs(e[0]) <= thresh) { ll = 1; split = true; }
+        else smax = fmax(smax, fmax(fabs(d[0]), fabs(e[0])));
+      }
+    } else {
+      smax = fabs(d[1]);
+      if (fabs(e[0]) <= thresh) { ll = 1; split = true; }
+      else smax = fmax(smax, fmax(fabs(d[0]), fabs(e[0])));
+    }
+    if (split) {
+      if (ll == 1) e[0] = 0.0; else e[1] = 0.0;
+      if (ll == M - 1) { M -= 1; continue; }
+    } else {
+      ll = 0;
+    }
+    ll += 1;
+    if (ll == M - 1) {
+      double sigmn, sigmx, sinr, cosr, sinl, cosl;
+      if (M == 3) {
+        dlasv2(d[1], e[1], d[2], &sigmn, &sigmx, &sinr, &cosr, &sinl, &cosl);
+        d[1] = sigmx; e[1] = 0.0; d[2] = sigmn;
+        rot3_rows<1, 2>(VT, cosr, sinr);
+        rot3_cols<1, 2>(U, cosl, sinl);
+      } else {
+        dlasv2(d[0], e[0], d[1], &sigmn, &sigmx, &sinr, &cosr, &sinl, &cosl);
+        d[0] = sigmx; e[0] = 0.0; d[1] = sigmn;
+        rot3_rows<0, 1>(VT, cosr, sinr);
+        rot3_cols<0, 1>(U, cosl, sinl);
+      }
+      M -= 2;
+      continue;
+    }
+    // here ll = 1, M = 3: the whole matrix
+    if (ll > oldm || M < oldll) {
+      if (fabs(d[0]) >= fabs(d[2])) idir = 1;
+      else idir = 2;
+    }
+    bool restart = false;
+    if (idir == 1) {
+      if (fabs(e[1]) <= mul(fabs(tol), fabs(d[2]))) { e[1] = 0.0; continue; }
+      double mu = fabs(d[0]);
+      smin = mu;
+      if (fabs(e[0]) <= mul(tol, mu)) { e[0] = 0.0; restart = true; }
+      else {
+        mu = mul(fabs(d[1]), div(mu, add(mu, fabs(e[0]))));
+        smin = fmin(smin, mu);
+        if (fabs(e[1]) <= mul(tol, mu)) { e[1] = 0.0; restart = true; }
+        else {
+          mu = mul(fabs(d[2]), div(mu, add(mu, fabs(e[1]))));
+          smin = fmin(smin, mu);
+        }
+      }
+    } else {
+      if (fabs(e[0]) <= mul(fabs(tol), fabs(d[0]))) { e[0] = 0.0; continue; }
+      double mu = fabs(d[2]);
+      smin = mu;
+      if (fabs(e[1]) <= mul(tol, mu)) { e[1] = 0.0; restart = true; }
+      else {
+        mu = mul(fabs(d[1]), div(mu, add(mu, fabs(e[1]))));
+        smin = fmin(smin, mu);
+        if (fabs(e[0]) <= mul(tol, mu)) { e[0] = 0.0; restart = true; }
+        else {
+          mu = mul(fabs(d[0]), div(mu, add(mu, fabs(e[0]))));
+          smin = fmin(smin, mu);
+        }
+      }
+    }
+    if (restart) continue;
+    oldll = ll;
+    oldm = M;
+    double shift, r;
+    if (mul(mul((double)n, tol), div(smin, smax)) <= fmax(eps, mul(0.01, tol))) {
+      shift = 0.0;
+    } else {
+      double sll;
+      if (idir == 1) {
+        sll = fabs(d[0]);
+        dlas2(d[1], e[1], d[2], &shift, &r);
+      } else {
+        sll = fabs(d[2]);
+        dlas2(d[0], e[0], d[1], &shift, &r);
+      }
+      if (sll > 0.0) {
+        const double q = div(shift, sll);
+        if (mul(q, q) < eps) shift = 0.0;
+      }
+    }
+    iter += M - ll;
+    double work[8];                                   // [cs 0..1 | sn | oldcs | oldsn], n - 1 = 2 each
+    if (shift == 0.0) {
+      if (idir == 1) {
+        double cs = 1.0, oldcs = 1.0, sn = 0.0, oldsn = 0.0;
+        dlartg(mul(d[0], cs), e[0], &cs, &sn, &r);
+        dlartg(mul(oldcs, r), mul(d[1], sn), &oldcs, &oldsn, &d[0]);
+        work[0] = cs; work[2] = sn; work[4] = oldcs; work[6] = oldsn;
+        dlartg(mul(d[1], cs), e[1], &cs, &sn, &r);
+        e[0] = mul(oldsn, r);
+        dlartg(mul(oldcs, r), mul(d[2], sn), &oldcs, &oldsn, &d[1]);
+        work[1] = cs; work[3] = sn; work[5] = oldcs; work[7] = oldsn;
+        const double hh = mul(d[2], cs);
+        d[2] = mul(hh, oldcs);
+        e[1] = mul(hh, oldsn);
+        dlasr3_left<true>(&work[0], &work[2], VT);
+        dlasr3_right<true>(&work[4], &work[6], U);
+        if (fabs(e[1]) <= thresh) e[1] = 0.0;
+      } else {
+        double cs = 1.0, oldcs = 1.0, sn = 0.0, oldsn = 0.0;
+        dlartg(mul(d[2], cs), e[1], &cs, &sn, &r);
+        dlartg(mul(oldcs, r), mul(d[1], sn), &oldcs, &oldsn, &d[2]);
+        work[1] = cs; work[3] = -sn; work[5] = oldcs; work[7] = -oldsn;
+        dlartg(mul(d[1], cs), e[0], &cs, &sn, &r);
+        e[1] = mul(oldsn, r);
+        dlartg(mul(oldcs, r), mul(d[0], sn), &oldcs, &oldsn, &d[1]);
+        work[0] = cs; work[2] = -sn; work[4] = oldcs; work[6] = -oldsn;
+        const double hh = mul(d[0], cs);
+        d[0] = mul(hh, oldcs);
+        e[0] = mul(hh, oldsn);
+        dlasr3_left<false>(&work[4], &work[6], VT);
+        dlasr3_right<false>(&work[0], &work[2], U);
+        if (fabs(e[0]) <= thresh) e[0] = 0.0;
+      }
+    } else {
+      if (idir == 1) {
+        double f = mul(sub(fabs(d[0]), shift), add(fsign(1.0, d[0]), div(shift, d[0])));
+        double g = e[0];
+        double cosr, sinr, cosl, sinl;
+        // i = 1
+        dlartg(f, g, &cosr, &sinr, &r);
+        f = add(mul(cosr, d[0]), mul(sinr, e[0]));
+        e[0] = sub(mul(cosr, e[0]), mul(sinr, d[0]));
+        g = mul(sinr, d[1]);
+        d[1] = mul(cosr, d[1]);
+        dlartg(f, g, &cosl, &sinl, &r);
+        d[0] = r;
+        f = add(mul(cosl, e[0]), mul(sinl, d[1]));
+        d[1] = sub(mul(cosl, d[1]), mul(sinl, e[0]));
+        g = mul(sinl, e[1]);
+        e[1] = mul(cosl, e[1]);
+        work[0] = cosr; work[2] = sinr; work[4] = cosl; work[6] = sinl;
+        // i = 2
+        dlartg(f, g, &cosr, &sinr, &r);
+        e[0] = r;
+        f = add(mul(cosr, d[1]), mul(sinr, e[1]));
+        e[1] = sub(mul(cosr, e[1]), mul(sinr, d[1]));
+        g = mul(sinr, d[2]);
+        d[2] = mul(cosr, d[2]);
+        dlartg(f, g, &cosl, &sinl, &r);
+        d[1] = r;
+        f = add(mul(cosl, e[1]), mul(sinl, d[2]));
+        d[2] = sub(mul(cosl, d[2]), mul(sinl, e[1]));
+        work[1] = cosr; work[3] = sinr; work[5] = cosl; work[7] = sinl;
+        e[1] = f;
+        dlasr3_left<true>(&work[0], &work[2], VT);
+        dlasr3_right<true>(&work[4], &work[6], U);
+        if (fabs(e[1]) <= thresh) e[1] = 0.0;
+      } else {
+        double f = mul(sub(fabs(d[2]), shift), add(fsign(1.0, d[2]), div(shift, d[2])));
+        double g = e[1];
+        double cosr, sinr, cosl, sinl;
+        // i = 3
+        dlartg(f, g, &cosr, &sinr, &r);
+        f = add(mul(cosr, d[2]), mul(sinr, e[1]));
+        e[1] = sub(mul(cosr, e[1]), mul(sinr, d[2]));
+        g = mul(sinr, d[1]);
+        d[1] = mul(cosr, d[1]);
+        dlartg(f, g, &cosl, &sinl, &r);
+        d[2] = r;
+        f = add(mul(cosl, e[1]), mul(sinl, d[1]));
+        d[1] = sub(mul(cosl, d[1]), mul(sinl, e[1]));
+        g = mul(sinl, e[0]);
+        e[0] = mul(cosl, e[0]);
+        work[1] = cosr; work[3] = -sinr; work[5] = cosl; work[7] = -sinl;
+        // i = 2
+        dlartg(f, g, &cosr, &sinr, &r);
+        e[1] = r;
+        f = add(mul(cosr, d[1]), mul(sinr, e[0]));
+        e[0] = sub(mul(cosr, e[0]), mul(sinr, d[1]));
+        g = mul(sinr, d[0]);
+        d[0] = mul(cosr, d[0]);
+        dlartg(f, g, &cosl, &sinl, &r);
+        d[1] = r;
+        f = add(mul(cosl, e[0]), mul(sinl, d[0]));
+        d[0] = sub(mul(cosl, d[0]), mul(sinl, e[0]));
+        work[0] = cosr; work[2] = -sinr; work[4] = cosl; work[6] = -sinl;
+        e[0] = f;
+        if (fabs(e[0]) <= thresh) e[0] = 0.0;
+        dlasr3_left<false>(&work[4], &work[6], VT);
+        dlasr3_right<false>(&work[0], &work[2], U);
+      }
+    }
+  }
+  // make singular values positive
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    if (d[i] < 0.0) {
+      d[i] = -d[i];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) VT[i + c * 3] = mul(VT[i + c * 3], -1.0);
+    }
+  }
+  // dbdsqr: sort into decreasing order (insertion of the minimum at the end)
+  for (int i = 1; i <= 2; ++i) {
+    int isub = 1;
+    double smn = d[0];
+    for (int j = 2; j <= 4 - i; ++j) {
+      const double dj = sel3(d, j - 1);
+      if (dj <= smn) { isub = j; smn = dj; }
+    }
+    if (isub != 4 - i) {
+      put3(d, isub - 1, sel3(d, 3 - i));
+      put3(d, 3 - i, smn);
+      sv3_swap(isub - 1, 3 - i, d, VT, U, true);
+    }
+  }
+  // dbdsdc: dlasdq sort (ascending scan, swap to the end)
+  for (int i = 1; i <= 3; ++i) {
+    int isub = i;
+    double smn = sel3(d, i - 1);
+    for (int j = i + 1; j <= 3; ++j) {
+      const double dj = sel3(d, j - 1);
+      if (dj < smn) { isub = j; smn = dj; }
+    }
+    if (isub != 4 - i) {
+      put3(d, isub - 1, sel3(d, 3 - i));
+      put3(d, 3 - i, smn);
+      const int a = isub - 1 < 3 - i ? isub - 1 : 3 - i, b = isub - 1 < 3 - i ? 3 - i : isub - 1;
+      sv3_swap(a, b, d, VT, U, true);
+    }
+  }
+  // dbdsdc: selection sort into decreasing order
+  for (int ii = 2; ii <= 3; ++ii) {
+    const int i = ii - 1;
+    int kk = i;
+    double p = sel3(d, i - 1);
+    for (int j = ii; j <= 3; ++j) {
+      const double dj = sel3(d, j - 1);
+      if (dj > p) { kk = j; p = dj; }
+    }
+    if (kk != i) {
+      put3(d, kk - 1, sel3(d, i - 1));
+      put3(d, i - 1, p);
+      sv3_swap(i - 1, kk - 1, d, VT, U, false);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) dio[i] = d[i];
+  eio[0] = e[0];
+  eio[1] = e[1];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) { Uo[i] = U[i]; VTo[i] = VT[i]; }
+  return 0;
+}
+
 VK_HDN int dbdsdc(int n, double* d, double* e, double* U, int ldu, double* VT, int ldvt) {
+  if (n == 3 && ldu == 3 && ldvt == 3) return dbdsdc3(d, e, U, VT);
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) {
       U[i + j * ldu] = (i == j) ? 1.0 : 0.0;

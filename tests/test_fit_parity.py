@@ -116,10 +116,26 @@ def test_lapack_pieces_are_openblas(shim, openblas):
                            *[C.byref(o) for o in o1])
         shim.vkl_dlasv2(f, g, h, o2.ctypes.data)
         assert [o.value for o in o1] == list(o2)
-    for _ in range(300):
+    for t in range(3000):
+        # random bidiagonals plus the structures that take dbdsqr's other
+        # branches: zero / tiny off-diagonals (splits, 2 x 2 blocks), zero
+        # diagonal entries, graded magnitudes (zero shift, both directions)
         d = _rv(rng, 3, 4)
         e = _rv(rng, 3, 4)
         e[2] = 0
+        k = t % 6
+        if k == 1:
+            e[rng.integers(0, 2)] *= 1e-18
+        elif k == 2:
+            d[rng.integers(0, 3)] = 0.0
+        elif k == 3:
+            d *= np.array([1e-9, 1.0, 1e9])[rng.permutation(3)]
+        elif k == 4:
+            e[rng.integers(0, 2)] = 0.0
+        elif k == 5:
+            d = np.round(d * 4) / 4
+            e = np.round(e * 4) / 4
+            e[2] = 0
         d1, e1, d2, e2 = d.copy(), e.copy(), d.copy(), e.copy()
         U1 = np.zeros((3, 3), order="F"); V1 = np.zeros((3, 3), order="F")
         U2 = np.zeros((3, 3), order="F"); V2 = np.zeros((3, 3), order="F")
