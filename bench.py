@@ -374,6 +374,16 @@ def run_gpu(args, cfg, ks):
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, ks, stream, rank, world, dev)
 
+    # the reference-shaped calls a drop-in user makes (kriging.py:264, :458):
+    # per sub-part, fit_variogram on the part's (coords, values) samples and
+    # fill_missing on its host NaN grid -- numpy in, numpy out, every upload,
+    # plan lookup and download inside the timed region; a bounded sample of
+    # the step's sub-parts (the samples and grids are the caller's own data,
+    # built outside the timed region)
+    dropin = None
+    if rank == 0 and not args.no_e2e:
+        dropin = run_dropin(args, cfg, ks)
+
     # strong scaling: ONE volume (the base config's K slices) split over the
     # ranks by Z sub-parts, halo over the C-ABI NCCL communicator inside the
     # step; the gather of the core planes to rank 0 timed separately
@@ -404,7 +414,7 @@ def run_gpu(args, cfg, ks):
             "config": _config(cfg, args, world),
             "schedule": "serial" if args.serial else "per-part fit->solve->predict chains",
             "roofline": roof, "stage_ms_serial": stages, "cpu_baseline": cpu, "e2e": e2e,
-            "pipelined": pipelined, "strong": strong,
+            "pipelined": pipelined, "dropin_e2e": dropin, "strong": strong,
             "gpu_launches": kpe * args.steps, "clocks": clk.summary(),
         }
         if scaling == "strong":
@@ -556,6 +566,44 @@ def run_pipelined(args, cfg, stack, K_loc, rank, world, dev, stream):
             "scheme": f"{depth} plans x {depth} streams in turn: a step's stats/pairs/bins/fits/solves "
                       "overlap earlier steps' predictions; every step runs the whole path "
                       "(no halo exchange in this loop)"}
+
+
+def run_dropin(args, cfg, ks, n_sample=4, reps=2):
+    """Reference-shaped drop-in calls on host numpy grids (see run_gpu)."""
+    import torch
+    from paper_2303_09523_b200 import VolumeGrid, fill_missing, fit_variogram
+    from paper_2303_09523_b200.block_pipeline import subpart_ranges
+    planes = _values(args, cfg, ks)
+    ranges = subpart_ranges(cfg.n_known, cfg.n_subparts, cfg.n_known // cfg.n_subparts)
+    pick = ranges[:: max(1, len(ranges) // n_sample)][:n_sample]
+    inputs = []
+    for (b, e) in pick:
+        # the caller's data: the part's NaN grid (known slice i at z = (i - b) f)
+        # and its known voxels in np.nonzero order as (x, y, z) samples
+        data = np.full(((e - b) * cfg.factor + 1, cfg.height, cfg.width), np.nan, dtype=np.float32)
+        data[::cfg.factor] = planes[b:e + 1]
+        mask = np.isnan(data)
+        kz, ky, kx = np.nonzero(~mask)
+        samples = (np.column_stack([kx, ky, kz]).astype(np.float64), data[kz, ky, kx].astype(np.float64))
+        inputs.append((VolumeGrid(data, mask), samples))
+    vox = sum(int(g.missing_mask.sum()) for g, _ in inputs)
+    g0, smp0 = inputs[0]
+    for g, smp in inputs:                      # plan cache, pinned host cache, scratch: warm
+        fill_missing(g, fit_variogram(smp, "exponential"), args.drift)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for g, smp in inputs:
+            out = fill_missing(g, fit_variogram(smp, "exponential"), args.drift)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    assert out.data.dtype == np.float32
+    return {"value": vox / dt, "unit": UNIT, "ms_per_part": 1e3 * dt / len(inputs),
+            "parts_timed": len(inputs), "reps": reps,
+            "calls": "fit_variogram((coords, values)) + fill_missing(VolumeGrid(host NaN grid), model) "
+                     "per sub-part, numpy in / numpy out (host wall clock, synchronized)",
+            "h2d_bytes_per_part": int(smp0[0].nbytes + smp0[1].nbytes + g0.data.nbytes + g0.missing_mask.nbytes),
+            "d2h_bytes_per_part": int(g0.data.nbytes + g0.missing_mask.nbytes)}
 
 
 def run_e2e(args, cfg, ks, stream, rank=0, world=1, dev=None):

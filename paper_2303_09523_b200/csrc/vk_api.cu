@@ -7,6 +7,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <mutex>
 #include <vector>
 #include <thread>
 #include <memory>
@@ -1156,12 +1157,27 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   const int64_t npmax = std::min<int64_t>(max_pairs, m * (m - 1) / 2);
   const int nchunk = (int)((m + STATS_CHUNK - 1) / STATS_CHUNK);
   const int nblk = (int)std::max<int64_t>(1, (npmax + 4095) / 4096);
+  // device scratch: the blocks of the previous call are reused in allocation
+  // order (grown when too small), so repeated drop-in calls do no cudaMalloc /
+  // cudaFree (each a device synchronisation); calls are serialised, and each
+  // call synchronises its stream before it returns
+  static std::mutex scratch_mu;
+  static std::vector<std::pair<void*, size_t>> scratch;
+  std::lock_guard<std::mutex> scratch_lock(scratch_mu);
   std::vector<void*> mem;
+  size_t n_get = 0;
   auto get = [&](size_t bytes) -> void* {
-    void* q = nullptr;
-    if (cudaMalloc(&q, std::max<size_t>(bytes, 8)) != cudaSuccess) return nullptr;
-    mem.push_back(q);
-    return q;
+    bytes = (std::max<size_t>(bytes, 8) + 255) & ~(size_t)255;
+    if (n_get == scratch.size()) scratch.push_back({nullptr, 0});
+    auto& blk = scratch[n_get++];
+    if (blk.second < bytes) {
+      if (blk.first) cudaFree(blk.first);
+      blk = {nullptr, 0};
+      void* q = nullptr;
+      if (cudaMalloc(&q, bytes) == cudaSuccess) blk = {q, bytes};
+    }
+    mem.push_back(blk.first);
+    return blk.first;
   };
   PairTable t;
   t.ii = (int32_t*)get(npmax * 4);
@@ -1209,7 +1225,7 @@ int vk_fit_variogram_samples(const double* coords, const double* values, int64_t
   int32_t* zero32 = (int32_t*)get(8);
   int64_t* zero64 = (int64_t*)get(8);
   int64_t* mm = (int64_t*)get(8);
-  auto cleanup = [&]() { for (void* q : mem) cudaFree(q); };
+  auto cleanup = [&]() {};                     // scratch stays cached for the next call
   for (void* q : mem)
     if (!q) { cleanup(); return set_err(VK_E_CUDA, "cudaMalloc failed"); }
   cudaError_t e = cudaMemcpyAsync(d_t, &t, sizeof(PairTable), cudaMemcpyHostToDevice, st);
