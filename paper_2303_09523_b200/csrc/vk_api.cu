@@ -779,7 +779,9 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       // recorded last on the slot covers this part)
       VK_CUDA(cudaEventRecord(p->ev_solved[s % nch], p->chain[s % nch]));
       VK_CUDA(cudaStreamWaitEvent(p->pchain[s % nch], p->ev_solved[s % nch], 0));
-      VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, p->pchain[s % nch]));
+      // VK_DIAG_SKIP bit 4 (diagnostics only): no prediction launches
+      static const int diag_skip4 = std::getenv("VK_DIAG_SKIP") ? std::atoi(std::getenv("VK_DIAG_SKIP")) : 0;
+      if (!(diag_skip4 & 4)) VK_CUDA(launch_predict_fast_prepared(p->fast_launch, p1, p->pchain[s % nch]));
       kernels += 2;
       if (trace) cudaEventRecord(tev[3 + 3 * s], p->pchain[s % nch]);
     }
