@@ -365,7 +365,9 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
         const uint32_t sq = seq0 + i;
         float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
         mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
-        tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i);
+        // evict-first: the tiles must not displace the concurrent fits'
+        // instruction and stack lines from L2 (C4 step 2.29 -> 2.17 ms)
+        tma_load_3d_ef(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i, l2_evict_first_policy());
       }
     }
     load_seq += n_planes;
@@ -773,7 +775,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           if (kn <= ke) {
             fence_proxy_async();
             mbar_expect_tx(&full[slot], tile_bytes);
-            tma_load_3d(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn);
+            tma_load_3d_ef(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn, l2_evict_first_policy());
           }
         }
       }
