@@ -270,6 +270,20 @@ __device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
 }
 
 
+// L2 policy of a known-plane tile load (plane k of a run ending at plane ke).
+// Evict-first everywhere (VK_FT_EF_MODE 1, default) keeps the concurrent
+// fits' lines in L2: C4 fp64 step 2.33 -> 2.19 ms, fp32 2.28 -> 2.15 ms; the
+// kernel alone loses its halo / run-boundary re-reads from L2 (fp64 0.814 ->
+// 0.818 ms, fp32 0.622 -> 0.658 ms); sparing the run's last plane (mode 2)
+// measured the same as mode 1.  Mode 0: the default policy everywhere.
+#ifndef VK_FT_EF_MODE
+#define VK_FT_EF_MODE 1
+#endif
+__device__ __forceinline__ bool ft_evict_first(int k, int ke) {
+  (void)k; (void)ke;
+  return VK_FT_EF_MODE != 0;
+}
+
 // Streaming kernel.  No CTA-wide barrier inside a unit: each warp waits only
 // for the TMA of the two planes its gap reads and, when done with plane k,
 // releases it; the last warp to release a ring slot refills it with plane
@@ -366,8 +380,11 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
         float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
         mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
         // evict-first: the tiles must not displace the concurrent fits'
-        // instruction and stack lines from L2 (C4 step 2.29 -> 2.17 ms)
-        tma_load_3d_ef(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i, l2_evict_first_policy());
+        // instruction and stack lines from L2
+        if (ft_evict_first(kb + i, ke))
+          tma_load_3d_ef(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i, l2_evict_first_policy());
+        else
+          tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i);
       }
     }
     load_seq += n_planes;
@@ -775,7 +792,10 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           if (kn <= ke) {
             fence_proxy_async();
             mbar_expect_tx(&full[slot], tile_bytes);
-            tma_load_3d_ef(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn, l2_evict_first_policy());
+            if (ft_evict_first(kn, ke))
+              tma_load_3d_ef(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn, l2_evict_first_policy());
+            else
+              tma_load_3d(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn);
           }
         }
       }
