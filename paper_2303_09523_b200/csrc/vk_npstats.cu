@@ -102,6 +102,9 @@ __device__ __forceinline__ double np_leaf_sum(const NpVarArgs& a, int64_t g, int
 // leaf), then lane 0 adds the subtree's internal nodes in height order from
 // shared memory; the root's value goes to a.leaf for the top-tree kernel.
 constexpr int NPW_WARPS = 8;
+#ifndef VK_NPW_PAIR
+#define VK_NPW_PAIR 1
+#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(32 * NPW_WARPS) npsum_warp_kernel(NpVarArgs a) {
@@ -115,13 +118,68 @@ __global__ void __launch_bounds__(32 * NPW_WARPS) npsum_warp_kernel(NpVarArgs a)
   if (r >= T.nleaf) return;
   const int l0 = T.wr_leaf[r], nl = T.wr_leaf[r + 1] - l0;
   const double mean = MODE ? a.mean[s] : 0.0;
-  double v = 0.0;
-  if (lane < nl) {
-    const int o = T.leaf_off[l0 + lane];
-    v = np_leaf_sum<MODE>(a, a.part_base[s] + o, T.leaf_off[l0 + lane + 1] - o, mean);
-  }
   __shared__ double val[NPW_WARPS][64];
-  val[warp][lane] = v;
+#if VK_NPW_PAIR
+  // two lanes per leaf, sixteen leaves per round: lane h of a leaf holds
+  // numpy's accumulators r[4h .. 4h+3] and reads their four columns of every
+  // eight-element row with one 16-byte load, so a load instruction touches
+  // sixteen 32-byte sectors (a lane per leaf touched 32 lines per
+  // instruction and was bound by L1 tag throughput at ~3 TB/s)
+  {
+    const int h = lane & 1;
+    auto f = [&](float x) -> double {
+      const double v = (double)x;
+      if (MODE == 0) return v;
+      const double t = __dsub_rn(v, mean);
+      return __dmul_rn(t, t);
+    };
+    const int64_t base = a.part_base[s];
+    for (int l = lane >> 1; l < ((nl + 15) & ~15); l += 16) {
+      const bool act = l < nl;
+      int o = 0, n = 0;
+      if (act) {
+        o = T.leaf_off[l0 + l];
+        n = T.leaf_off[l0 + l + 1] - o;
+      }
+      const int64_t g = base + o;
+      const int n8 = n - n % 8;
+      const bool vec = act && !a.values && (g & 3) == 0 && n >= 8;
+      double part = 0.0;
+      if (vec) {
+        const float4* p = reinterpret_cast<const float4*>(a.known + g) + h;
+        float4 x = __ldg(p);
+        double r0 = f(x.x), r1 = f(x.y), r2 = f(x.z), r3 = f(x.w);
+#pragma unroll 4
+        for (int q = 1; q < n8 / 8; ++q) {
+          x = __ldg(p + 2 * q);
+          r0 = __dadd_rn(r0, f(x.x)); r1 = __dadd_rn(r1, f(x.y));
+          r2 = __dadd_rn(r2, f(x.z)); r3 = __dadd_rn(r3, f(x.w));
+        }
+        part = __dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3));   // (r0+r1)+(r2+r3) / (r4+r5)+(r6+r7)
+      }
+      const double other = __shfl_down_sync(0xffffffffu, part, 1);
+      if (act && h == 0) {
+        double res;
+        if (vec) {
+          res = __dadd_rn(part, other);
+          for (int i = n8; i < n; ++i) res = __dadd_rn(res, f(__ldg(a.known + g + i)));
+        } else {
+          res = np_leaf_sum<MODE>(a, g, n, mean);          // explicit samples / unaligned / n < 8
+        }
+        val[warp][l] = res;
+      }
+    }
+  }
+#else
+  {
+    double v = 0.0;
+    if (lane < nl) {
+      const int o = T.leaf_off[l0 + lane];
+      v = np_leaf_sum<MODE>(a, a.part_base[s] + o, T.leaf_off[l0 + lane + 1] - o, mean);
+    }
+    val[warp][lane] = v;
+  }
+#endif
   __syncwarp();
   if (lane == 0) {
     const int ni = T.wr_nint[r];
