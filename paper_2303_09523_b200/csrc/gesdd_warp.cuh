@@ -20,6 +20,12 @@
 namespace vk {
 namespace lapack {
 
+// svd_m3_2w: the 3 x 3 stages' results, from warp 1 to both warps
+struct SvdXchg {
+  double d[3], Ub[9], VTb[9];
+  int info;
+};
+
 struct SvdWarpSmem {
   double A[GMAXM * 3];        // column-major, lda = M
   double U[GMAXM * 3];        // row-major result
@@ -252,6 +258,98 @@ VK_DN int svd_m3_warp(const double* A_rm, int M, double* U_rm, double* s, double
   for (int i = 0; i < N; ++i) {
     s[i] = d[i];
     for (int j = 0; j < N; ++j) VT_rm[i * N + j] = VTb[i + j * N];
+  }
+  __syncwarp();
+  VK_TACC(11, t5);
+  return 0;
+}
+
+// Two-warp form of svd_m3_warp (same operations, same bits): both warps run
+// the Householder QR on their own copy of the matrix, then warp 0 forms Q
+// (dorg2r) while warp 1 runs the 3 x 3 stages (dgebd2, dbdsdc, dormbr x 2);
+// after one CTA barrier each warp forms U = Q U_B from warp 0's Q and warp
+// 1's U_B.  Called by both warps of the fit CTA with their own `sm` (`other`
+// is the other warp's).  A warp rewrites its Q / the exchange only in its
+// next call, after the caller's next CTA barrier (trf_warp.cuh).
+VK_DN int svd_m3_2w(const double* A_rm, int M, double* U_rm, double* s, double* VT_rm, SvdWarpSmem& sm,
+                    const SvdWarpSmem& other, SvdXchg& xc, int lane, int wid) {
+  const int N = 3;
+  double* A = sm.A;
+  VK_TP(t0);
+  for (int t = lane; t < M * N; t += 32) {
+    const int r = t / N, c = t - r * N;
+    A[r + c * M] = A_rm[t];
+  }
+  __syncwarp();
+  double tau[3];
+  // dgeqr2
+  for (int i = 0; i < N; ++i) {
+    dlarfg_warp(M - i, &A[i + i * M], &A[(i + 1 < M ? i + 1 : M - 1) + i * M], &tau[i], sm, lane);
+    if (i < N - 1) {
+      const double aii = A[i + i * M];
+      __syncwarp();
+      if (lane == 0) A[i + i * M] = 1.0;
+      __syncwarp();
+      VK_TP(tl);
+      dlarf_left_warp(M - i, N - i - 1, &A[i + i * M], tau[i], &A[i + (i + 1) * M], M, lane);
+      VK_TACC(15, tl);
+      if (lane == 0) A[i + i * M] = aii;
+      __syncwarp();
+    }
+  }
+  VK_TACC(8, t0);
+  VK_TP(t1);
+  double R[9];
+  for (int j = 0; j < N; ++j)
+    for (int i = 0; i < N; ++i) R[i + j * N] = (i <= j) ? A[i + j * M] : 0.0;
+  __syncwarp();
+  if (wid == 0) {
+    // dorg2r(M, 3, 3)
+    for (int i = N - 1; i >= 0; --i) {
+      if (i < N - 1) {
+        if (lane == 0) A[i + i * M] = 1.0;
+        __syncwarp();
+        dlarf_left_warp(M - i, N - i - 1, &A[i + i * M], tau[i], &A[i + (i + 1) * M], M, lane);
+      }
+      if (i < M - 1) dscal_warp(M - i - 1, -tau[i], &A[i + 1 + i * M], lane);
+      if (lane == 0) A[i + i * M] = sub(1.0, tau[i]);
+      if (lane < i) A[lane + i * M] = 0.0;
+      __syncwarp();
+    }
+    VK_TACC(9, t1);
+  } else {
+    // the 3 x 3 stages, redundantly on every lane of warp 1
+    double d[3], e[3], tauq[3], taup[3];
+    dgebd2(N, N, R, N, d, e, tauq, taup);
+    double Ub[9], VTb[9];
+    const int info = dbdsdc(N, d, e, Ub, N, VTb, N);
+    if (!info) {
+      dorm2r_ln(N, N, N, R, N, tauq, Ub, N);
+      dorml2_rn(N, N - 1, N - 1, &R[0 + 1 * N], N, taup, &VTb[0 + 1 * N], N);
+    }
+    if (lane == 0) {
+      xc.info = info;
+      for (int i = 0; i < 3; ++i) xc.d[i] = d[i];
+      for (int i = 0; i < 9; ++i) { xc.Ub[i] = Ub[i]; xc.VTb[i] = VTb[i]; }
+    }
+  }
+  __syncthreads();                                   // Q and the 3 x 3 results visible to both warps
+  if (xc.info) return xc.info;
+  VK_TP(t5);
+  // dgemm('N','N', M, 3, 3, 1, Q, Ub, 0, U)
+  const double* Q = wid == 0 ? A : other.A;
+  for (int t = lane; t < M * N; t += 32) {
+    const int i = t / N, j = t - i * N;
+    double c = mul(Q[i + 0 * M], xc.Ub[0 + j * N]);
+    c = fma_(Q[i + 1 * M], xc.Ub[1 + j * N], c);
+    c = fma_(Q[i + 2 * M], xc.Ub[2 + j * N], c);
+    sm.U[t] = c;
+  }
+  __syncwarp();
+  for (int t = 0; t < M * N; ++t) U_rm[t] = sm.U[t];
+  for (int i = 0; i < N; ++i) {
+    s[i] = xc.d[i];
+    for (int j = 0; j < N; ++j) VT_rm[i * N + j] = xc.VTb[i + j * N];
   }
   __syncwarp();
   VK_TACC(11, t5);

@@ -54,6 +54,7 @@ struct TrfWork {
   double f[MAX_BINS], J[MAX_BINS * 3], Ja[TRF_MAXM * 3], U[TRF_MAXM * 3];
   double f_new[MAX_BINS], fa[TRF_MAXM];
   double q1[MAX_BINS], q2[MAX_BINS];   // evaluate_quadratic / build_quadratic_1d rows
+  double J_new[MAX_BINS * 3];          // Jacobian at the trial point (speculative)
 };
 
 VK_HD bool finite_d(double v) { return v - v == 0.0; }
@@ -131,6 +132,12 @@ struct TrfScalarEval {
   // numpy.linalg.svd of the augmented Jacobian (gesdd.h)
   VK_HD int svd(const double* A, int M, double* U, double* s, double* VT) const {
     return lapack::svd_m3(A, M, U, s, VT);
+  }
+  // the residuals at a trial point and, speculatively, the Jacobian there
+  // (used only if the step is accepted: then it is jac(x_new, f_new))
+  VK_HD void resid_spec(const double* x, const double* lb, const double* ub, double* f, double* J) const {
+    resid(x, f);
+    jac(x, f, lb, ub, J);
   }
   VK_HD void jac(const double* x, const double* f0, const double* lb, const double* ub, double* J) const {
     double f1[MAX_BINS];
@@ -488,8 +495,8 @@ __device__ unsigned long long g_fit_prof[16];
 #endif
 #if defined(VK_FIT_PROFILE) && defined(__CUDA_ARCH__)
 #define VK_TP(v) const long long v = clock64()
-#define VK_TACC(slot, a) if ((threadIdx.x & 31) == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)(clock64() - (a)))
-#define VK_TADD(slot, n) if ((threadIdx.x & 31) == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)(n))
+#define VK_TACC(slot, a) if (threadIdx.x == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)(clock64() - (a)))
+#define VK_TADD(slot, n) if (threadIdx.x == 0) atomicAdd(&g_fit_prof[slot], (unsigned long long)(n))
 #else
 #define VK_TP(v)
 #define VK_TACC(slot, a)
@@ -599,7 +606,10 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
       for (int i = 0; i < 3; ++i) x_new[i] = np::add(x[i], step[i]);
       make_strictly_feasible(x_new, lb, ub, 0.0);
       VK_TP(t_res);
-      ev.resid(x_new, f_new);
+      // residuals at the trial point together with the Jacobian there: an
+      // evaluator with spare lanes computes both in one round, and an
+      // accepted step (most of them) then needs no Jacobian evaluation
+      ev.resid_spec(x_new, lb, ub, f_new, w.J_new);
       VK_TACC(0, t_res);
       nfev += 1;
       const double step_h_norm = np::norm(step_h, 3);
@@ -632,7 +642,7 @@ VK_HD TrfResult trf_fit_t(const Eval& ev, const double* x0_in, const double* lb,
       for (int r = 0; r < m; ++r) f[r] = f_new[r];
       cost = cost_new;
       VK_TP(t_jac);
-      ev.jac(x, f, lb, ub, J);
+      for (int k = 0; k < 3 * m; ++k) J[k] = w.J_new[k];    // jac(x, f): evaluated with the step
       trf_grad(J, f, m, g);
       VK_TACC(1, t_jac);
     }

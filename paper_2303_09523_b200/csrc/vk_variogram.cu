@@ -365,12 +365,15 @@ __global__ void __launch_bounds__(256) bins_kernel(BinsArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
-  // One warp per sub-part.  Statistics are merged redundantly by every lane
-  // (same order -> same bits); bins are reduced lane-per-bin; the TRF runs
-  // redundantly on every lane with residual rows evaluated lane-parallel
-  // (trf_warp.cuh).
-  const int s = a.part0 + blockIdx.x, lane = threadIdx.x;
+__global__ void __launch_bounds__(FIT_THREADS) fit_kernel(FitArgs a) {
+  // One CTA of FIT_WARPS warps per sub-part.  Statistics are merged
+  // redundantly by every warp (same order -> same bits); bins are reduced
+  // lane-per-bin; the TRF runs redundantly on every thread with residual
+  // rows, Jacobian columns and the SVD's independent stages spread over the
+  // threads (trf_warp.cuh).
+  if ((int)threadIdx.x >= FIT_THREADS) return;
+  const int s = a.part0 + blockIdx.x, lane = threadIdx.x & 31;
+  const bool lead = threadIdx.x == 0;
   __shared__ TrfProblem P;
   // Chan merge of the part's chunk statistics: lanes merge strided chunks,
   // then a butterfly merges lanes in a canonical (lower, upper) order so every
@@ -408,24 +411,24 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
       merge(n, mean, m2, on, om, oq);
     }
   }
-  if (lane == 0) {
+  if (lead) {
     a.lohi[2 * s + 0] = mn;
     a.lohi[2 * s + 1] = mx;
   }
   int status = PS_OK;
   if (bad > 0) status = PS_NONFINITE;
   else if (n <= 0) status = PS_FIT_FAILED;
-  if (!a.fit) { if (lane == 0) a.status[s] = status; return; }
+  if (!a.fit) { if (lead) a.status[s] = status; return; }
   const double svar = a.svar ? a.svar[s] : m2 / n;
   const int64_t m = a.part_m[s];
-  if (m * (m - 1) / 2 < 30) { if (lane == 0) a.status[s] = PS_INSUFFICIENT; return; }
+  if (m * (m - 1) / 2 < 30) { if (lead) a.status[s] = PS_INSUFFICIENT; return; }
   const PairTable t = a.tables[a.part_class[s]];
-  if (t.scal[3] != 0.0) { if (lane == 0) a.status[s] = PS_PAIRS_SHORT; return; }
+  if (t.scal[3] != 0.0) { if (lead) a.status[s] = PS_PAIRS_SHORT; return; }
   const double hmax = t.scal[0];
-  if (!(hmax > 0.0)) { if (lane == 0) a.status[s] = PS_DEGENERATE; return; }
+  if (!(hmax > 0.0)) { if (lead) a.status[s] = PS_DEGENERATE; return; }
   double* model = a.models + 3 * s;
   if (svar == 0.0) {                    // kriging.py:294-297
-    if (lane == 0) {
+    if (lead) {
       model[0] = 0.0; model[1] = 0.0; model[2] = fmax(t.scal[1], 1.0);
       a.status[s] = status;
     }
@@ -448,18 +451,16 @@ __global__ void __launch_bounds__(32) fit_kernel(FitArgs a) {
     P.gemp[r] = sum / (double)cnt;
     P.w[r] = sqrt((double)cnt);
   }
-  if (lane == 0) { P.kind = a.kind; P.nb = __popc(nzmask); }
-  __syncwarp();
+  if (lane == 0) { P.kind = a.kind; P.nb = __popc(nzmask); }   // identical from both warps
+  __syncthreads();
   const double x0[3] = {0.0, svar, hmax / 3.0};
   const double lb[3] = {0.0, 0.0, 1e-6};
   const double ub[3] = {2.0 * svar + 1e-12, 4.0 * svar + 1e-12, 10.0 * hmax};
-  if (!(ub[2] > lb[2])) { if (lane == 0) a.status[s] = PS_FIT_FAILED; return; }
-  __shared__ double rowbuf[3 * MAX_BINS];
-  __shared__ lapack::SvdWarpSmem svsm;
-  __shared__ TrfWork wk;
+  if (!(ub[2] > lb[2])) { if (lead) a.status[s] = PS_FIT_FAILED; return; }
+  __shared__ FitShared fsh;
   TrfResult r;
-  r = trf_fit_t(WarpEval(P, rowbuf, svsm, wk, lane), x0, lb, ub);
-  if (lane != 0) return;
+  r = trf_fit_t(WarpEval(P, fsh, threadIdx.x), x0, lb, ub);
+  if (!lead) return;
   if (r.status < 0) { a.status[s] = PS_FIT_FAILED; return; }
   const double nug = pymax(r.x[0], 0.0);
   model[0] = nug;
@@ -759,7 +760,7 @@ cudaError_t launch_fit(const FitArgs& a, cudaStream_t st) {
       set_to = a.reserve_smem;
     }
   }
-  fit_kernel<<<a.n_parts, 32, a.reserve_smem, st>>>(a);
+  fit_kernel<<<a.n_parts, FIT_THREADS, a.reserve_smem, st>>>(a);
   return cudaGetLastError();
 }
 
