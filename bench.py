@@ -16,9 +16,11 @@ serial-schedule pass).  Scaling is weak: under torchrun
 every rank owns its own 256-slice stack and receives a one-slice halo from
 the next rank over NCCL inside the timed step.
 
-``--impl reference`` times the reference algorithm on the host cores instead
-(the oracle port of volkrig's fit_variogram + fill_missing, multiprocessing
-over sub-parts, a bounded sample of the same workload per step).
+``--impl reference`` times the reference on the host cores instead: the
+unmodified volkrig ``fit_variogram`` + ``fill_missing`` per Z sub-part from
+the git-ignored ``baseline/_ref`` install (``tools/vendor_ref.py``), a process
+pool over sub-parts, a bounded sample of the same workload per step; without
+that install it falls back to the oracle port and labels the line "port".
 """
 
 from __future__ import annotations
@@ -136,23 +138,55 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-# CPU reference arm (oracle port of the reference algorithm)
+# CPU reference arm: the unmodified reference (volkrig, installed into the
+# git-ignored baseline/_ref by tools/vendor_ref.py) when it is there, else the
+# oracle port of its algorithm (labelled "port")
 # --------------------------------------------------------------------------
+
+REF_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+
+
+def cpu_kind() -> str:
+    """"reference" when the vendored volkrig is present, else "port"."""
+    return "reference" if os.path.isfile(os.path.join(REF_DIR, "volkrig", "kriging.py")) else "port"
+
 
 def _cpu_worker(args):
     os.environ["OMP_NUM_THREADS"] = "1"
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    from oracle import kriging_oracle as O
     slices, b, e, factor, drift = args
+    if cpu_kind() == "reference":
+        # what the reference's reconstruct_block does per Z sub-part
+        # (SPEC.md:401-404): fit_variogram on the known voxels, fill_missing
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from volkrig.kriging import fill_missing, fit_variogram
+        from volkrig.model import VolumeGrid
+        nk = e - b + 1
+        data = np.full(((nk - 1) * factor + 1,) + slices.shape[1:], np.nan, dtype=np.float32)
+        data[::factor] = slices[b:e + 1]
+        grid = VolumeGrid(data)
+        kz, ky, kx = np.nonzero(~grid.missing_mask)
+        coords = np.column_stack([kx, ky, kz]).astype(np.float64)
+        model = fit_variogram((coords, data[kz, ky, kx].astype(np.float64)))
+        out = fill_missing(grid, model, drift=drift)
+        return out.data.shape[0]
+    from oracle import kriging_oracle as O
     out, _, _ = O.reconstruct_zpart(slices, b, e, factor, drift=drift)
     return out.shape[0]
 
 
+def _subpart_ranges(k, n_parts):
+    """Equal Z sub-parts of k known slices, each with its trailing halo slice
+    (the reference's split; same as zshard / the oracle)."""
+    from paper_2303_09523_b200.block_pipeline import subpart_ranges
+    return subpart_ranges(k, n_parts)
+
+
 def cpu_reference_sample(ks, factor, n_parts, cores, pool=None, n_sample=None, drift="linear"):
-    """Run the reference algorithm on a bounded sample of sub-parts with a
+    """Run the reference (or its port) on a bounded sample of sub-parts with a
     process pool; returns (voxels, seconds, sample description)."""
-    from oracle import kriging_oracle as O
-    ranges = O.subpart_ranges(ks.shape[0], n_parts)
+    ranges = _subpart_ranges(ks.shape[0], n_parts)
     n_sample = n_sample or min(len(ranges), cores)
     sel = ranges[:n_sample]
     H, W = ks.shape[1:]
@@ -165,7 +199,8 @@ def cpu_reference_sample(ks, factor, n_parts, cores, pool=None, n_sample=None, d
     else:
         pool.map(_cpu_worker, jobs)
     dt = time.perf_counter() - t0
-    return vox, dt, f"{n_sample} of {n_parts} sub-parts ({vox} voxels), pool of {cores}"
+    who = "volkrig fit_variogram + fill_missing" if cpu_kind() == "reference" else "oracle port"
+    return vox, dt, f"{who}: {n_sample} of {n_parts} sub-parts ({vox} voxels), pool of {cores}"
 
 
 def _host_cores() -> int:
@@ -202,7 +237,7 @@ def run_reference(args, cfg, ks):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": _data_desc(cfg),
         "config": _config(cfg, args, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": cpu_kind(),
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -399,7 +434,7 @@ def run_gpu(args, cfg, ks):
             pool.map(_cpu_worker, [(ks[:2].copy(), 0, 1, cfg.factor, args.drift)] * cores)
             v, dt, sample = cpu_reference_sample(ks, cfg.factor, cfg.n_subparts, cores, pool,
                                                  drift=args.drift)
-        cpu = {"value": v / dt, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        cpu = {"value": v / dt, "unit": UNIT, "cores": cores, "kind": cpu_kind(), "sample": sample}
 
     scaling = "weak"
     if args.scaling == "strong":
