@@ -189,6 +189,14 @@ int vk_grid_scan(const float* data, const uint8_t* mask, int64_t planes,
 int vk_gather_planes(const float* src, const int32_t* known_z, int32_t K,
                      int64_t plane_elems, float* dst, void* stream);
 
+/* Host -> device copy of a caller-owned (pageable) host buffer through a
+ * ring of page-locked staging chunks filled by host threads while the DMA of
+ * the previous chunk runs (replaces the driver's ~11 GB/s pageable copy for
+ * the drop-in entry points, whose inputs are numpy arrays: fit_variogram
+ * samples, kriging.py:264; fill_missing grids, kriging.py:458).  Enqueued on
+ * `stream`; returns once `src` may be reused. */
+int vk_copy_h2d(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Generic per-voxel fill for masks that are not whole known / missing
  * planes: the reference's fallback _predict_generic (kriging.py:408-431,
  * window schedule kriging.py:37-40, _gather_window kriging.py:345-357,

@@ -87,6 +87,7 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vk_solve_systems": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vk_copy_h2d": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "vk_plan_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vk_crc32": (C.c_int, [C.c_void_p, C.c_int64, C.c_uint32, C.POINTER(C.c_uint32), C.c_void_p]),
     "vk_packbits": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),

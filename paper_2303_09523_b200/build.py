@@ -34,6 +34,7 @@ UNITS = {
     "vk_volio.cu": [],
     "vk_geometry.cpp": [],
     "vk_comm.cpp": [],
+    "vk_hostio.cpp": [],
 }
 
 
@@ -62,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", str(INCLUDE), "-I", str(CSRC), *extra, *exp, "-c", str(src),
                "-o", str(obj)]
-        if unit.endswith(".cpp") and unit != "vk_comm.cpp":
+        if unit.endswith(".cpp") and unit not in ("vk_comm.cpp", "vk_hostio.cpp"):
             cmd.insert(1, "-x")
             cmd.insert(2, "cu")
         if verbose:

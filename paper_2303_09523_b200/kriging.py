@@ -82,6 +82,20 @@ def _stream_handle(stream) -> int:
     return int(s.cuda_stream)
 
 
+def _upload(arr: np.ndarray):
+    """A device copy of a host numpy array through the library's staged
+    uploader (``vk_copy_h2d``: page-locked chunks filled by host threads while
+    the previous chunk's DMA runs), on torch's current stream."""
+    torch = _torch()
+    arr = np.ascontiguousarray(arr)
+    dt = torch.from_numpy(arr[:0]).dtype
+    out = torch.empty(arr.shape, dtype=dt, device="cuda")
+    if arr.nbytes:
+        raise_for_status(_lib.load().vk_copy_h2d(out.data_ptr(), arr.ctypes.data, arr.nbytes,
+                                                 _stream_handle(None)))
+    return out
+
+
 def _model_params(model):
     """(kind, [nugget, sill, range_len]) of any object with the reference
     VariogramModel's attributes (kriging.py:44-57) -- ours or volkrig's."""
@@ -316,8 +330,8 @@ def fit_variogram(samples, kind: str = "exponential", n_bins: int = 15,
         raise InsufficientSamples(f"{m} samples give {m * (m - 1) // 2} pairs; need >= 30")
     torch = _torch()
     lib = _lib.load()
-    c_d = torch.from_numpy(np.ascontiguousarray(coords)).cuda()
-    v_d = torch.from_numpy(np.ascontiguousarray(values)).cuda()
+    c_d = _upload(coords)
+    v_d = _upload(values)
     out = np.zeros(3)
     raise_for_status(lib.vk_fit_variogram_samples(
         c_d.data_ptr(), v_d.data_ptr(), m, _lib.KIND_IDS[kind], int(n_bins),
@@ -464,8 +478,8 @@ def fill_missing(grid: VolumeGrid, model: VariogramModel, drift="linear",
     if on_dev:
         data_d, mask_d = data, mask.view(torch.uint8)
     else:
-        data_d = torch.from_numpy(data).cuda()
-        mask_d = torch.from_numpy(mask.view(np.uint8)).cuda()
+        data_d = _upload(data)
+        mask_d = _upload(mask.view(np.uint8))
     T, H, W = data_d.shape
     counts = _scan_grid(data_d, mask_d)
     if counts[:, 2].any():

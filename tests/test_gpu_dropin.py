@@ -13,6 +13,8 @@ Also: a plane mask whose z window reaches more than NPMAX = 8 known planes
 matches the oracle.
 """
 
+import os
+import sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -57,15 +59,29 @@ def _grid(seed=3, T=13, H=24, W=32, f=4):
     return data, mask
 
 
+REF_INSTALL = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def _volkrig():
+    """The unmodified reference: the git-ignored baseline/_ref install that
+    travels with the snapshot (tools/vendor_ref.py), else the mounted source
+    tree (build container); None when neither is there."""
+    for path in (REF_INSTALL, "/root/reference/pkg/src"):
+        if os.path.isfile(os.path.join(path, "volkrig", "kriging.py")):
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            try:
+                import volkrig.kriging as K
+                import volkrig.model as M
+                return K, M
+            except Exception:
+                return None
+    return None
+
+
 def _reference_classes():
-    try:
-        import sys
-        sys.path.insert(0, "/root/reference/pkg/src")
-        from volkrig.kriging import VariogramModel as RM
-        from volkrig.model import VolumeGrid as RG
-        return [(RG, RM)]
-    except Exception:
-        return []
+    vk = _volkrig()
+    return [(vk[1].VolumeGrid, vk[0].VariogramModel)] if vk else []
 
 
 @pytest.mark.parametrize("classes", [(RefGrid, RefModel)] + _reference_classes(),
@@ -126,3 +142,53 @@ def test_plane_mask_beyond_npmax_takes_the_per_voxel_path(cuda):
     exp, _ = O.fill_missing(data, mask, O.Model("exponential", 0.5, 150.0, 8.0))
     rng_ = float(np.nanmax(data) - np.nanmin(data))
     assert np.abs(got.data.astype(np.float64) - exp).max() <= 1e-6 * rng_
+
+
+def test_integration_switch_against_the_live_reference(cuda):
+    """INTEGRATION.md section 1 verbatim on the unmodified reference: its own
+    VolumeGrid and its own fit_variogram output go into our fill_missing; the
+    result matches the reference's fill_missing at the fp64 gate, and our
+    fit_variogram reproduces its fit (kriging.py:264-328, 458-496)."""
+    vk = _volkrig()
+    if vk is None:
+        pytest.skip("reference not installed (python tools/vendor_ref.py)")
+    K, M = vk
+    from paper_2303_09523_b200 import fill_missing, fit_variogram
+    for seed, drift in ((21, "linear"), (22, "constant")):
+        data, mask = _grid(seed=seed)
+        grid = M.VolumeGrid(data.copy(), mask.copy())
+        kz, ky, kx = np.nonzero(~mask)
+        samples = (np.column_stack([kx, ky, kz]).astype(np.float64), data[kz, ky, kx].astype(np.float64))
+        ref_model = K.fit_variogram(samples)
+        expect = K.fill_missing(grid, ref_model, drift=drift)
+        got = fill_missing(grid, ref_model, drift)
+        assert type(got) is M.VolumeGrid
+        rng = float(np.nanmax(data) - np.nanmin(data))
+        err = np.abs(got.data.astype(np.float64) - expect.data.astype(np.float64)).max()
+        assert err <= 1e-6 * rng, (seed, drift, err / rng)
+        known = ~mask
+        assert np.array_equal(got.data[known], expect.data[known])
+        ours = fit_variogram(samples)
+        assert abs(ours.nugget - ref_model.nugget) <= 1e-7 * ref_model.sill
+        assert abs(ours.sill - ref_model.sill) <= 1e-6 * ref_model.sill
+        assert abs(ours.range_len - ref_model.range_len) <= 1e-4 * ref_model.range_len
+
+
+@pytest.mark.parametrize("nbytes,offset", [(0, 0), (1, 3), (1 << 20, 0), ((1 << 20) - 1, 5),
+                                           ((4 << 20) + 3, 1), ((13 << 20) + 5, 7)])
+def test_staged_upload_is_byte_exact(cuda, nbytes, offset):
+    """vk_copy_h2d (the drop-in's host -> device path) at sizes around its
+    pageable / staged switch and its 4 MB chunks, from unaligned sources."""
+    import torch
+    from paper_2303_09523_b200 import _lib
+    from paper_2303_09523_b200.kriging import _stream_handle
+    rng = np.random.default_rng(nbytes)
+    buf = rng.integers(0, 256, nbytes + offset + 16, dtype=np.uint8)
+    src = buf[offset:offset + nbytes]
+    expect = src.copy()
+    dst = torch.full((nbytes + 16,), 0xAB, dtype=torch.uint8, device="cuda")
+    assert _lib.load().vk_copy_h2d(dst.data_ptr(), src.ctypes.data, nbytes, _stream_handle(None)) == 0
+    buf[offset:offset + nbytes] = 0                 # the source may be reused once the call returns
+    got = dst.cpu().numpy()
+    assert np.array_equal(got[:nbytes], expect)
+    assert (got[nbytes:] == 0xAB).all()
