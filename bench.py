@@ -623,8 +623,10 @@ def run_dropin(args, cfg, ks, n_sample=4, reps=2):
         inputs.append((VolumeGrid(data, mask), samples))
     vox = sum(int(g.missing_mask.sum()) for g, _ in inputs)
     g0, smp0 = inputs[0]
-    for g, smp in inputs:                      # plan cache, pinned host cache, scratch: warm
-        fill_missing(g, fit_variogram(smp, "exponential"), args.drift)
+    out = None
+    for _ in range(2):                         # plan cache, scratch, and the pinned host blocks
+        for g, smp in inputs:                  # of the steady state (the previous result is still
+            out = fill_missing(g, fit_variogram(smp, "exponential"), args.drift)   # held): warm
     torch.cuda.synchronize()
     t_fit = t_fill = 0.0
     t0 = time.perf_counter()

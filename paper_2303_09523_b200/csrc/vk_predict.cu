@@ -335,11 +335,25 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
   const int wx = warp % WX, wy = warp / WX;
   const int lc = lane + 32 * wx;                           // column group in the tile
 
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-    const int chunk_id = u / n_tiles, tile = u - chunk_id * n_tiles;
+  // Balanced static partition: the (tile, gap) items in tile-major order are
+  // split into gridDim.x contiguous ranges whose sizes differ by at most one
+  // gap; a CTA walks its range as units of <= `chunk` gaps of one tile (the
+  // host caps `chunk` so a unit spans <= FT_WPARTS parts).  (Round-robin units
+  // of a fixed length left C4's serial launch with 7 units on some CTAs and 6
+  // on most: ~12 % tail.)
+  const int n_gaps_all = a.gap1 - a.gap0;
+  const int64_t n_items = (int64_t)n_tiles * n_gaps_all;
+  int64_t it = n_items * blockIdx.x / gridDim.x;
+  const int64_t it_end = n_items * (blockIdx.x + 1) / gridDim.x;
+  (void)n_units;
+  for (int uc = 0; it < it_end; ++uc) {
+    const int tile = (int)(it / n_gaps_all);
+    const int kb = a.gap0 + (int)(it - (int64_t)tile * n_gaps_all);
+    const int64_t room = it_end - it;
+    const int ke = min(min(a.gap1, kb + chunk), room < chunk ? kb + (int)room : a.gap1);
+    it += ke - kb;                                         // gaps [kb, ke) of `tile`
     const int tx = tile % n_tiles_x, ty = tile / n_tiles_x;
     const int x0 = tx * FT_TX, y0 = ty * FT_TY;
-    const int kb = a.gap0 + chunk_id * chunk, ke = min(a.gap1, kb + chunk);   // gaps [kb, ke)
     const int ty1 = min(H, y0 + FT_TY), tx1 = min(W, x0 + FT_TX);
     int nbc = 0, bcol[3] = {0, 0, 0};                      // border columns in this tile
     int nky = 1, kyl[4] = {AXIS_INTERIOR, 0, 0, 0};        // row kinds: interior first
@@ -354,7 +368,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
     const int s_first = a.gap_part[kb];
     const int npu = a.gap_part[ke - 1] - s_first + 1;       // <= FT_WPARTS (host caps chunk)
     if (npu > FT_WPARTS) __trap();
-    Acc* sw = s_w[((u - blockIdx.x) / gridDim.x) & 1];
+    Acc* sw = s_w[uc & 1];
     {
       const int per_k = 16 * NSTP_S, n = npu * nky * per_k;
       for (int i = tid; i < n; i += FT_THREADS) {
@@ -879,15 +893,21 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   const int n_tiles = ntx * nty, n_gaps = a.gap1 - a.gap0;
   if (n_gaps <= 0) return cudaSuccess;
   const int resident = a.num_sms * fl.occ;
-  // gap runs: long enough to amortise the extra plane per run, short enough
-  // that (tiles x runs) covers the resident CTAs several times
-  int chunk = std::max(1, (int)((int64_t)n_tiles * n_gaps / ((int64_t)resident * 6)));
-  chunk = std::min(std::max(chunk, std::min(4, n_gaps)), n_gaps);
-  if (a.chunk > 0) chunk = std::min(a.chunk, n_gaps);
+  // a CTA's share of the (tile, gap) items is a contiguous range walked as
+  // units of <= chunk gaps of one tile; chunk <= max_chunk keeps a unit within
+  // FT_WPARTS parts.  An explicit a.chunk (per-part chains: half a part's
+  // gaps, so CTAs retire often) also sets the share; otherwise every resident
+  // CTA gets an equal share of at least 4 gaps (the extra plane per run).
+  const int64_t n_items = (int64_t)n_tiles * n_gaps;
+  int chunk = n_gaps;
   if (a.max_chunk > 0) chunk = std::min(chunk, a.max_chunk);
-  const int n_chunks = (n_gaps + chunk - 1) / chunk;
-  const int n_units = n_tiles * n_chunks;
-  const int grid = std::min(n_units, resident);
+  int64_t share = std::min(4, n_gaps);
+  if (a.chunk > 0) {
+    chunk = std::min(chunk, a.chunk);
+    share = chunk;
+  }
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(resident, (n_items + share - 1) / share));
+  const int n_units = 0;                   // unused by the balanced partition
   const int n_st = (a.part1 - a.part0) * a.NK * 16;
   if (n_st > 0) fast_stencil_kernel<G, Acc><<<(n_st + 255) / 256, 256, 0, st>>>(a);
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(fl.tmap);

@@ -75,6 +75,21 @@ def main():
     res["fill.d2h_pinned"] = t(lambda: torch.empty(tuple(out_d.shape), dtype=out_d.dtype,
                                                    pin_memory=True).copy_(out_d))
     res["fill.result_grid"] = t(lambda: KR._result(grid, out_d, None, False, (0, 0, 0), False))
+    # the bench's loop: 4 distinct sub-parts, 2 reps, per-call times
+    grids = []
+    for b in range(0, 4 * q, q):
+        d = np.full((q * cfg.factor + 1, cfg.height, cfg.width), np.nan, dtype=np.float32)
+        d[::cfg.factor] = ks[b:b + q + 1]
+        grids.append(VolumeGrid(d, np.isnan(d)))
+    seq = []
+    for _ in range(2):
+        for g in grids:
+            sync()
+            t0 = time.perf_counter()
+            o = fill_missing(g, model)
+            sync()
+            seq.append(round(1e3 * (time.perf_counter() - t0), 2))
+    res["fill_missing_bench_loop"] = seq
     res["bytes"] = {"coords": coords.nbytes, "values": values.nbytes, "data": data.nbytes,
                     "mask": mask.nbytes}
     print(json.dumps(res))
