@@ -91,7 +91,7 @@ struct vk_plan {
   int* d_inexact = nullptr;           // stats pass: any known value not an integer below 2^23
   uint32_t* d_fxb = nullptr;           // fixed path tables
   float *d_fxc = nullptr, *d_fxq = nullptr;
-  int max_chunk = 0;                  // fast path: a run of this many gaps spans <= 4 parts
+  int max_chunk = 0;                  // fast path: a run of this many gaps spans <= 3 parts
   int fit_reserve = 160 * 1024;       // overlapped schedule: smem a fit CTA reserves on its SM
   int32_t *d_part_status = nullptr, *d_sys_status = nullptr;
   std::vector<PairTable> tables;
@@ -419,14 +419,14 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
     for (int s = 0; s <= S; ++s) p->gap_begin[s] = (s < S) ? g.parts[s].b : g.K - 1;
     for (int s = 0; s < S; ++s) p->gap_begin[s] = std::min(p->gap_begin[s], g.K - 1);
     // shortest non-empty run of gaps owned by one part: a run of c gaps that
-    // touches 5 parts holds 3 of them whole, so c <= 3 * min_len + 1 keeps
-    // every unit within the kernel's 4 staged parts
+    // touches 4 parts holds 2 of them whole, so c <= 2 * min_len + 1 keeps
+    // every unit within the kernel's 3 staged parts (FT_WPARTS)
     int min_len = g.K;
     for (int k = 0, run = 0; k < g.K - 1; ++k) {
       ++run;
       if (k == g.K - 2 || g.gap_part[k + 1] != g.gap_part[k]) { min_len = std::min(min_len, run); run = 0; }
     }
-    p->max_chunk = 3 * std::max(1, min_len) + 1;
+    p->max_chunk = 2 * std::max(1, min_len) + 1;
   }
   if (const char* e = std::getenv("VK_FIT_RESERVE")) p->fit_reserve = std::atoi(e);   // tuning
   // per-part chains are the default schedule whenever there is more than one

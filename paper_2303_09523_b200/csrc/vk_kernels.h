@@ -207,7 +207,10 @@ struct PredictArgs {
   int num_sms;
 };
 // doubles the K+- table needs (fast path)
-inline size_t kpm_elems(int S, int NK) { return (size_t)S * (size_t)NK * 16 * 8; }
+// (the fp64 table [S][NK][16][8], then the exact-split interior stencils
+// [S][16][8] of (hi, lo) float pairs, vk_predict.cu split_stencil_kernel)
+VK_HD size_t split_table_offset(int S, int NK) { return (size_t)S * (size_t)NK * 16 * 8; }
+VK_HD size_t kpm_elems(int S, int NK) { return split_table_offset(S, NK) + (size_t)S * 16 * 8; }
 // Launch state of the streaming kernel prepared once per known-plane buffer:
 // TMA descriptor, occupancy-derived grid size.
 struct FastLaunch {

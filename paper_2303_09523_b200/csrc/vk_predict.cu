@@ -127,7 +127,8 @@ __host__ __device__ constexpr int ft_stages(int G, bool f32 = false) {
 __host__ __device__ constexpr int ft_minb(int G, bool f32 = false) {
   return (G <= 4 || (f32 && VK_FT_F32_MINB3)) ? 3 : VK_FT_MINB;
 }
-constexpr int FT_WPARTS = 4;             // parts whose stencils a unit stages
+constexpr int FT_WPARTS = 3;             // parts whose stencils a unit stages (host:
+                                         // max_chunk = 2 * shortest part run + 1)
 
 template <typename Acc>
 struct AccVec;
@@ -184,6 +185,9 @@ __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
 #endif
 #ifndef VK_FT_SYM32
 #define VK_FT_SYM32 1                    // x<->y symmetric interior rows in the fp32 kernel
+#endif
+#ifndef VK_FT_SPLIT
+#define VK_FT_SPLIT 1                    // fp64 kernel: exact-split FFMA2 symmetric rows (integer planes)
 #endif
 #ifndef VK_FT_SYM32_MAXG
 #define VK_FT_SYM32_MAXG 4               // ... for gaps of up to this many missing planes
@@ -256,6 +260,69 @@ __global__ void __launch_bounds__(256) fast_stencil_kernel(PredictArgs a) {
   }
 }
 
+// Exact-split stencils for the fp64 symmetric rows (integer planes).  For
+// each mirror pair j of part s (interior kind) the stencils K+_j, K-_j are
+// split as K = Kh + Kl with Kh = round(K 2^e) 2^-e on a grid 2^-e shared by
+// the pair, e chosen so that 2 Vmax (sum|K+_j| + sum|K-_j|) 2^e <= 2^23
+// (Vmax = max |known| of the part).  For integer pair sums v, every product
+// Kh v and every partial sum of the Kh parts -- and Sh +- Dh -- is then a
+// multiple of 2^-e below 2^24 2^-e: exact in fp32.  Kl = fl32(K - Kh)
+// (|Kl| <= 2^-e-1) carries the rest with an fp32 rounding error below
+// ~1e-8 of the range for |known| < 2^17, so one FFMA2 per (tap, stencil,
+// column) on the FMA pipe replaces a DFMA plus the fp32 -> fp64 conversion
+// of its operand (F2F, a quarter-rate MIO instruction: 22 % of the fp64
+// kernel's stall samples).  Layout per (part, tap): the run layout of
+// StLayout<G, float> with (hi, lo) float pairs -- [K+_0 .. K+_{n-1}, K_mid,
+// (pad) | K-_0 .. K-_{n-1}, (pad)] -- after the part's [NK][16][8] fp64
+// table block of kpm.
+template <int G>
+__global__ void __launch_bounds__(128) split_stencil_kernel(PredictArgs a) {
+  using L = StLayout<G, double>;
+  using LR = StLayout<G, float>;
+  constexpr int NPAIR = L::NPAIR;
+  constexpr bool MID = L::MID;
+  constexpr int NJ = NPAIR + (MID ? 1 : 0);
+  const int n = (a.part1 - a.part0) * NJ;
+  const int kin = a.kmap[NKIND1 + AXIS_INTERIOR] * a.nkx + a.kmap[AXIS_INTERIOR];
+  if (a.kmap[AXIS_INTERIOR] < 0 || a.kmap[NKIND1 + AXIS_INTERIOR] < 0) return;
+  const double* kpm = reinterpret_cast<const double*>(a.kpm);
+  float2* spl = reinterpret_cast<float2*>(const_cast<double*>(kpm) + split_table_offset(a.S, a.NK));
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = a.part0 + i / NJ, j = i % NJ;
+    const double* w = kpm + ((size_t)s * a.NK + kin) * 16 * L::NSTP;
+    const bool pair = j < NPAIR;
+    const int ip = pair ? L::plus(j) : L::mid(), im = L::minus(j);
+    const double vmax = fmax(fabs(a.lohi[2 * s]), fabs(a.lohi[2 * s + 1]));
+    double bsum = 0.0;
+    for (int t = 0; t < 16; ++t) bsum += fabs(w[t * L::NSTP + ip]) + (pair ? fabs(w[t * L::NSTP + im]) : 0.0);
+    const double bound = 2.0 * vmax * bsum;
+    int e = 0;
+    if (bound > 0.0) {
+      int x;
+      frexp(bound, &x);                                    // bound < 2^x
+      e = 23 - x;
+    }
+    const double sc = ldexp(1.0, e), isc = ldexp(1.0, -e);
+    float2* dst = spl + (size_t)s * 16 * LR::NSTP;
+    for (int t = 0; t < 16; ++t) {
+      const double kp = w[t * L::NSTP + ip];
+      const double hp = rint(kp * sc) * isc;
+      dst[t * LR::NSTP + (pair ? LR::plus(j) : LR::mid())] = make_float2((float)hp, (float)(kp - hp));
+      if (pair) {
+        const double km = w[t * L::NSTP + im];
+        const double hm = rint(km * sc) * isc;
+        dst[t * LR::NSTP + LR::minus(j)] = make_float2((float)hm, (float)(km - hm));
+      }
+    }
+    if (j == 0)                                            // padding entries
+      for (int t = 0; t < 16; ++t)
+        for (int q = 0; q < LR::NSTP; ++q) {
+          const bool used = (q < NJ) || (q >= LR::NPP && q < LR::NPP + NPAIR);
+          if (!used) dst[t * LR::NSTP + q] = make_float2(0.f, 0.f);
+        }
+  }
+}
+
 // packed fp32x2 FMA (FFMA2) on 64-bit register pairs; a pair built from one
 // value twice becomes the instruction's broadcast operand
 __device__ __forceinline__ uint64_t f2pack(float x, float y) {
@@ -313,6 +380,10 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
   // tile (interior x kind), double-buffered by unit so staging the next
   // unit's needs no barrier beyond the unit-start one
   __shared__ __align__(16) Acc s_w[2][FT_WPARTS * 4 * 16 * NSTP_S];
+  // exact-split interior stencils ((hi, lo) float pairs, run layout) of the
+  // unit's parts for the fp64 symmetric rows (split_stencil_kernel)
+  constexpr bool SPLIT = F64 && VK_FT_SPLIT;
+  __shared__ __align__(16) uint64_t s_ws[SPLIT ? 2 : 1][SPLIT ? FT_WPARTS * 16 * LR::NSTP : 2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = a.H, W = a.W;
   const int64_t P = a.P;
@@ -382,6 +453,12 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           else src = (d - NPP < NPAIR) ? L::minus(d - NPP) : -1;
         }
         sw[i] = src >= 0 ? kpm[(((size_t)(s_first + pi) * a.NK + kind) * 16 + t) * NSTP + src] : (Acc)0;
+      }
+      if constexpr (SPLIT) {
+        const uint64_t* spl = reinterpret_cast<const uint64_t*>(a.kpm) + split_table_offset(a.S, a.NK) +
+                              (size_t)s_first * 16 * LR::NSTP;
+        uint64_t* sws = s_ws[uc & 1];
+        for (int i = tid; i < npu * 16 * LR::NSTP; i += FT_THREADS) sws[i] = spl[i];
       }
     }
     const uint32_t seq0 = load_seq;
@@ -728,28 +805,100 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           }
         });
       };
-      auto row_steps = [&](auto exact_c, auto sym_c) {
+      // exact-split symmetric row step (fp64 gate, integer planes): the same
+      // 10-tap x<->y symmetric form, each stencil as (hi, lo) fp32 parts on
+      // one FFMA2 against the broadcast pair sum (split_stencil_kernel: the
+      // hi sums are exact, the lo sums carry < ~1e-8 of the range), so no
+      // operand is converted to fp64 and no DFMA is issued
+      auto row_split = [&](int r, int gy) {
+        const uint64_t* wk = s_ws[uc & 1] + (size_t)(s - s_first) * 16 * LR::NSTP;
+        constexpr int NJ = NPAIR + (MID ? 1 : 0);
+        uint64_t aS[NJ > 0 ? NJ : 1][COLS], aD[NPAIR > 0 ? NPAIR : 1][COLS];
+        float selfA[COLS], selfB[COLS];
+        float Wv[4][COLS + 3];
+#pragma unroll
+        for (int c = 0; c < COLS; ++c) {
+#pragma unroll
+          for (int q = 0; q < NJ; ++q) aS[q][c] = 0;
+#pragma unroll
+          for (int q = 0; q < NPAIR; ++q) aD[q][c] = 0;
+        }
+#pragma unroll
+        for (int ph = 0; ph < 2; ++ph) {                   // 0: S = A + B, 1: D = A - B
+#pragma unroll
+          for (int oy = -1; oy <= 2; ++oy) {
+            float fa[COLS + 3], fb[COLS + 3];
+            load_rows(r + 1 + oy, fa, fb);
+            if (ph == 0 && oy == 0) {
+#pragma unroll
+              for (int c = 0; c < COLS; ++c) { selfA[c] = fa[c + 1]; selfB[c] = fb[c + 1]; }
+            }
+#pragma unroll
+            for (int i = 0; i < COLS + 3; ++i) Wv[oy + 1][i] = ph == 0 ? fa[i] + fb[i] : fa[i] - fb[i];
+          }
+#pragma unroll
+          for (int by = 0; by < 4; ++by) {
+#pragma unroll
+            for (int bx = 0; bx <= by; ++bx) {
+              const uint64_t* wt = wk + (by * 4 + bx) * LR::NSTP + (ph == 0 ? 0 : NPP);
+              constexpr int NW = NJ > NPAIR ? NJ : NPAIR;
+              uint64_t kw[NW > 0 ? NW : 1];
+#pragma unroll
+              for (int q = 0; q < (ph == 0 ? NJ : NPAIR); ++q) kw[q] = wt[q];
+#pragma unroll
+              for (int c = 0; c < COLS; ++c) {
+                const float v = bx == by ? Wv[by][c + bx] : Wv[by][c + bx] + Wv[bx][c + by];
+                const uint64_t vv = f2pack(v, v);
+                if (ph == 0) {
+#pragma unroll
+                  for (int q = 0; q < NJ; ++q) aS[q][c] = f2fma(kw[q], vv, aS[q][c]);
+                } else {
+#pragma unroll
+                  for (int q = 0; q < NPAIR; ++q) aD[q][c] = f2fma(kw[q], vv, aD[q][c]);
+                }
+              }
+            }
+          }
+        }
+        emit(gy, AXIS_INTERIOR, selfA, selfB, [&](int j, int c) -> float {
+          if (MID && j == NPAIR) return f2lo(aS[NPAIR][c]) + f2hi(aS[NPAIR][c]);
+          const int q = j < NPAIR ? j : G - 1 - j;
+          // hi parts: exact (common 2^-e grid of the pair); then one rounding
+          const float h = j < NPAIR ? f2lo(aS[q][c]) + f2lo(aD[q][c]) : f2lo(aS[q][c]) - f2lo(aD[q][c]);
+          const float l = j < NPAIR ? f2hi(aS[q][c]) + f2hi(aD[q][c]) : f2hi(aS[q][c]) - f2hi(aD[q][c]);
+          return h + l;
+        });
+      };
+      auto row_steps = [&](auto exact_c, auto sym_c, auto split_c) {
         constexpr bool SYM = decltype(sym_c)::value;
+        constexpr bool SPL = decltype(split_c)::value;
 #pragma unroll 1
         for (int rs = 0; rs < FT_TY / WY; ++rs) {
           const int r = wy + rs * WY;                      // tile row (warp-uniform)
           const int gy = y0 + r;
           if (gy >= H || !col_ok) continue;
           const int kyr = axis_kind(gy, H);
-          if (SYM && kyr == AXIS_INTERIOR) row_sym(r, gy);
+          if (SPL && kyr == AXIS_INTERIOR) row_split(r, gy);
+          else if (SYM && kyr == AXIS_INTERIOR) row_sym(r, gy);
           else row_general(exact_c, r, gy, kyr);
         }
       };
+      // exact split (row_split): integer planes with |known| < 2^17, and the
+      // final fp32 rounding (<= 1 ulp of |known| from the reference's) well
+      // inside 1e-6 of the range: max |known| <= 4 (hi - lo)
+      const float vmx = fmaxf(fabsf(lo), fabsf(hi));
+      const bool split_ok = SPLIT && sym_ok && vmx < 131072.f && vmx <= 4.f * (hi - lo);
       if constexpr (F64) {
-        if (sym_ok) row_steps(std::true_type{}, std::true_type{});
-        else if (sd_exact) row_steps(std::true_type{}, std::false_type{});
-        else row_steps(std::false_type{}, std::false_type{});
+        if (split_ok) row_steps(std::true_type{}, std::true_type{}, std::true_type{});
+        else if (sym_ok) row_steps(std::true_type{}, std::true_type{}, std::false_type{});
+        else if (sd_exact) row_steps(std::true_type{}, std::false_type{}, std::false_type{});
+        else row_steps(std::false_type{}, std::false_type{}, std::false_type{});
       } else {
         // fp32: pair sums round like every other fp32 operation (1e-3 gate)
         // (measured: C5 (G = 3) 2.757 -> 2.654 ms; C4 (G = 7) 0.628 -> 0.635 ms,
         // so the 16-tap form stays for G > 4)
-        if (VK_FT_SYM32 && G <= VK_FT_SYM32_MAXG) row_steps(std::false_type{}, std::true_type{});
-        else row_steps(std::false_type{}, std::false_type{});
+        if (VK_FT_SYM32 && G <= VK_FT_SYM32_MAXG) row_steps(std::false_type{}, std::true_type{}, std::false_type{});
+        else row_steps(std::false_type{}, std::false_type{}, std::false_type{});
       }
       // ---- border columns x in {0, W-2, W-1}: one thread per (row, column),
       // all G planes with the column's window kind, same mirror-pair form
@@ -910,6 +1059,10 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   const int n_units = 0;                   // unused by the balanced partition
   const int n_st = (a.part1 - a.part0) * a.NK * 16;
   if (n_st > 0) fast_stencil_kernel<G, Acc><<<(n_st + 255) / 256, 256, 0, st>>>(a);
+  if (std::is_same<Acc, double>::value && VK_FT_SPLIT && a.part1 > a.part0) {
+    const int n_sp = (a.part1 - a.part0) * (G / 2 + (G & 1));
+    split_stencil_kernel<G><<<(n_sp + 127) / 128, 128, 0, st>>>(a);
+  }
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(fl.tmap);
   if (a.var)
     predict_fast_kernel<G, Acc, true><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);

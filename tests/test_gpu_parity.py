@@ -251,11 +251,15 @@ def test_streaming_variance_all_fast_gaps(cuda, f, accum):
     assert np.allclose(var.cpu().numpy(), rvar, rtol=1e-7, atol=1e-9 * max(m.sill for m in rmodels))
 
 
-def test_integer_data_fast_sd_path_is_bit_identical(cuda):
-    """Integer-valued known planes take the fp32 S/D form in the fp64
-    streaming kernel (A +- B exact in fp32); one non-integer voxel switches the
-    gaps that read its plane to the general form (per-plane flags).  Voxels whose windows do not reach the
-    changed voxel must come out bit-identical from both."""
+def test_integer_data_paths_agree(cuda):
+    """Integer-valued known planes take the exact-split FFMA2 symmetric rows
+    in the fp64 streaming kernel (split_stencil_kernel: hi parts exact in
+    fp32, lo parts < ~1e-8 of the range); one non-integer voxel switches the
+    gaps that read its plane to the fp64 DFMA form (per-plane flags).  Gaps
+    that do not read the changed plane come out bit-identical; in the gap
+    that does, voxels whose windows miss the changed voxel agree between the
+    two forms to well inside the fp64 gate, and both forms match the oracle
+    at the gate."""
     torch = cuda
     from paper_2303_09523_b200 import VariogramModel, ZPartKriging
     from paper_2303_09523_b200.phantoms import known_slices, small_config
@@ -274,9 +278,45 @@ def test_integer_data_fast_sd_path_is_bit_identical(cuda):
         zk.finish()
         outs.append(o.cpu().numpy())
     a, b = outs
-    # gaps 0..6 never read plane 8; rows/cols away from (60, 120) in gap 7
+    rng = float(hi - lo)
+    # gaps 0..6 never read plane 8
     assert np.array_equal(a[:7 * cfg.factor + 1], b[:7 * cfg.factor + 1])
-    assert np.array_equal(a[:, :50], b[:, :50])
+    # gap 7 away from (60, 120): exact split (a) vs fp64 DFMA rows (b)
+    # (at most one f32 rounding step apart: the hi sums are exact and the lo
+    # sums' error is far below half an ulp)
+    d = np.abs(a[:, :50].astype(np.float64) - b[:, :50].astype(np.float64)).max()
+    assert d <= float(np.spacing(np.float32(max(abs(lo), abs(hi))))), d
+    om = O.Model("exponential", 1.0, 900.0, 12.0)
+    for data, out in ((ks, a), (ks2, b)):
+        g, msk = O.subpart_grid(data, 0, cfg.n_known - 1, cfg.factor)
+        ref, _ = O.fill_missing(g, msk, om)
+        assert np.abs(out.astype(np.float64) - ref).max() <= TOL64 * rng
+
+
+@pytest.mark.parametrize("offset,scale", [(0.0, 1.0), (20000.0, 1.0), (-3000.0, 1.0), (0.0, 30.0),
+                                          (0.0, -1.0), (0.0, 600.0)])
+def test_exact_split_rows_vs_oracle(cuda, offset, scale):
+    """The exact-split rows on integer planes against the oracle at the fp64
+    gate, and the data they must refuse (max |known| > 4 x range, or
+    |known| >= 2^17: the fp64 DFMA rows run instead) -- offsets and scales
+    of an integer phantom, gaps of every fast-path size."""
+    torch = cuda
+    from paper_2303_09523_b200 import VariogramModel, ZPartKriging
+    from paper_2303_09523_b200.phantoms import known_slices, small_config
+    for f in (2, 3, 5, 8, 9):
+        cfg = small_config("spine", 40, 96, 5, f, n_subparts=1, seed=5 + f)
+        ks = known_slices(cfg).astype(np.float64) * scale + offset
+        ks = ks.astype(np.float32)
+        assert np.array_equal(ks, np.rint(ks))
+        m = VariogramModel("exponential", 2.0, 700.0 * scale * scale, 9.0)
+        zk = ZPartKriging(cfg.n_known, cfg.height, cfg.width, cfg.factor, 1, fit=False)
+        out, _ = zk.run(torch.from_numpy(ks).cuda(), models=[m])
+        zk.finish()
+        g, msk = O.subpart_grid(ks, 0, cfg.n_known - 1, cfg.factor)
+        ref, _ = O.fill_missing(g, msk, O.Model("exponential", 2.0, 700.0 * scale * scale, 9.0))
+        rng = float(ks.max() - ks.min())
+        err = np.abs(out.cpu().numpy().astype(np.float64) - ref).max() / rng
+        assert err <= TOL64, (f, offset, scale, err)
 
 
 @pytest.mark.parametrize("bad", [np.inf, -np.inf, np.nan])
