@@ -129,6 +129,7 @@ __host__ __device__ constexpr int ft_minb(int G, bool f32 = false) {
 }
 constexpr int FT_WPARTS = 3;             // parts whose stencils a unit stages (host:
                                          // max_chunk = 2 * shortest part run + 1)
+constexpr int FT_MAXU = 32;              // gaps per unit (per-gap metadata staged in shared memory)
 
 template <typename Acc>
 struct AccVec;
@@ -384,6 +385,12 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
   // unit's parts for the fp64 symmetric rows (split_stencil_kernel)
   constexpr bool SPLIT = F64 && VK_FT_SPLIT;
   __shared__ __align__(16) uint64_t s_ws[SPLIT ? 2 : 1][SPLIT ? FT_WPARTS * 16 * LR::NSTP : 2];
+  // per-gap metadata of the unit (part, output plane, exact-S/D flag) and the
+  // clamp range of its parts, staged with the stencils: read per gap from
+  // global memory they were a chain of dependent loads (gap -> part -> range)
+  // on every warp's critical path (5 % of the kernel's stall samples)
+  __shared__ int s_gpart[2][FT_MAXU], s_gz[2][FT_MAXU], s_gflag[2][FT_MAXU];
+  __shared__ float2 s_plohi[2][FT_WPARTS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = a.H, W = a.W;
   const int64_t P = a.P;
@@ -460,6 +467,17 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
         uint64_t* sws = s_ws[uc & 1];
         for (int i = tid; i < npu * 16 * LR::NSTP; i += FT_THREADS) sws[i] = spl[i];
       }
+      if (ke - kb > FT_MAXU) __trap();
+      for (int i = tid; i < ke - kb; i += FT_THREADS) {
+        s_gpart[uc & 1][i] = a.gap_part[kb + i];
+        s_gz[uc & 1][i] = a.known_z[kb + i];
+        s_gflag[uc & 1][i] =
+            a.sd_inexact != nullptr && (a.sd_inexact[kb + i] | a.sd_inexact[kb + i + 1]) == 0;
+      }
+      if (tid >= FT_THREADS - FT_WPARTS && tid - (FT_THREADS - FT_WPARTS) < npu) {
+        const int pi = tid - (FT_THREADS - FT_WPARTS);
+        s_plohi[uc & 1][pi] = make_float2((float)a.lohi[2 * (s_first + pi)], (float)a.lohi[2 * (s_first + pi) + 1]);
+      }
     }
     const uint32_t seq0 = load_seq;
     const int n_planes = ke - kb + 1;
@@ -484,18 +502,19 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
     const bool xb0 = (gx == 0), xb1 = (gx + COLS > W - 2);  // group holds border columns
     for (int k = kb; k < ke; ++k) {
       const uint32_t sq_a = seq0 + (k - kb), sq_b = sq_a + 1;
-      const int s = a.gap_part[k];
+      const int s = s_gpart[uc & 1][k - kb];
       const Acc* wpart = kpm + (size_t)s * a.NK * 16 * NSTP;
       // the clamp commutes with the f32 rounding (lo, hi are f32 values and
       // rounding is monotone), so it is applied after the conversion
-      const float lo = (float)a.lohi[2 * s], hi = (float)a.lohi[2 * s + 1];
-      const int64_t zk = a.known_z[k];
+      const float2 plh = s_plohi[uc & 1][s - s_first];
+      const float lo = plh.x, hi = plh.y;
+      const int64_t zk = s_gz[uc & 1][k - kb];
       const bool copy_b = (k == n_gaps - 1);
       mbar_wait(&full[sq_a % FT_STAGES], (sq_a / FT_STAGES) & 1);
       mbar_wait(&full[sq_b % FT_STAGES], (sq_b / FT_STAGES) & 1);
       const float* bufA = ring + (sq_a % FT_STAGES) * FT_BUF_FLOATS;
       const float* bufB = ring + (sq_b % FT_STAGES) * FT_BUF_FLOATS;
-      const bool sd_exact = a.sd_inexact != nullptr && (a.sd_inexact[k] | a.sd_inexact[k + 1]) == 0;
+      const bool sd_exact = s_gflag[uc & 1][k - kb] != 0;
       // x<->y symmetric interior rows (fp64, integer planes): pair sums of S
       // and D are exact in fp32 when |known| < 2^22 (|S1 + S2| <= 2^24)
       const bool sym_ok = F64 && sd_exact && fmaxf(fabsf(lo), fabsf(hi)) < 4194304.f;
@@ -904,7 +923,12 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
       // all G planes with the column's window kind, same mirror-pair form
       if (nbc > 0) {
         const int rows_in = ty1 - y0;
-        for (int idx = tid; idx < rows_in * nbc; idx += FT_THREADS) {
+        // the (row, column) items fill at most three warps; which warps take
+        // them rotates with the gap (the ring lets warps drift by two gaps),
+        // so no warp is the CTA's slowest on every gap: with fixed warps a
+        // border tile's CTA ran ~1.25 x longer than an interior tile's
+        const int vt = (tid + FT_THREADS - 32 * ((3 * k) % FT_WARPS)) % FT_THREADS;
+        for (int idx = vt; idx < rows_in * nbc; idx += FT_THREADS) {
           const int ic = idx % nbc, r = idx / nbc;
           const int gy = y0 + r, xb = bcol[ic];
           const int kind = a.kmap[NKIND1 + axis_kind(gy, H)] * a.nkx + a.kmap[axis_kind(xb, W)];
@@ -1048,7 +1072,7 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   // gaps, so CTAs retire often) also sets the share; otherwise every resident
   // CTA gets an equal share of at least 4 gaps (the extra plane per run).
   const int64_t n_items = (int64_t)n_tiles * n_gaps;
-  int chunk = n_gaps;
+  int chunk = std::min(n_gaps, FT_MAXU);     // per-gap metadata of a unit is staged in shared memory
   if (a.max_chunk > 0) chunk = std::min(chunk, a.max_chunk);
   int64_t share = std::min(4, n_gaps);
   if (a.chunk > 0) {
