@@ -89,6 +89,7 @@ struct vk_plan {
   double *d_partial = nullptr, *d_models = nullptr, *d_lohi = nullptr, *d_weights = nullptr, *d_var = nullptr;
   double* d_kpm = nullptr;
   int* d_inexact = nullptr;           // stats pass: any known value not an integer below 2^23
+  int* d_work = nullptr;              // [S + 1][2] unit counters of the streaming launches (part s; S: serial)
   uint32_t* d_fxb = nullptr;           // fixed path tables
   float *d_fxc = nullptr, *d_fxq = nullptr;
   int max_chunk = 0;                  // fast path: a run of this many gaps spans <= 3 parts
@@ -323,6 +324,8 @@ int vk_plan_create(const vk_plan_desc* d, vk_plan** out) {
   VK_TRY(p->alloc(&p->d_var, (size_t)S * std::max(1, p->NP) * std::max(1, p->NK)));
   if (g.fast) VK_TRY(p->alloc(&p->d_kpm, kpm_elems(S, std::max(1, p->NK))));
   VK_TRY(p->alloc(&p->d_inexact, (size_t)g.K));
+  VK_TRY(p->alloc(&p->d_work, (size_t)(S + 1) * 2));
+  VK_TRY(cudaMemset(p->d_work, 0, (size_t)(S + 1) * 2 * sizeof(int)));
   if (g.fast && d->accum == VK_ACCUM_FIXED) {
     VK_TRY(p->alloc(&p->d_fxb, fxb_words(S, std::max(1, p->NK))));
     VK_TRY(p->alloc(&p->d_fxc, fxc_floats(S, std::max(1, p->NK))));
@@ -704,6 +707,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
   pa.fxc = p->d_fxc;
   pa.fxq = p->d_fxq;
   pa.num_sms = p->num_sms;
+  pa.work = p->d_work + 2 * S;
   if (fast) VK_CUDA(prepare_predict_fast(pa, &p->fast_launch));
   if (chained) {
     // ---- overlapped schedule: part s runs fit -> solve -> predict on chain
@@ -774,6 +778,7 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       if (chain_chunk > 0) p1.chunk = std::min(part_gaps, chain_chunk);
       p1.part0 = s;
       p1.part1 = s + 1;
+      p1.work = p->d_work + 2 * s;
       // the part's solve finished on its high-priority chain (a part reuses
       // a chain slot only when S > NCH, in launch order, so the event
       // recorded last on the slot covers this part)

@@ -205,6 +205,8 @@ struct PredictArgs {
   const int* sd_inexact;       // [K] per-plane flags from the stats pass: 0 -> every value of the
                                // plane is an integer below 2^23, so A +- B is exact in fp32
   int num_sms;
+  int* work = nullptr;         // fast path: {next unit, CTAs done} of this launch (zero between
+                               // launches; concurrent launches need their own pair)
 };
 // doubles the K+- table needs (fast path)
 // (the fp64 table [S][NK][16][8], then the exact-split interior stencils

@@ -24,6 +24,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <cstdio>
+#include <algorithm>
 #include <type_traits>
 #include "vk_kernels.h"
 #include "vk_tma.cuh"
@@ -352,6 +354,40 @@ __device__ __forceinline__ bool ft_evict_first(int k, int ke) {
   return VK_FT_EF_MODE != 0;
 }
 
+// Guided unit schedule of one launch.  Units are (tile, run of gaps); every
+// tile's gap range is cut into levels of decreasing unit length and the units
+// are handed out level by level (tile fastest) from a global counter: the
+// first gridDim.x units statically, the rest to whichever CTA asks next, so
+// all CTAs -- and both CTAs of an SM -- stay busy until the pool is empty and
+// the end-time spread is one short unit.  (A static equal split left CTAs
+// running 333-644 us of a 644 us launch on C4: whichever CTA of an SM the
+// warp schedulers favour finishes early and its sibling, alone on the SM, is
+// latency-bound; SMs were idle 8 % of the launch.)
+constexpr int FT_NLV = 6;
+struct FtSched {
+  int n_lv;
+  int len[FT_NLV];          // gaps per unit of the level
+  int off[FT_NLV + 1];      // the level's first gap within a tile's range (off[n_lv] = gaps)
+  int base[FT_NLV + 1];     // the level's first unit index (base[n_lv] = units in all)
+};
+__device__ __forceinline__ bool ft_unit(const FtSched& sc, int u, int n_tiles, int gap0, int& tile, int& kb,
+                                        int& ke) {
+  if (u >= sc.base[sc.n_lv]) return false;
+  int l = 0;
+  while (l + 1 < sc.n_lv && u >= sc.base[l + 1]) ++l;
+  const int idx = u - sc.base[l];
+  tile = idx % n_tiles;
+  kb = gap0 + sc.off[l] + (idx / n_tiles) * sc.len[l];
+  ke = min(kb + sc.len[l], gap0 + sc.off[l + 1]);
+  return true;
+}
+
+#ifdef VK_FT_DIAG
+// development diagnostic (tools/cta_times.py, variant builds only): per CTA
+// {smid, first tile, start, end} of the last streaming launch (globaltimer ns)
+__device__ unsigned long long g_cta_diag[4 * 1024];
+#endif
+
 // Streaming kernel.  No CTA-wide barrier inside a unit: each warp waits only
 // for the TMA of the two planes its gap reads and, when done with plane k,
 // releases it; the last warp to release a ring slot refills it with plane
@@ -361,7 +397,7 @@ __device__ __forceinline__ bool ft_evict_first(int k, int ke) {
 template <int G, typename Acc, bool VAR, int COLS = VK_FT_COLS>
 __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float>::value))
     predict_fast_kernel(const __grid_constant__ CUtensorMap tmap, PredictArgs a, int n_tiles_x,
-                        int n_tiles, int chunk, int n_units) {
+                        int n_tiles, const FtSched sch) {
   using L = StLayout<G, Acc>;
   constexpr int NPAIR = L::NPAIR;
   constexpr bool MID = L::MID;
@@ -391,9 +427,14 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
   // on every warp's critical path (5 % of the kernel's stall samples)
   __shared__ int s_gpart[2][FT_MAXU], s_gz[2][FT_MAXU], s_gflag[2][FT_MAXU];
   __shared__ float2 s_plohi[2][FT_WPARTS];
+  __shared__ int s_unit[2][4];                             // unit of iteration uc + 1: tile, kb, ke, valid
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int H = a.H, W = a.W;
   const int64_t P = a.P;
+#ifdef VK_FT_DIAG
+  unsigned long long diag_t0 = 0;
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(diag_t0));
+#endif
   if (tid == 0) {
     for (int i = 0; i < FT_STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -413,23 +454,20 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
   const int wx = warp % WX, wy = warp / WX;
   const int lc = lane + 32 * wx;                           // column group in the tile
 
-  // Balanced static partition: the (tile, gap) items in tile-major order are
-  // split into gridDim.x contiguous ranges whose sizes differ by at most one
-  // gap; a CTA walks its range as units of <= `chunk` gaps of one tile (the
-  // host caps `chunk` so a unit spans <= FT_WPARTS parts).  (Round-robin units
-  // of a fixed length left C4's serial launch with 7 units on some CTAs and 6
-  // on most: ~12 % tail.)
-  const int n_gaps_all = a.gap1 - a.gap0;
-  const int64_t n_items = (int64_t)n_tiles * n_gaps_all;
-  int64_t it = n_items * blockIdx.x / gridDim.x;
-  const int64_t it_end = n_items * (blockIdx.x + 1) / gridDim.x;
-  (void)n_units;
-  for (int uc = 0; it < it_end; ++uc) {
-    const int tile = (int)(it / n_gaps_all);
-    const int kb = a.gap0 + (int)(it - (int64_t)tile * n_gaps_all);
-    const int64_t room = it_end - it;
-    const int ke = min(min(a.gap1, kb + chunk), room < chunk ? kb + (int)room : a.gap1);
-    it += ke - kb;                                         // gaps [kb, ke) of `tile`
+  // Units come from the guided schedule (FtSched): the first is unit
+  // blockIdx.x; while a unit is staged, thread 0 claims the next one, so its
+  // first planes can be loaded as the current unit's ring slots drain.
+  int tile = 0, kb = 0, ke = 0, n_prev = 0;
+  bool have = ft_unit(sch, blockIdx.x, n_tiles, a.gap0, tile, kb, ke);
+  for (int uc = 0; have; ++uc) {
+    if (tid == 0) {
+      int t2 = 0, kb2 = 0, ke2 = 0;
+      const bool v = ft_unit(sch, (int)gridDim.x + atomicAdd(a.work, 1), n_tiles, a.gap0, t2, kb2, ke2);
+      s_unit[(uc + 1) & 1][0] = t2;
+      s_unit[(uc + 1) & 1][1] = kb2;
+      s_unit[(uc + 1) & 1][2] = ke2;
+      s_unit[(uc + 1) & 1][3] = v;
+    }
     const int tx = tile % n_tiles_x, ty = tile / n_tiles_x;
     const int x0 = tx * FT_TX, y0 = ty * FT_TY;
     const int ty1 = min(H, y0 + FT_TY), tx1 = min(W, x0 + FT_TX);
@@ -481,21 +519,25 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
     }
     const uint32_t seq0 = load_seq;
     const int n_planes = ke - kb + 1;
-    __syncthreads();                                       // ring free, stencils staged
-    if (tid == 0) {
+    // load `sq` of the CTA's plane sequence: plane kp of the tile at (xt, yt)
+    // (evict-first: the tiles must not displace the concurrent fits'
+    // instruction and stack lines from L2)
+    auto issue = [&](uint32_t sq, int xt, int yt, int kp) {
+      float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
       fence_proxy_async();
-      for (int i = 0; i < min(FT_STAGES, n_planes); ++i) {
-        const uint32_t sq = seq0 + i;
-        float* buf = ring + (sq % FT_STAGES) * FT_BUF_FLOATS;
-        mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
-        // evict-first: the tiles must not displace the concurrent fits'
-        // instruction and stack lines from L2
-        if (ft_evict_first(kb + i, ke))
-          tma_load_3d_ef(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i, l2_evict_first_policy());
-        else
-          tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], x0 - 4, y0 - 1, kb + i);
-      }
-    }
+      mbar_expect_tx(&full[sq % FT_STAGES], tile_bytes);
+      if (ft_evict_first(kp, kp))
+        tma_load_3d_ef(buf, &tmap, &full[sq % FT_STAGES], xt, yt, kp, l2_evict_first_policy());
+      else
+        tma_load_3d(buf, &tmap, &full[sq % FT_STAGES], xt, yt, kp);
+    };
+    __syncthreads();                                       // stencils staged, next unit known
+    // The ring runs across units: the last warp to release load q issues load
+    // q + FT_STAGES, of this unit or -- past its end -- of the next one.  What
+    // is left for the unit start are the loads whose slot was last used
+    // before the previous unit (all of them for the CTA's first unit).
+    if (tid == 0)
+      for (int i = 0; i < min(FT_STAGES - n_prev, n_planes); ++i) issue(seq0 + i, x0 - 4, y0 - 1, kb + i);
     load_seq += n_planes;
     const int gx = x0 + COLS * lc;
     const bool col_ok = gx < W;
@@ -966,31 +1008,66 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           }
         }
       }
-      // ---- release plane k; the last warp out refills its slot
+      // ---- release plane k (and the unit's last plane with its last gap);
+      // the last warp out refills the slot
       __syncwarp();
       if (lane == 0) {
-        const int slot = sq_a % FT_STAGES;
-        __threadfence_block();
-        const int c = atomicAdd(&released[slot], 1);
-        if (c == FT_WARPS - 1) {
+        for (uint32_t q = sq_a; q <= (k == ke - 1 ? sq_b : sq_a); ++q) {
+          const int slot = q % FT_STAGES;
           __threadfence_block();
-          released[slot] = 0;
-          const int kn = k + FT_STAGES;                    // plane of load sq_a + FT_STAGES
-          if (kn <= ke) {
-            fence_proxy_async();
-            mbar_expect_tx(&full[slot], tile_bytes);
-            if (ft_evict_first(kn, ke))
-              tma_load_3d_ef(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn, l2_evict_first_policy());
-            else
-              tma_load_3d(ring + slot * FT_BUF_FLOATS, &tmap, &full[slot], x0 - 4, y0 - 1, kn);
+          const int c = atomicAdd(&released[slot], 1);
+          if (c == FT_WARPS - 1) {
+            __threadfence_block();
+            released[slot] = 0;
+            const int j = (int)(q + FT_STAGES - seq0);     // plane of load q + FT_STAGES
+            if (j < n_planes) {
+              issue(q + FT_STAGES, x0 - 4, y0 - 1, kb + j);
+            } else if (s_unit[(uc + 1) & 1][3] && j - n_planes <= s_unit[(uc + 1) & 1][2] - s_unit[(uc + 1) & 1][1]) {
+              const int t2 = s_unit[(uc + 1) & 1][0];
+              issue(q + FT_STAGES, (t2 % n_tiles_x) * FT_TX - 4, (t2 / n_tiles_x) * FT_TY - 1,
+                    s_unit[(uc + 1) & 1][1] + j - n_planes);
+            }
           }
         }
       }
     }
+    n_prev = min(n_planes, FT_STAGES);
+    tile = s_unit[(uc + 1) & 1][0];
+    kb = s_unit[(uc + 1) & 1][1];
+    ke = s_unit[(uc + 1) & 1][2];
+    have = s_unit[(uc + 1) & 1][3] != 0;
   }
+  // the last CTA out rewinds the unit counter for the next launch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(a.work + 1, 1) == (int)gridDim.x - 1) {
+      a.work[0] = 0;
+      a.work[1] = 0;
+      __threadfence();
+    }
+  }
+#ifdef VK_FT_DIAG
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < 1024) {
+    unsigned long long t1;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta_diag[4 * blockIdx.x + 0] = smid;
+    g_cta_diag[4 * blockIdx.x + 1] = 0;
+    g_cta_diag[4 * blockIdx.x + 2] = diag_t0;
+    g_cta_diag[4 * blockIdx.x + 3] = t1;
+  }
+#endif
 }
 
 }  // namespace
+
+#ifdef VK_FT_DIAG
+extern "C" int vk_debug_cta_times(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_cta_diag, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024));
+}
+#endif
 
 cudaError_t launch_copy_known(const PredictArgs& a, cudaStream_t st) {
   const int64_t per = (a.P & 3) == 0 ? a.P / 4 : a.P;
@@ -1059,28 +1136,68 @@ cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Guided schedule of a launch over n_gaps gaps of every tile.  `fixed` (the
+// per-part chains: units of half a part's gaps) gives one level; otherwise the
+// unit length starts at `cap` (<= FT_WPARTS parts, <= FT_MAXU gaps, and no more
+// than a resident CTA's equal share) and halves over the levels, whose shares
+// of a tile's gaps are 55 / 20 / 13 / 12 % (VK_FT_GUIDE="55,20,13" overrides;
+// development only).
+static FtSched make_sched(int n_gaps, int n_tiles, int cap, bool fixed) {
+  FtSched sc{};
+  static const char* env = std::getenv("VK_FT_GUIDE");
+  int pct[3] = {55, 20, 13};
+  if (env) std::sscanf(env, "%d,%d,%d", &pct[0], &pct[1], &pct[2]);
+  int off = 0, base = 0, nl = 0;
+  const int levels = fixed ? 1 : 4;
+  for (int l = 0; l < levels && off < n_gaps; ++l) {
+    const int len = std::max(1, cap >> l);
+    const bool last = l == levels - 1 || len == 1;
+    int cnt = last ? (n_gaps - off + len - 1) / len : (int)((int64_t)pct[l] * n_gaps / 100 / len);
+    cnt = std::min(cnt, (n_gaps - off + len - 1) / len);
+    if (cnt <= 0) continue;
+    sc.len[nl] = len;
+    sc.off[nl] = off;
+    sc.base[nl] = base;
+    off = std::min(n_gaps, off + cnt * len);
+    base += cnt * n_tiles;
+    ++nl;
+    if (last) break;
+  }
+  if (off < n_gaps) {                      // remainder after skipped levels: single gaps
+    sc.len[nl] = 1;
+    sc.off[nl] = off;
+    sc.base[nl] = base;
+    base += (n_gaps - off) * n_tiles;
+    off = n_gaps;
+    ++nl;
+  }
+  sc.n_lv = nl;
+  sc.off[nl] = n_gaps;
+  sc.base[nl] = base;
+  return sc;
+}
+
 template <int G, typename Acc>
 static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
   const size_t smem = fast_smem(G, std::is_same<Acc, float>::value);
   const int ntx = (a.W + FT_TX - 1) / FT_TX, nty = (a.H + FT_TY - 1) / FT_TY;
   const int n_tiles = ntx * nty, n_gaps = a.gap1 - a.gap0;
   if (n_gaps <= 0) return cudaSuccess;
+  if (!a.work) return cudaErrorInvalidValue;
   const int resident = a.num_sms * fl.occ;
-  // a CTA's share of the (tile, gap) items is a contiguous range walked as
-  // units of <= chunk gaps of one tile; chunk <= max_chunk keeps a unit within
-  // FT_WPARTS parts.  An explicit a.chunk (per-part chains: half a part's
-  // gaps, so CTAs retire often) also sets the share; otherwise every resident
-  // CTA gets an equal share of at least 4 gaps (the extra plane per run).
+  // unit length: <= max_chunk keeps a unit within FT_WPARTS parts and FT_MAXU
+  // bounds the staged per-gap metadata.  An explicit a.chunk (per-part chains:
+  // half a part's gaps, so CTAs retire often) is taken as is; otherwise the
+  // first level's units are at most a resident CTA's equal share, at least 4
+  // gaps (the extra plane per run).
   const int64_t n_items = (int64_t)n_tiles * n_gaps;
-  int chunk = std::min(n_gaps, FT_MAXU);     // per-gap metadata of a unit is staged in shared memory
-  if (a.max_chunk > 0) chunk = std::min(chunk, a.max_chunk);
-  int64_t share = std::min(4, n_gaps);
-  if (a.chunk > 0) {
-    chunk = std::min(chunk, a.chunk);
-    share = chunk;
-  }
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(resident, (n_items + share - 1) / share));
-  const int n_units = 0;                   // unused by the balanced partition
+  int cap = std::min(n_gaps, FT_MAXU);
+  if (a.max_chunk > 0) cap = std::min(cap, a.max_chunk);
+  const bool fixed = a.chunk > 0;
+  if (fixed) cap = std::min(cap, a.chunk);
+  else cap = (int)std::max<int64_t>(std::min(4, n_gaps), std::min<int64_t>(cap, n_items / std::max(1, resident)));
+  const FtSched sc = make_sched(n_gaps, n_tiles, cap, fixed);
+  const int grid = std::max(1, std::min(resident, sc.base[sc.n_lv]));
   const int n_st = (a.part1 - a.part0) * a.NK * 16;
   if (n_st > 0) fast_stencil_kernel<G, Acc><<<(n_st + 255) / 256, 256, 0, st>>>(a);
   if (std::is_same<Acc, double>::value && VK_FT_SPLIT && a.part1 > a.part0) {
@@ -1089,9 +1206,9 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   }
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(fl.tmap);
   if (a.var)
-    predict_fast_kernel<G, Acc, true><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
+    predict_fast_kernel<G, Acc, true><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, sc);
   else
-    predict_fast_kernel<G, Acc, false><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, chunk, n_units);
+    predict_fast_kernel<G, Acc, false><<<grid, FT_THREADS, smem, st>>>(map, a, ntx, n_tiles, sc);
   return cudaGetLastError();
 }
 
