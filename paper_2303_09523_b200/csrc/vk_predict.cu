@@ -129,8 +129,9 @@ __host__ __device__ constexpr int ft_stages(int G, bool f32 = false) {
 __host__ __device__ constexpr int ft_minb(int G, bool f32 = false) {
   return (G <= 4 || (f32 && VK_FT_F32_MINB3)) ? 3 : VK_FT_MINB;
 }
-constexpr int FT_WPARTS = 3;             // parts whose stencils a unit stages (host:
-                                         // max_chunk = 2 * shortest part run + 1)
+constexpr int FT_WPARTS = 4;             // parts whose stencils a unit stages ...
+constexpr int FT_WSLOTS = 12;            // ... in (part, row kind) slots: four parts unless one tile
+                                         // holds all three border rows (H <= FT_TY: three parts)
 constexpr int FT_MAXU = 32;              // gaps per unit (per-gap metadata staged in shared memory)
 
 template <typename Acc>
@@ -191,6 +192,13 @@ __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
 #endif
 #ifndef VK_FT_SPLIT
 #define VK_FT_SPLIT 1                    // fp64 kernel: exact-split FFMA2 symmetric rows (integer planes)
+#endif
+#ifndef VK_FT_L2PF
+#define VK_FT_L2PF 0                     // planes ahead of a ring load to prefetch into L2 (0: none;
+                                         // C4: 1 or 2 planes ahead 0.627 vs 0.626 ms, no effect)
+#endif
+#ifndef VK_FT_ROWROT
+#define VK_FT_ROWROT 0                   // rows rotate over the warps with the gap (C4: 0.626 vs 0.619 ms)
 #endif
 #ifndef VK_FT_SYM32_MAXG
 #define VK_FT_SYM32_MAXG 4               // ... for gaps of up to this many missing planes
@@ -416,7 +424,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
   // mirror-pair stencils of the unit's parts (<= FT_WPARTS) x row kinds of the
   // tile (interior x kind), double-buffered by unit so staging the next
   // unit's needs no barrier beyond the unit-start one
-  __shared__ __align__(16) Acc s_w[2][FT_WPARTS * 4 * 16 * NSTP_S];
+  __shared__ __align__(16) Acc s_w[2][FT_WSLOTS * 16 * NSTP_S];
   // exact-split interior stencils ((hi, lo) float pairs, run layout) of the
   // unit's parts for the fp64 symmetric rows (split_stencil_kernel)
   constexpr bool SPLIT = F64 && VK_FT_SPLIT;
@@ -483,7 +491,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
     }
     const int s_first = a.gap_part[kb];
     const int npu = a.gap_part[ke - 1] - s_first + 1;       // <= FT_WPARTS (host caps chunk)
-    if (npu > FT_WPARTS) __trap();
+    if (npu > FT_WPARTS || npu * nky > FT_WSLOTS) __trap();
     Acc* sw = s_w[uc & 1];
     {
       const int per_k = 16 * NSTP_S, n = npu * nky * per_k;
@@ -615,7 +623,9 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           if constexpr (COLS == 4) {
             // border columns (x = 0, W-2, W-1) belong to the border pass:
             // predicated stores, no divergent branch (groups at x = 0 and
-            // x = W-4 hold them; W % 4 == 0 on the streaming path)
+            // x = W-4 hold them; W % 4 == 0 on the streaming path).  (A
+            // CTA-uniform branch to one plain store for tiles without border
+            // columns measured slower: C4 0.632 vs 0.619 ms.)
             st_cs_f4_if(dst, o, !xb0 && !xb1);
             st_cs_f1_if(dst + 1, o[1], xb0);
             st_cs_f2_if(dst + 2, o[2], o[3], xb0);
@@ -935,7 +945,10 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
         constexpr bool SPL = decltype(split_c)::value;
 #pragma unroll 1
         for (int rs = 0; rs < FT_TY / WY; ++rs) {
-          const int r = wy + rs * WY;                      // tile row (warp-uniform)
+          // tile row (warp-uniform); the rows rotate over the warps with the
+          // gap so a tile's border rows (general 16-tap form) are not always
+          // the same warps'
+          const int r = (VK_FT_ROWROT ? (wy + k) % WY : wy) + rs * WY;
           const int gy = y0 + r;
           if (gy >= H || !col_ok) continue;
           const int kyr = axis_kind(gy, H);
@@ -1022,6 +1035,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
             const int j = (int)(q + FT_STAGES - seq0);     // plane of load q + FT_STAGES
             if (j < n_planes) {
               issue(q + FT_STAGES, x0 - 4, y0 - 1, kb + j);
+              if (VK_FT_L2PF > 0 && j + VK_FT_L2PF < n_planes) tma_prefetch_3d(&tmap, x0 - 4, y0 - 1, kb + j + VK_FT_L2PF);
             } else if (s_unit[(uc + 1) & 1][3] && j - n_planes <= s_unit[(uc + 1) & 1][2] - s_unit[(uc + 1) & 1][1]) {
               const int t2 = s_unit[(uc + 1) & 1][0];
               issue(q + FT_STAGES, (t2 % n_tiles_x) * FT_TX - 4, (t2 / n_tiles_x) * FT_TY - 1,
@@ -1139,41 +1153,42 @@ cudaError_t fast_stencil_table(int G, const PredictArgs& a, cudaStream_t st) {
 // Guided schedule of a launch over n_gaps gaps of every tile.  `fixed` (the
 // per-part chains: units of half a part's gaps) gives one level; otherwise the
 // unit length starts at `cap` (<= FT_WPARTS parts, <= FT_MAXU gaps, and no more
-// than a resident CTA's equal share) and halves over the levels, whose shares
-// of a tile's gaps are 55 / 20 / 13 / 12 % (VK_FT_GUIDE="55,20,13" overrides;
-// development only).
+// than a resident CTA's equal share) and halves level by level down to single
+// gaps; the levels after the first take 15 / 9 / 6 / 4 % of a tile's gaps
+// (VK_FT_GUIDE="15,9,6,4" overrides; development only).  The single-gap tail
+// is what levels the CTAs' end times: C4 with 15/7/3/1-gap units 0.622 ms,
+// with 22/11/5/2-gap units (no single gaps) 0.647 ms.
 static FtSched make_sched(int n_gaps, int n_tiles, int cap, bool fixed) {
   FtSched sc{};
   static const char* env = std::getenv("VK_FT_GUIDE");
-  int pct[3] = {55, 20, 13};
-  if (env) std::sscanf(env, "%d,%d,%d", &pct[0], &pct[1], &pct[2]);
-  int off = 0, base = 0, nl = 0;
-  const int levels = fixed ? 1 : 4;
-  for (int l = 0; l < levels && off < n_gaps; ++l) {
-    const int len = std::max(1, cap >> l);
-    const bool last = l == levels - 1 || len == 1;
-    int cnt = last ? (n_gaps - off + len - 1) / len : (int)((int64_t)pct[l] * n_gaps / 100 / len);
-    cnt = std::min(cnt, (n_gaps - off + len - 1) / len);
-    if (cnt <= 0) continue;
-    sc.len[nl] = len;
-    sc.off[nl] = off;
-    sc.base[nl] = base;
-    off = std::min(n_gaps, off + cnt * len);
-    base += cnt * n_tiles;
-    ++nl;
-    if (last) break;
+  int pct[4] = {15, 9, 6, 4};
+  if (env) std::sscanf(env, "%d,%d,%d,%d", &pct[0], &pct[1], &pct[2], &pct[3]);
+  int len[FT_NLV] = {cap}, gaps[FT_NLV] = {n_gaps}, nl = 1;
+  if (!fixed) {
+    int tail = 0;
+    for (int l = 1; l <= 4 && (cap >> l) >= 1; ++l) {
+      const int ln = cap >> l;
+      len[nl] = ln;
+      gaps[nl] = (pct[l - 1] * n_gaps + 50 * ln) / (100 * ln) * ln;
+      tail += gaps[nl++];
+      if (ln == 1) break;
+    }
+    if (tail > n_gaps / 2) nl = 1;         // a handful of gaps: one level
+    else gaps[0] = n_gaps - tail;
   }
-  if (off < n_gaps) {                      // remainder after skipped levels: single gaps
-    sc.len[nl] = 1;
-    sc.off[nl] = off;
-    sc.base[nl] = base;
-    base += (n_gaps - off) * n_tiles;
-    off = n_gaps;
-    ++nl;
+  int off = 0, base = 0, k = 0;
+  for (int l = 0; l < nl; ++l) {
+    if (gaps[l] <= 0) continue;
+    sc.len[k] = len[l];
+    sc.off[k] = off;
+    sc.base[k] = base;
+    off += gaps[l];
+    base += (gaps[l] + len[l] - 1) / len[l] * n_tiles;
+    ++k;
   }
-  sc.n_lv = nl;
-  sc.off[nl] = n_gaps;
-  sc.base[nl] = base;
+  sc.n_lv = k;
+  sc.off[k] = n_gaps;
+  sc.base[k] = base;
   return sc;
 }
 
@@ -1192,10 +1207,22 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   // gaps (the extra plane per run).
   const int64_t n_items = (int64_t)n_tiles * n_gaps;
   int cap = std::min(n_gaps, FT_MAXU);
-  if (a.max_chunk > 0) cap = std::min(cap, a.max_chunk);
+  if (a.max_chunk > 0) {
+    // max_chunk = 2 * (shortest part run) + 1 bounds a unit to three parts;
+    // four parts fit the staged (part, row kind) slots when H > FT_TY
+    const int min_len = (a.max_chunk - 1) / 2, parts = a.H > FT_TY ? FT_WPARTS : FT_WPARTS - 1;
+    cap = std::min(cap, (parts - 1) * min_len + 1);
+  }
   const bool fixed = a.chunk > 0;
   if (fixed) cap = std::min(cap, a.chunk);
   else cap = (int)std::max<int64_t>(std::min(4, n_gaps), std::min<int64_t>(cap, n_items / std::max(1, resident)));
+  // Longer units are not better: warps drift apart inside a unit until the
+  // ring stops the leaders, and the unit-start barrier realigns them.  C4
+  // (G = 7): 6 / 10 / 15 / 22 gaps 0.626 / 0.620 / 0.629 / 0.650 ms; C5 (G = 3):
+  // 8 / 16 / 24 / 32 gaps 3.370 / 3.334 / 3.325 / 3.325 ms (a unit's extra
+  // plane weighs more at small G) -> about 70 interpolated planes per unit.
+  static const int env_cap = std::getenv("VK_FT_CAP") ? std::atoi(std::getenv("VK_FT_CAP")) : 0;   // development
+  if (!fixed) cap = std::min(cap, env_cap > 0 ? env_cap : std::max(4, 70 / G));
   const FtSched sc = make_sched(n_gaps, n_tiles, cap, fixed);
   const int grid = std::max(1, std::min(resident, sc.base[sc.n_lv]));
   const int n_st = (a.part1 - a.part0) * a.NK * 16;

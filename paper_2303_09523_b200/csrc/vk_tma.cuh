@@ -58,6 +58,13 @@ __device__ __forceinline__ void tma_load_3d_ef(void* dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// L2 prefetch of a tile (no shared-memory slot, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
 // order earlier generic-proxy accesses of shared memory before a following
 // async-proxy (TMA) write to it
 __device__ __forceinline__ void fence_proxy_async() {
