@@ -261,7 +261,7 @@ def _l2_desc(cfg):
 def _config(cfg, args, world):
     values = ("normalised to [0, 1] (non-integer floats: the 16-tap fp64 stencil path)"
               if args.values == "normalized" else
-              f"{cfg.quantise} grey levels as float32 (integer-valued: the x<->y symmetric fp64 rows)"
+              f"{cfg.quantise} grey levels as float32 (integer-valued: the exact-split / x<->y symmetric rows)"
               if cfg.quantise in ("u8", "u12") else "float32 in [0, 1]")
     return {"workload": f"{cfg.name} {cfg.height}x{cfg.width}, K={cfg.n_known} known slices/GPU, "
                         f"factor {cfg.factor}, {cfg.n_subparts} Z sub-parts/GPU",
@@ -381,17 +381,31 @@ def run_gpu(args, cfg, ks):
     # output conversion + 2*floor(G/2)/G mirror-pair DADDs; other data the
     # 16-tap form -- 16 DFMA + 2 DADD (S, D) + 1 + 2*floor(G/2)/G
     G = f - 1
-    sym = bool(np.all(ks == np.rint(ks)) and float(np.abs(ks).max()) < 2.0 ** 22)
+    vmax = float(np.abs(ks).max())
+    sym = bool(np.all(ks == np.rint(ks)) and vmax < 2.0 ** 22)
+    # exact-split FFMA2 rows: integer planes below 2^17 whose
+    # magnitude is within 4x the range -- no FP64-pipe work in interior rows;
+    # per warp row step (128 G voxels) 40 G FFMA2 at two FMA-pipe cycles and
+    # 104 + 4 (6 floor(G/2) + G mod 2) FADD
+    split = bool(sym and args.accum == "fp64" and vmax < 2.0 ** 17
+                 and vmax <= 4.0 * float(ks.max() - ks.min()))
     fp64_ops = (10 + 20 / G if sym else 18) + 1 + 2 * (G // 2) / G
     fp64_cap = 148 * 58 * sm_max * 1e6 / fp64_ops
+    fma_cycles = 2 * 40 * G + 104 + 4 * (6 * (G // 2) + G % 2)
+    fma_cap = 148 * 4 * sm_max * 1e6 * (128 * G) / fma_cycles
+    vps = vox_local / (pred_avg / 1e3)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": _profile_traffic(args.accum),
             "kernel": "predict_fast_kernel", "bytes_per_launch": alg_bytes,
             "launch_ms": pred_avg, "peak_kind": peak_kind,
-            "launch_ms_from": "serial schedule, CUDA events around the prediction launch",
-            "fp64_pipe_frac": (vox_local / (pred_avg / 1e3)) / fp64_cap
-            if args.accum == "fp64" else None,
-            "fp64_ops_per_voxel": round(fp64_ops, 3) if args.accum == "fp64" else None}
+            "launch_ms_from": "serial schedule, CUDA events around the streaming kernel's launch "
+                              "(the stencil-table kernels close the solve stage)",
+            "rows": ("exact-split FFMA2 symmetric rows" if split else
+                     "x<->y symmetric DFMA rows" if sym and args.accum == "fp64" else
+                     "16-tap DFMA rows" if args.accum == "fp64" else "fp32 FFMA2 rows"),
+            "fma_pipe_frac": vps / fma_cap if split else None,
+            "fp64_pipe_frac": vps / fp64_cap if args.accum == "fp64" and not split else None,
+            "fp64_ops_per_voxel": round(fp64_ops, 3) if args.accum == "fp64" and not split else None}
     stages = {k2: v / args.steps for k2, v in stage_acc.items()}
     stages["sum_serial"] = serial_ms
 

@@ -828,6 +828,12 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
     VK_CUDA(launch_solve(sa, st));
     VK_CUDA(launch_derive(sa, st));
     if (p->n_sys) kernels += 1 + (p->n_derived > 0);
+    // the stencil tables derive from the solved weights: they close the
+    // solve stage, so the prediction stage times the streaming kernel alone
+    if (fast && d.accum != VK_ACCUM_FIXED) {
+      VK_CUDA(launch_predict_fast_tables(pa, st));
+      pa.tables_done = 1;
+    }
     VK_CUDA(mark(5));
     if (fast) {
       VK_CUDA(launch_predict_fast_prepared(p->fast_launch, pa, st));

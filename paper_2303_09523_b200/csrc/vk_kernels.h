@@ -205,6 +205,8 @@ struct PredictArgs {
   const int* sd_inexact;       // [K] per-plane flags from the stats pass: 0 -> every value of the
                                // plane is an integer below 2^23, so A +- B is exact in fp32
   int num_sms;
+  int tables_done = 0;         // fast path: the stencil tables of [part0, part1) were already built
+                               // (launch_predict_fast_tables) -- the launch is the streaming kernel alone
   int* work = nullptr;         // fast path: {next unit, CTAs done} of this launch (zero between
                                // launches; concurrent launches need their own pair)
 };
@@ -222,6 +224,8 @@ struct FastLaunch {
 };
 cudaError_t prepare_predict_fast(const PredictArgs& a, FastLaunch* fl);
 cudaError_t launch_predict_fast_prepared(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st);
+// the stencil-table kernels of the streaming launch on their own (fp64 / fp32 accumulation)
+cudaError_t launch_predict_fast_tables(const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_copy_known(const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_predict_generic(const PredictArgs& a, cudaStream_t st);
 cudaError_t launch_predict_fast(const PredictArgs& a, cudaStream_t st);

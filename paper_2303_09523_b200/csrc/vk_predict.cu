@@ -1192,6 +1192,19 @@ static FtSched make_sched(int n_gaps, int n_tiles, int cap, bool fixed) {
   return sc;
 }
 
+// mirror-pair stencil table (and, fp64, the exact-split table) of parts
+// [a.part0, a.part1) from the solved weights
+template <int G, typename Acc>
+static cudaError_t launch_tables_t(const PredictArgs& a, cudaStream_t st) {
+  const int n_st = (a.part1 - a.part0) * a.NK * 16;
+  if (n_st > 0) fast_stencil_kernel<G, Acc><<<(n_st + 255) / 256, 256, 0, st>>>(a);
+  if (std::is_same<Acc, double>::value && VK_FT_SPLIT && a.part1 > a.part0) {
+    const int n_sp = (a.part1 - a.part0) * (G / 2 + (G & 1));
+    split_stencil_kernel<G><<<(n_sp + 127) / 128, 128, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
 template <int G, typename Acc>
 static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cudaStream_t st) {
   const size_t smem = fast_smem(G, std::is_same<Acc, float>::value);
@@ -1225,11 +1238,9 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   if (!fixed) cap = std::min(cap, env_cap > 0 ? env_cap : std::max(4, 70 / G));
   const FtSched sc = make_sched(n_gaps, n_tiles, cap, fixed);
   const int grid = std::max(1, std::min(resident, sc.base[sc.n_lv]));
-  const int n_st = (a.part1 - a.part0) * a.NK * 16;
-  if (n_st > 0) fast_stencil_kernel<G, Acc><<<(n_st + 255) / 256, 256, 0, st>>>(a);
-  if (std::is_same<Acc, double>::value && VK_FT_SPLIT && a.part1 > a.part0) {
-    const int n_sp = (a.part1 - a.part0) * (G / 2 + (G & 1));
-    split_stencil_kernel<G><<<(n_sp + 127) / 128, 128, 0, st>>>(a);
+  if (!a.tables_done) {
+    cudaError_t e = launch_tables_t<G, Acc>(a, st);
+    if (e != cudaSuccess) return e;
   }
   const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(fl.tmap);
   if (a.var)
@@ -1275,6 +1286,19 @@ cudaError_t launch_predict_fast_prepared(const FastLaunch& fl, const PredictArgs
   switch (a.G) {
 #define VK_CASE(g) \
   case g: return f32 ? launch_fast_t<g, float>(fl, a, st) : launch_fast_t<g, double>(fl, a, st);
+    VK_CASE(1) VK_CASE(2) VK_CASE(3) VK_CASE(4) VK_CASE(5) VK_CASE(6) VK_CASE(7) VK_CASE(8)
+#undef VK_CASE
+    default:
+      return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t launch_predict_fast_tables(const PredictArgs& a, cudaStream_t st) {
+  if (a.accum == 2) return cudaErrorNotSupported;          // the fixed path builds its own tables
+  const bool f32 = a.accum == 1;
+  switch (a.G) {
+#define VK_CASE(g) \
+  case g: return f32 ? launch_tables_t<g, float>(a, st) : launch_tables_t<g, double>(a, st);
     VK_CASE(1) VK_CASE(2) VK_CASE(3) VK_CASE(4) VK_CASE(5) VK_CASE(6) VK_CASE(7) VK_CASE(8)
 #undef VK_CASE
     default:
