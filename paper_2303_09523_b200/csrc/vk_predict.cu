@@ -197,6 +197,11 @@ __device__ __forceinline__ void st_cs_cols(float* p, const float* v) {
 #define VK_FT_L2PF 0                     // planes ahead of a ring load to prefetch into L2 (0: none;
                                          // C4: 1 or 2 planes ahead 0.627 vs 0.626 ms, no effect)
 #endif
+#ifndef VK_FT_MIDF64
+#define VK_FT_MIDF64 0                   // exact-split rows: the middle plane's stencil on the FP64 pipe
+                                         // (C4: 0.645 vs 0.601 ms -- the 40 F2F conversions per row
+                                         // step cost more than the 80 FMA-pipe cycles they free)
+#endif
 #ifndef VK_FT_ROWROT
 #define VK_FT_ROWROT 0                   // rows rotate over the warps with the gap (C4: 0.626 vs 0.619 ms)
 #endif
@@ -883,8 +888,16 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
       // operand is converted to fp64 and no DFMA is issued
       auto row_split = [&](int r, int gy) {
         const uint64_t* wk = s_ws[uc & 1] + (size_t)(s - s_first) * 16 * LR::NSTP;
-        constexpr int NJ = NPAIR + (MID ? 1 : 0);
+        // VK_FT_MIDF64 (off: measured slower): the middle plane (odd G) has
+        // no antisymmetric part; its stencil as DFMA on the otherwise idle
+        // FP64 pipe, from the fp64 table's symmetrised K_mid, with the pair
+        // sums converted once (F2F), takes 80 of a row step's ~740 FMA-pipe
+        // cycles off the binding pipe.
+        constexpr bool MF = MID && VK_FT_MIDF64;
+        constexpr int NJ = NPAIR + (MID && !MF ? 1 : 0);
+        const Acc* wkd = sw + (size_t)((s - s_first) * nky + 0) * 16 * NSTP_S + NPAIR;   // K_mid, interior rows
         uint64_t aS[NJ > 0 ? NJ : 1][COLS], aD[NPAIR > 0 ? NPAIR : 1][COLS];
+        double accC[MF ? COLS : 1];
         float selfA[COLS], selfB[COLS];
         float Wv[4][COLS + 3];
 #pragma unroll
@@ -893,6 +906,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           for (int q = 0; q < NJ; ++q) aS[q][c] = 0;
 #pragma unroll
           for (int q = 0; q < NPAIR; ++q) aD[q][c] = 0;
+          if (MF) accC[c] = 0.0;
         }
 #pragma unroll
         for (int ph = 0; ph < 2; ++ph) {                   // 0: S = A + B, 1: D = A - B
@@ -916,6 +930,8 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
               uint64_t kw[NW > 0 ? NW : 1];
 #pragma unroll
               for (int q = 0; q < (ph == 0 ? NJ : NPAIR); ++q) kw[q] = wt[q];
+              double kmid = 0.0;
+              if (MF && ph == 0) kmid = (double)wkd[(by * 4 + bx) * NSTP_S];
 #pragma unroll
               for (int c = 0; c < COLS; ++c) {
                 const float v = bx == by ? Wv[by][c + bx] : Wv[by][c + bx] + Wv[bx][c + by];
@@ -923,6 +939,7 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
                 if (ph == 0) {
 #pragma unroll
                   for (int q = 0; q < NJ; ++q) aS[q][c] = f2fma(kw[q], vv, aS[q][c]);
+                  if (MF) accC[c] = fma(kmid, (double)v, accC[c]);
                 } else {
 #pragma unroll
                   for (int q = 0; q < NPAIR; ++q) aD[q][c] = f2fma(kw[q], vv, aD[q][c]);
@@ -932,7 +949,10 @@ __global__ void __launch_bounds__(FT_THREADS, ft_minb(G, std::is_same<Acc, float
           }
         }
         emit(gy, AXIS_INTERIOR, selfA, selfB, [&](int j, int c) -> float {
-          if (MID && j == NPAIR) return f2lo(aS[NPAIR][c]) + f2hi(aS[NPAIR][c]);
+          if (MID && j == NPAIR) {
+            if constexpr (MF) return (float)accC[c];
+            else return f2lo(aS[NJ - 1][c]) + f2hi(aS[NJ - 1][c]);
+          }
           const int q = j < NPAIR ? j : G - 1 - j;
           // hi parts: exact (common 2^-e grid of the pair); then one rounding
           const float h = j < NPAIR ? f2lo(aS[q][c]) + f2lo(aD[q][c]) : f2lo(aS[q][c]) - f2lo(aD[q][c]);
