@@ -150,6 +150,8 @@ int vk_plan_get_info(const vk_plan* plan, vk_plan_info* info);
 
 /* Stage timing with CUDA events recorded on the execute stream:
  * stats, pairs, bins, fit, solve, predict (ms; 0 for skipped stages).
+ * On the serial schedule "solve" ends with the stencil-table kernels built
+ * from the solved weights and "predict" is the streaming kernel alone.
  * set_timing(ring): keep events of the last `ring` executes (0 disables).
  * stage_ms(back): times of the execute `back` calls ago (0 = latest);
  * synchronises on that execute's last event. */
