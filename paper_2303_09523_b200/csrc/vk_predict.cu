@@ -1239,16 +1239,17 @@ static cudaError_t launch_fast_t(const FastLaunch& fl, const PredictArgs& a, cud
   // first level's units are at most a resident CTA's equal share, at least 4
   // gaps (the extra plane per run).
   const int64_t n_items = (int64_t)n_tiles * n_gaps;
-  int cap = std::min(n_gaps, FT_MAXU);
+  int hard = std::min(n_gaps, FT_MAXU);                    // what the staged tables hold
   if (a.max_chunk > 0) {
     // max_chunk = 2 * (shortest part run) + 1 bounds a unit to three parts;
     // four parts fit the staged (part, row kind) slots when H > FT_TY
     const int min_len = (a.max_chunk - 1) / 2, parts = a.H > FT_TY ? FT_WPARTS : FT_WPARTS - 1;
-    cap = std::min(cap, (parts - 1) * min_len + 1);
+    hard = std::min(hard, (parts - 1) * min_len + 1);
   }
   const bool fixed = a.chunk > 0;
+  int cap = hard;
   if (fixed) cap = std::min(cap, a.chunk);
-  else cap = (int)std::max<int64_t>(std::min(4, n_gaps), std::min<int64_t>(cap, n_items / std::max(1, resident)));
+  else cap = (int)std::min<int64_t>(hard, std::max<int64_t>(std::min(4, n_gaps), n_items / std::max(1, resident)));
   // Longer units are not better: warps drift apart inside a unit until the
   // ring stops the leaders, and the unit-start barrier realigns them.  C4
   // (G = 7): 6 / 10 / 15 / 22 gaps 0.626 / 0.620 / 0.629 / 0.650 ms; C5 (G = 3):

@@ -33,6 +33,8 @@ def _planes(shape, seed, integer):
     ((256, 128, 384), 8, 32, "fp64", False),    # 16-tap DFMA rows
     ((128, 96, 256), 4, 16, "fp32", False),     # G = 3: three CTAs per SM, 3-deep ring
     ((40, 70, 132), 2, 5, "fp64", True),        # G = 1, ragged tile edges, uneven parts
+    ((5, 24, 64), 4, 4, "fp64", True),          # one gap per part, all border rows in one tile
+    ((9, 30, 64), 8, 8, "fp64", False),         # same with G = 7
 ])
 def test_guided_schedule_complete_deterministic_and_equal_to_chains(cuda, shape, factor, parts, accum, integer):
     torch = cuda
