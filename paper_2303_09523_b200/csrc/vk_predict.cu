@@ -6,6 +6,10 @@
 //                  streamed into a 4-deep shared-memory ring by TMA
 //                  (cp.async.bulk.tensor, OOB zero fill supplies the volume
 //                  halo) so each known plane is read from HBM once per run.
+//                  Units come from a guided dynamic schedule (FtSched: unit
+//                  lengths halving from ~70 interpolated planes to single
+//                  gaps, claimed from a global counter) and the ring runs
+//                  across units, so all CTAs end within one short unit.
 //                  The G missing planes of a gap come in z-mirror pairs
 //                  (j, G-1-j) whose interior stencils are mirror images, so
 //                  each pair is computed from S = A+B and D = A-B (exact in
