@@ -127,8 +127,11 @@ constexpr int FT_BUF_FLOATS = ((FT_SX * FT_SY * 4 + 127) / 128) * 128 / 4;
 #ifndef VK_FT_F32_MINB3
 #define VK_FT_F32_MINB3 0                // fp32 kernel: three CTAs per SM at every G
 #endif
+#ifndef VK_FT_NSTAGE
+#define VK_FT_NSTAGE 4                   // ring depth at two CTAs per SM
+#endif
 __host__ __device__ constexpr int ft_stages(int G, bool f32 = false) {
-  return (G <= 4 || (f32 && VK_FT_F32_MINB3)) ? 3 : 4;
+  return (G <= 4 || (f32 && VK_FT_F32_MINB3)) ? 3 : VK_FT_NSTAGE;
 }
 __host__ __device__ constexpr int ft_minb(int G, bool f32 = false) {
   return (G <= 4 || (f32 && VK_FT_F32_MINB3)) ? 3 : VK_FT_MINB;
