@@ -771,10 +771,17 @@ int vk_plan_execute(vk_plan* p, const float* known, const double* models, float*
       // units of half a part's gaps: streaming CTAs retire often enough that
       // a late part's solve finds a free slot soon (they hold all of an SM's
       // registers), at the cost of one extra known-plane load per unit
-      // (C4: 8-gap units 1.351 ms, 4-gap 1.329 ms, 2-gap 1.342 ms)
+      // (C4: 8-gap units 1.351 ms, 4-gap 1.329 ms, 2-gap 1.342 ms with the
+      // round-1 fit).  With the exact fit the step ends with the slowest
+      // part's prediction alone on the GPU, where shorter units spread its
+      // gaps over more CTAs: a quarter of the part's gaps when a gap is seven
+      // or more interpolated planes (C4: 2 / 3 / 4 / 8-gap units 2.051 / 2.062
+      // / 2.069 / 2.097 ms); at smaller G the unit's extra known plane weighs
+      // more and the step is bandwidth-bound (C5), so half a part stays
       static const int chain_chunk = std::getenv("VK_CHAIN_CHUNK") ? std::atoi(std::getenv("VK_CHAIN_CHUNK")) : 0;
       const int part_gaps = p1.gap1 - p1.gap0;
-      p1.chunk = part_gaps > 4 ? (part_gaps + 1) / 2 : part_gaps;
+      const int div = g.G >= 7 ? 4 : 2;
+      p1.chunk = part_gaps > 4 ? std::max(2, (part_gaps + div - 1) / div) : part_gaps;
       if (chain_chunk > 0) p1.chunk = std::min(part_gaps, chain_chunk);
       p1.part0 = s;
       p1.part1 = s + 1;
