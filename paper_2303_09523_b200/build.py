@@ -25,7 +25,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 UNITS = {
     "vk_api.cu": [],
-    "vk_variogram.cu": [],
+    # ptxas -O1: the fit kernel is a 31 k-instruction serial FP64 chain that
+    # waits on instruction fetches a fifth of the time; the default level's
+    # scheduling buys it nothing (C4 fit 1.479 -> 1.449 ms, C2 1.058 -> 1.047;
+    # the unit's bandwidth kernels measure the same; bits unchanged -- FMA
+    # contraction is decided before ptxas)
+    "vk_variogram.cu": ["-Xptxas", "-O1"],
     "vk_npstats.cu": [],
     "vk_solve.cu": [],
     "vk_predict.cu": [],
